@@ -1,0 +1,172 @@
+/*
+ * attnpred.h — C-ABI of libattnpred.so, the B200 (sm_100a) implementation of
+ * AttentionPredictor's decode-time critical-token path.
+ *
+ * The reference (Python package `attncast`, /root/reference/pkg/src/attncast)
+ * has no FFI of its own: its boundary is the Python module API of
+ * attncast.compress / attncast.predictor / attncast.selector.  Each entry point
+ * below names the reference function it replaces (file:line); the Python
+ * package `paper_2502_04077_b200` binds these through ctypes and re-exposes
+ * the reference names, signatures and exceptions (INTEGRATION.md shows the
+ * binding a maintainer would add on the reference side).
+ *
+ * Conventions
+ *  - Every pointer argument is DEVICE memory unless marked [host].
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t, may be NULL),
+ *    does not allocate, does not synchronise, and is CUDA-graph capturable
+ *    (ap_set_weights included: it issues a memcpy node + one kernel).
+ *  - Return value: synchronous argument/shape check (AP_OK or AP_E*).
+ *  - Data-dependent failures (non-finite input, out-of-range block id) are
+ *    written by the kernels into a caller-provided device status word
+ *    (`int32_t* status`, 0 = ok, else an AP_E* code) which the host inspects
+ *    when it next synchronises.
+ */
+#ifndef ATTNPRED_H
+#define ATTNPRED_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes → Python exceptions (paper_2502_04077_b200/_lib.py) */
+#define AP_OK        0
+#define AP_EPARAM    1  /* ParameterError */
+#define AP_ECONFIG   2  /* ConfigError    */
+#define AP_ESTATE    3  /* StateError     */
+#define AP_ENUMERIC  4  /* NumericError   */
+#define AP_ECUDA     5  /* DeviceError    */
+
+/* element types */
+#define AP_F32   0
+#define AP_F64   1
+#define AP_BF16  2
+
+/* predictor arithmetic (DESIGN.md §Predictor precision) */
+#define AP_PREC_FP32    0  /* SIMT fp32 FMA, no tensor cores (tolerance rtol 1e-3) */
+#define AP_PREC_BF16X3  1  /* tcgen05 bf16 hi/lo split, 3 MMAs per tap (rtol 1e-3) */
+#define AP_PREC_BF16    2  /* tcgen05 single bf16 MMA per tap (rtol 2e-2) */
+
+#define AP_PARAM_COUNT 4833 /* predictor.py:36-40 */
+
+int ap_version(void);
+/* [host] human-readable text of the last synchronous error in this thread */
+const char* ap_last_error(void);
+/* [host] number of SMs of the current device (grid sizing in callers) */
+int ap_device_sm_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Predictor weights — predictor.py:45-98 (PredictorWeights), APW1 order
+ * w1(16,1,3,3) b1(16) w2(32,16,3,3) b2(32) w3(32) b3().
+ * Installs one weight set (4833 fp32, device) for every later predictor call
+ * ("one weight set serves every (layer, head)", predictor.py:10-13;
+ * "weights immutable during inference").  Copies into constant
+ * memory and packs the bf16 hi/lo tcgen05 B-operand tiles.
+ * ------------------------------------------------------------------------- */
+int ap_set_weights(const float* weights4833, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * compress.max_pool — compress.py:28-40, batched over rows.
+ * rows: n_rows rows of t elements (in_dtype), row i at rows + i*row_stride
+ * (elements).  out: ceil(t/b) values per row (out_dtype), stride out_stride.
+ * Zero-pads the tail block, per-block max; NaN propagates like numpy.
+ * ------------------------------------------------------------------------- */
+int ap_max_pool(const void* rows, int in_dtype, int64_t n_rows, int64_t row_stride, int64_t t,
+                int32_t b, void* out, int out_dtype, int64_t out_stride, void* stream);
+
+/* compress.expand_indices — compress.py:43-57.  Writes the token ids of the
+ * given blocks (each block's range clipped to t) in block order, and the
+ * count into *n_tokens.  Out-of-range block → *status = AP_EPARAM. */
+int ap_expand_indices(const int32_t* blocks, int32_t n_blocks, int32_t b, int64_t t,
+                      int64_t* tokens, int32_t* n_tokens, int32_t* status, void* stream);
+
+/* selector.topk — selector.py:73-81, batched.  For each of n_rows rows of n
+ * values (AP_F32 or AP_F64): the k largest, ties to the lower index, -0.0 ==
+ * +0.0; ids written in ASCENDING order (set semantics), count in out_count. */
+int ap_topk(const void* values, int dtype, int64_t n_rows, int64_t row_stride, int32_t n, int32_t k,
+            int32_t* out_ids, int64_t out_stride, int32_t* out_count, int32_t* status, void* stream);
+
+/* predictor.forward — predictor.py:185-216 on explicit H x W grids (fp32,
+ * row-major, grid i at grids + i*grid_stride).  out: W fp32 per grid.
+ * rscratch: n_grids*H*W fp32 workspace (per-row contributions). */
+int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W, int64_t grid_stride,
+                       float* out, int64_t out_stride, float* rscratch, int precision,
+                       int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Batched, device-resident selector: one map per (sequence, layer, q-head).
+ * Replaces selector.init_state / selector.step (selector.py:61-70,91-154) for
+ * n_maps maps at once.  All buffers are caller-owned device memory.
+ * ------------------------------------------------------------------------- */
+typedef struct ap_map_state {
+    int64_t n_pushed;  /* rows pushed into the ring so far (prefill + decode) */
+    int64_t r_pushed;  /* n_pushed when the r-map was last brought up to date; -1 = never */
+    int64_t row_len;   /* t of the newest pushed row */
+    int64_t counter;   /* selector step counter (selector.py:112,126,153) */
+    int64_t mid_clip;  /* t used to clip the current middle blocks (selector.py:145) */
+    int32_t width;     /* W of the newest row = ceil(row_len / b) */
+    int32_t r_width;   /* W when the r-map was last brought up to date */
+    int32_t n_mid;     /* number of middle blocks currently selected */
+    int32_t pad_;
+} ap_map_state;
+
+typedef struct ap_selector {
+    int32_t n_maps;
+    int32_t history;          /* H   (SelectorConfig.history)            */
+    int32_t block;            /* b   (SelectorConfig.block_size)         */
+    int32_t w_max;            /* ring / r-map row pitch in blocks       */
+    int32_t k_mid;            /* SelectorConfig.middle_blocks           */
+    int32_t sink;             /* SelectorConfig.sink_tokens             */
+    int32_t local;            /* SelectorConfig.local_tokens            */
+    int32_t calib_period;     /* M   (SelectorConfig.calibration_period) */
+    int32_t update_interval;  /* SelectorConfig.update_interval         */
+    int32_t pad_;
+    float* ring;              /* [n_maps][H][w_max] compressed history rows        */
+    float* rmap;              /* [n_maps][H][w_max] per-row predictor contributions */
+    int32_t* slot_width;      /* [n_maps][H] width of the row stored in each slot   */
+    ap_map_state* state;      /* [n_maps]                                           */
+    float* scores;            /* [n_maps][w_max] last forecast (selector.py:133)    */
+    int32_t* mid_blocks;      /* [n_maps][k_mid] middle block ids, ascending        */
+    uint32_t* mid_mask;       /* [n_maps][ceil(w_max/32)] bitmask of middle blocks  */
+    int32_t* status;          /* [1] device status word                             */
+} ap_selector;
+
+/* Zero the state of every map (selector.init_state with no prefill rows). */
+int ap_sel_reset(const ap_selector* s, void* stream);
+
+/* Compress one t-length attention row per map and append it to the history
+ * ring (selector.py:112-120).  rows: map i's row at rows + i*row_stride.
+ * t: row length, the same for all maps (host scalar).
+ * mode 0 = prefill push (selector.init_state, selector.py:61-70: no masking,
+ *          counter untouched);
+ * mode 1 = decode push: the row is the DENSE row; on calibration steps
+ *          (counter % M == 0) it is stored as is, otherwise it is first masked
+ *          to the previous selection (evaluation.py:109-112 observed row:
+ *          dense values at sink ∪ local ∪ middle, zeros elsewhere);
+ * mode 2 = decode push of an already-observed row (stored as given). */
+int ap_sel_push_rows(const ap_selector* s, const void* rows, int dtype, int64_t row_stride, int64_t t,
+                     int mode, void* stream);
+
+/* Append already-compressed rows (width W each, fp32) — used by the fused
+ * attention kernels' outputs and by tests. Same counter semantics as mode 2
+ * (or mode 0 when prefill != 0). */
+int ap_sel_push_compressed(const ap_selector* s, const float* comp, int64_t comp_stride, int64_t t,
+                           int prefill, void* stream);
+
+/* One selector.step tail (selector.py:122-154) for every map: when
+ * counter % update_interval == 0 and k_mid > 0, bring the r-map up to date
+ * (incrementally: only the history rows whose 3x3 receptive field changed),
+ * forecast the next compressed row, mask the sink/local covering blocks
+ * (selector.py:134-142), take top-min(K, available) (selector.py:143-145)
+ * into mid_blocks / mid_mask; then counter += 1. */
+int ap_sel_step(const ap_selector* s, int precision, void* stream);
+
+/* Number of persistent CTAs the predictor kernels use (for reporting). */
+int ap_sel_grid_ctas(int precision);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ATTNPRED_H */

@@ -1,0 +1,140 @@
+"""ctypes binding of libattnpred.so (include/attnpred.h).
+
+This is the only way the package reaches compute: there is no CPU fallback.
+If the in-tree library is missing, importing the compute modules raises
+:class:`NativeLibraryMissing` (build it with ``python -c "import
+__graft_entry__ as g; g.build()"``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from . import errors as E
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libattnpred.so"
+
+AP_OK, AP_EPARAM, AP_ECONFIG, AP_ESTATE, AP_ENUMERIC, AP_ECUDA = range(6)
+AP_F32, AP_F64, AP_BF16 = 0, 1, 2
+PREC = {"fp32": 0, "bf16x3": 1, "bf16": 2}
+
+_ERR = {
+    AP_EPARAM: E.ParameterError,
+    AP_ECONFIG: E.ConfigError,
+    AP_ESTATE: E.StateError,
+    AP_ENUMERIC: E.NumericError,
+    AP_ECUDA: E.DeviceError,
+}
+
+
+class NativeLibraryMissing(ImportError):
+    pass
+
+
+class MapState(ctypes.Structure):
+    _fields_ = [
+        ("n_pushed", ctypes.c_int64), ("r_pushed", ctypes.c_int64), ("row_len", ctypes.c_int64),
+        ("counter", ctypes.c_int64), ("mid_clip", ctypes.c_int64), ("width", ctypes.c_int32),
+        ("r_width", ctypes.c_int32), ("n_mid", ctypes.c_int32), ("pad_", ctypes.c_int32),
+    ]
+
+
+class Selector(ctypes.Structure):
+    _fields_ = [
+        ("n_maps", ctypes.c_int32), ("history", ctypes.c_int32), ("block", ctypes.c_int32),
+        ("w_max", ctypes.c_int32), ("k_mid", ctypes.c_int32), ("sink", ctypes.c_int32),
+        ("local", ctypes.c_int32), ("calib_period", ctypes.c_int32), ("update_interval", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+        ("ring", ctypes.c_void_p), ("rmap", ctypes.c_void_p), ("slot_width", ctypes.c_void_p),
+        ("state", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("mid_blocks", ctypes.c_void_p),
+        ("mid_mask", ctypes.c_void_p), ("status", ctypes.c_void_p),
+    ]
+
+
+MAP_STATE_BYTES = ctypes.sizeof(MapState)  # 56
+
+_P = ctypes.c_void_p
+_I32, _I64 = ctypes.c_int32, ctypes.c_int64
+
+# symbol -> (restype, argtypes); the table is also what tests check the .so exports
+SIGNATURES = {
+    "ap_version": (ctypes.c_int, []),
+    "ap_last_error": (ctypes.c_char_p, []),
+    "ap_device_sm_count": (ctypes.c_int, []),
+    "ap_set_weights": (ctypes.c_int, [_P, _P]),
+    "ap_max_pool": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I64, _I32, _P, ctypes.c_int, _I64, _P]),
+    "ap_expand_indices": (ctypes.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _P]),
+    "ap_topk": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I32, _I32, _P, _I64, _P, _P, _P]),
+    "ap_predict_forward": (ctypes.c_int, [_P, _I32, _I32, _I32, _I64, _P, _I64, _P, ctypes.c_int, _P, _P]),
+    "ap_sel_reset": (ctypes.c_int, [ctypes.POINTER(Selector), _P]),
+    "ap_sel_push_rows": (ctypes.c_int, [ctypes.POINTER(Selector), _P, ctypes.c_int, _I64, _I64, ctypes.c_int, _P]),
+    "ap_sel_push_compressed": (ctypes.c_int, [ctypes.POINTER(Selector), _P, _I64, _I64, ctypes.c_int, _P]),
+    "ap_sel_step": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.c_int, _P]),
+    "ap_sel_grid_ctas": (ctypes.c_int, [ctypes.c_int]),
+}
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the native library; raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("ATTNPRED_LIB", LIB_PATH))
+    if not path.exists():
+        raise NativeLibraryMissing(
+            f"{path} not found: the CUDA path is the only implementation; build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(str(path))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            continue  # optional symbols are checked by callers / tests
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def fn(name: str):
+    lib = load()
+    f = getattr(lib, name, None)
+    if f is None:
+        raise NativeLibraryMissing(f"{LIB_PATH.name} does not export {name}")
+    if name in SIGNATURES:
+        f.restype, f.argtypes = SIGNATURES[name]
+    return f
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a synchronous AP_E* status to the reference exception classes."""
+    if rc == AP_OK:
+        return
+    msg = load().ap_last_error()
+    text = msg.decode() if msg else what
+    raise _ERR.get(rc, E.DeviceError)(text or f"{what} failed with status {rc}")
+
+
+def raise_device_status(code: int, what: str) -> None:
+    """Map a device status word (set by kernels) to an exception."""
+    if code == 0:
+        return
+    msgs = {
+        AP_ENUMERIC: f"{what}: non-finite values encountered",
+        AP_EPARAM: f"{what}: index out of range",
+    }
+    raise _ERR.get(code, E.DeviceError)(msgs.get(code, f"{what}: device status {code}"))
+
+
+def ptr(t) -> int:
+    """Raw device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)

@@ -1,0 +1,134 @@
+"""Device-resident selector over many maps at once.
+
+One *map* is one (sequence, layer, q-head) attention history.  The
+``BatchedSelector`` owns, in HBM, every map's compressed-history ring
+(H x w_max fp32), its per-row forecaster contributions (the r-map, same
+shape), per-slot widths, step state, last forecast and middle-block
+selection; a decode step is three stream-ordered launches with no host
+round trip (push → predict/top-k → counter), so whole decode steps capture
+into one CUDA graph.
+
+Semantics per map are those of ``attncast.selector.init_state`` / ``step``
+(selector.py:61-154) and of the evaluation loop's observed-row feedback
+(evaluation.py:90-115); see ``paper_2502_04077_b200.selector`` for the
+per-head reference-compatible wrapper.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .errors import ConfigError, ParameterError
+
+PUSH_PREFILL, PUSH_DENSE, PUSH_OBSERVED = 0, 1, 2
+
+_STATE_DTYPE = np.dtype([
+    ("n_pushed", "<i8"), ("r_pushed", "<i8"), ("row_len", "<i8"), ("counter", "<i8"), ("mid_clip", "<i8"),
+    ("width", "<i4"), ("r_width", "<i4"), ("n_mid", "<i4"), ("pad_", "<i4"),
+])
+assert _STATE_DTYPE.itemsize == _lib.MAP_STATE_BYTES
+
+
+class BatchedSelector:
+    """n_maps independent selectors sharing one forecaster weight set.
+
+    cfg: a SelectorConfig-like object (budget, block_size, history,
+    calibration_period, sink_tokens, local_tokens, update_interval).
+    w_max: the largest compressed width any map will reach (ceil(t_max/b)).
+    """
+
+    def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "bf16x3", device=None):
+        cfg.validate()
+        if n_maps < 1 or w_max < 1:
+            raise ParameterError("n_maps and w_max must be >= 1")
+        if precision not in _lib.PREC:
+            raise ParameterError(f"unknown precision {precision!r}")
+        torch = D.torch()
+        dev = device or D.device()
+        self.cfg = cfg
+        self.n_maps, self.w_max, self.precision = int(n_maps), int(w_max), precision
+        H = cfg.history
+        self.k_mid = cfg.middle_blocks
+        words = (w_max + 31) // 32
+        f32, i32 = torch.float32, torch.int32
+        self.ring = torch.zeros(n_maps, H, w_max, dtype=f32, device=dev)
+        self.rmap = torch.zeros(n_maps, H, w_max, dtype=f32, device=dev)
+        self.slot_width = torch.zeros(n_maps, H, dtype=i32, device=dev)
+        self.state = torch.zeros(n_maps * _STATE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.scores = torch.zeros(n_maps, w_max, dtype=f32, device=dev)
+        self.mid_blocks = torch.zeros(n_maps, max(self.k_mid, 1), dtype=i32, device=dev)
+        self.mid_mask = torch.zeros(n_maps, words, dtype=i32, device=dev)
+        self.status = torch.zeros(1, dtype=i32, device=dev)
+        self._desc = _lib.Selector(
+            n_maps=n_maps, history=H, block=cfg.block_size, w_max=w_max, k_mid=self.k_mid,
+            sink=cfg.sink_tokens, local=cfg.local_tokens, calib_period=cfg.calibration_period,
+            update_interval=cfg.update_interval, pad_=0,
+            ring=self.ring.data_ptr(), rmap=self.rmap.data_ptr(), slot_width=self.slot_width.data_ptr(),
+            state=self.state.data_ptr(), scores=self.scores.data_ptr(), mid_blocks=self.mid_blocks.data_ptr(),
+            mid_mask=self.mid_mask.data_ptr(), status=self.status.data_ptr(),
+        )
+        self.reset()
+
+    # ------------------------------------------------------------ launches
+    def _call(self, name, *args, stream=None):
+        _lib.check(_lib.fn(name)(ctypes.byref(self._desc), *args, _lib.stream_handle(stream)), name)
+
+    def reset(self, stream=None) -> None:
+        """selector.init_state with no prefill rows, for every map."""
+        self._call("ap_sel_reset", stream=stream)
+
+    def push_rows(self, rows, t: int, mode: int = PUSH_DENSE, stream=None) -> None:
+        """Compress one t-length row per map (rows[i] at row i of a 2-D float32/float64 tensor) and
+        append it to map i's history (selector.py:112-120; mode semantics in include/attnpred.h)."""
+        torch = D.torch()
+        if rows.dim() != 2 or rows.shape[0] != self.n_maps or rows.shape[1] < t or rows.stride(1) != 1:
+            raise ParameterError("rows must be a [n_maps, >=t] tensor with unit column stride")
+        if -(-t // self.cfg.block_size) > self.w_max:
+            raise ParameterError("row longer than w_max * block_size")
+        dt = {torch.float32: _lib.AP_F32, torch.float64: _lib.AP_F64}.get(rows.dtype)
+        if dt is None:
+            raise ParameterError("rows must be float32 or float64")
+        self._call("ap_sel_push_rows", _lib.ptr(rows), dt, rows.stride(0), int(t), int(mode), stream=stream)
+
+    def push_compressed(self, comp, t: int, prefill: bool = False, stream=None) -> None:
+        """Append already-compressed rows (fp32 [n_maps, >=ceil(t/b)]) — the attention kernels' output."""
+        self._call("ap_sel_push_compressed", _lib.ptr(comp), comp.stride(0), int(t), int(prefill), stream=stream)
+
+    def step(self, stream=None) -> None:
+        """selector.py:122-154 for every map: forecast + mask + top-k on update steps, then counter += 1."""
+        self._call("ap_sel_step", _lib.PREC[self.precision], stream=stream)
+
+    # ------------------------------------------------------------ readback
+    def states(self) -> np.ndarray:
+        return self.state.cpu().numpy().view(_STATE_DTYPE)
+
+    def middle(self, i: int) -> list[int]:
+        st = self.states()[i]
+        return self.mid_blocks[i, : int(st["n_mid"])].cpu().tolist()
+
+    def check_status(self) -> None:
+        D.sync_and_check(self.status, "selector")
+
+    def history_rows(self, i: int) -> list[np.ndarray]:
+        """Map i's stored window, oldest first, each row at its own width (host copy)."""
+        st = self.states()[i]
+        H = self.cfg.history
+        n = int(st["n_pushed"])
+        ring = self.ring[i].cpu().numpy()
+        widths = self.slot_width[i].cpu().numpy()
+        out = []
+        for k in range(max(0, n - H), n):
+            s = k % H
+            out.append(ring[s, : widths[s]].astype(np.float64))
+        return out
+
+
+def check_config(cfg) -> None:
+    try:
+        cfg.validate()
+    except ConfigError:
+        raise

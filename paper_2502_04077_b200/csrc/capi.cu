@@ -1,0 +1,42 @@
+// Library-wide host helpers: version, last-error text, SM count.
+#include <cstdarg>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace ap {
+
+static thread_local char g_last_error[512] = "";
+
+void set_last_error(const char* fmt, ...) {
+    va_list ap_;
+    va_start(ap_, fmt);
+    vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap_);
+    va_end(ap_);
+}
+
+int launch_status(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_last_error("%s: %s", what, cudaGetErrorString(e));
+        return AP_ECUDA;
+    }
+    return AP_OK;
+}
+
+}  // namespace ap
+
+extern "C" {
+
+int ap_version(void) { return 10000; /* 1.0.0 */ }
+
+const char* ap_last_error(void) { return ap::g_last_error; }
+
+int ap_device_sm_count(void) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return n;
+}
+
+}  // extern "C"

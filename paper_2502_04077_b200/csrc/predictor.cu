@@ -1,0 +1,465 @@
+// Kernel (2): the shared 4833-parameter conv forecaster over every map.
+//
+// Reference: predictor._forward_cached / forward (predictor.py:185-216):
+//   a1 = relu(conv3x3_{1->16}(x) + b1); s2 = conv3x3_{16->32}(a1) + b2
+//   out[w] = w3 . mean_i relu(s2[:, i, w]) + b3
+// which we evaluate in the equivalent per-history-row form
+//   r[i][w] = sum_c w3[c] relu(s2[c, i, w]);  out[w] = b3 + (1/H) sum_i r[i][w]
+// (oracle.hotpath.row_contributions checks the identity against the golden
+// vectors).  r is kept per ring slot ("r-map") so a decode step only
+// recomputes the history rows whose 3x3∘3x3 receptive field changed:
+// rows {0,1} (new zero padding at the top) and rows [H-s-2, H) (the s new
+// rows at the bottom), plus every row of the column chunks touched by a
+// width change.  See DESIGN.md §Predictor.
+//
+// conv2 (92% of the FLOPs) is an implicit GEMM on the 5th-gen tensor cores:
+// M = 128 consecutive output pixels of one history row, N = 32 out channels,
+// K = 9 taps x 16 in channels, issued as 9 (or 27 for the bf16 hi/lo split)
+// tcgen05.mma K=16 steps whose A operands are shifted windows of the same
+// SWIZZLE_NONE K-major a1 tile in shared memory; accumulators live in TMEM
+// and the epilogue (bias, ReLU, dot w3) reads them with tcgen05.ld.
+// conv1 (K = 9, 3% of FLOPs) runs on the FMA pipe straight into that tile.
+#include "common.cuh"
+
+namespace ap {
+
+// APW1 order (predictor.py:45-52): w1 144 | b1 16 | w2 4608 | b2 32 | w3 32 | b3 1
+constexpr int OFF_W1 = 0, OFF_B1 = 144, OFF_W2 = 160, OFF_B2 = 4768, OFF_W3 = 4800, OFF_B3 = 4832;
+__constant__ float c_w[AP_PARAM_COUNT];
+
+// bf16 B operands: [hi/lo][tap] tiles of N=32 x K=16, K-major SWIZZLE_NONE:
+// element (n, k) at byte (k/8)*512 + n*16 + (k%8)*2  (LBO 512, SBO 128).
+constexpr int BTILE_BYTES = 1024;
+__device__ __align__(16) uint4 g_bpack[2 * 9 * BTILE_BYTES / 16];
+
+constexpr int TW = 128;            // output pixels per MMA tile (M)
+constexpr int BAND = 4;            // history rows per band (TMEM: BAND*32 fp32 columns)
+constexpr int A1R = BAND + 2;      // a1 tile rows
+constexpr int A1C = TW + 2;        // a1 tile cols
+constexpr int XR = BAND + 4;       // x tile rows
+constexpr int XC = TW + 4;         // x tile cols
+constexpr int A1PIX = A1R * A1C;   // 780
+constexpr int PLANE = A1PIX * 16;  // bytes of one 8-channel bf16 plane
+constexpr int NTHREADS = 128;
+
+__global__ void pack_weights_kernel() {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // over 9 taps * 32 n * 16 k
+    if (idx >= 9 * 32 * 16) return;
+    const int tap = idx / 512, n = (idx / 16) % 32, k = idx % 16;
+    const float w = c_w[OFF_W2 + n * 144 + k * 9 + tap];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
+    __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(g_bpack);
+    const int off = (k / 8) * 256 + n * 8 + (k % 8);  // in bf16 elements
+    base[(0 * 9 + tap) * 512 + off] = hi;
+    base[(1 * 9 + tap) * 512 + off] = lo;
+}
+
+struct ConvParams {
+    const float* ring;      // x rows: ring + map*map_stride + slot*pitch + col
+    int64_t map_stride;
+    int32_t pitch;
+    float* rmap;            // r rows: rmap + map*map_stride + slot*pitch + col (same geometry)
+    float* scores;          // scores + map*score_stride + col
+    int64_t score_stride;
+    const int32_t* slot_width;  // [map][H] (selector mode)
+    const ap_map_state* state;  // [map]    (selector mode); null => explicit grids
+    int32_t n_maps, H, W_explicit, n_chunks, update_interval, k_mid;
+    int32_t* status;
+};
+
+struct Task {
+    bool skip;
+    int W;
+    int64_t n_pushed;
+    int nr;          // number of row ranges
+    int ra[2], rb[2];
+};
+
+__device__ __forceinline__ Task plan_task(const ConvParams& P, int map, int chunk) {
+    Task T;
+    T.skip = false;
+    T.nr = 0;
+    const int H = P.H;
+    if (!P.state) {  // explicit grids: full forward
+        T.W = P.W_explicit;
+        T.n_pushed = H;
+        T.nr = 1; T.ra[0] = 0; T.rb[0] = H;
+        T.skip = chunk * TW >= T.W;
+        return T;
+    }
+    const ap_map_state st = P.state[map];
+    T.W = st.width;
+    T.n_pushed = st.n_pushed;
+    if (P.k_mid <= 0 || st.width <= 0 || (st.counter % P.update_interval) != 0 || chunk * TW >= T.W) {
+        T.skip = true;
+        return T;
+    }
+    const int64_t s = st.n_pushed - st.r_pushed;
+    bool full = st.r_pushed < 0 || (int64_t)H - s - 2 <= 2;
+    if (!full && st.r_width != st.width) {  // columns from min(W_old, W_new)-1 changed in every row
+        int lo = (st.r_width < st.width ? st.r_width : st.width) - 1;
+        if (lo < 0) lo = 0;
+        if (chunk * TW + TW > lo) full = true;
+    }
+    if (full) {
+        T.nr = 1; T.ra[0] = 0; T.rb[0] = H;
+    } else if (s > 0) {
+        T.nr = 2; T.ra[0] = 0; T.rb[0] = 2; T.ra[1] = (int)(H - s - 2); T.rb[1] = H;
+    }
+    return T;
+}
+
+// slot of history position p (0 = oldest) given n_pushed; k < 0 => missing (zero) row
+__device__ __forceinline__ int64_t row_index(int64_t n_pushed, int H, int p) { return n_pushed - H + p; }
+__device__ __forceinline__ int slot_of(int64_t k, int H) {
+    int64_t r = k % H;
+    return (int)(r < 0 ? r + H : r);
+}
+
+template <int PREC>
+struct SmemLayout {
+    static constexpr int kBpack = (PREC == AP_PREC_FP32) ? 0 : 2 * 9 * BTILE_BYTES;
+    static constexpr int kA1 = (PREC == AP_PREC_FP32) ? A1PIX * 16 * 4 : 4 * PLANE;  // fp32 or [hl][g] bf16 planes
+    static constexpr int kX = XR * XC * 4;
+    static constexpr int off_bpack = 0;
+    static constexpr int off_a1 = off_bpack + kBpack;
+    static constexpr int off_x = off_a1 + kA1;
+    static constexpr int off_bar = (off_x + kX + 15) / 16 * 16;
+    static constexpr int total = off_bar + 16;
+};
+
+template <int PREC>
+__global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P) {
+    using L = SmemLayout<PREC>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    float* xs = reinterpret_cast<float*>(smem + L::off_x);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_bar + 8);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    constexpr bool kTC = PREC != AP_PREC_FP32;
+    uint32_t tmem_base = 0, phase = 0;
+
+    if constexpr (kTC) {
+        // B operands once per persistent CTA
+        const uint4* src = g_bpack;
+        uint4* dst = reinterpret_cast<uint4*>(smem + L::off_bpack);
+        for (int i = tid; i < L::kBpack / 16; i += NTHREADS) dst[i] = src[i];
+        if (tid == 0) mbar_init(mbar, 1);
+        if (warp == 0) tmem_alloc(tmem_slot, BAND * 32);
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        tmem_base = *tmem_slot;
+    }
+
+    const int H = P.H;
+    const int n_tasks = P.n_maps * P.n_chunks;
+    for (int task = blockIdx.x; task < n_tasks; task += gridDim.x) {
+        const int map = task / P.n_chunks, chunk = task % P.n_chunks;
+        const Task T = plan_task(P, map, chunk);
+        if (T.skip) continue;
+        const int W = T.W, w0 = chunk * TW;
+        const float* ring = P.ring + (int64_t)map * P.map_stride;
+        float* rmap = P.rmap + (int64_t)map * P.map_stride;
+        const int32_t* sw = P.state ? P.slot_width + (int64_t)map * H : nullptr;
+
+        for (int rr = 0; rr < T.nr; ++rr) {
+            for (int r0 = T.ra[rr]; r0 < T.rb[rr]; r0 += BAND) {
+                const int r1 = (r0 + BAND < T.rb[rr]) ? r0 + BAND : T.rb[rr];
+                const int nb = r1 - r0;
+                // ---- 1. x tile: positions [r0-2, r1+2) x cols [w0-2, w0+TW+2)
+                const int xrows = nb + 4;
+                for (int i = tid; i < xrows * XC; i += NTHREADS) {
+                    const int xr = i / XC, xc = i % XC;
+                    const int p = r0 - 2 + xr, c = w0 - 2 + xc;
+                    float v = 0.f;
+                    if (p >= 0 && p < H && c >= 0 && c < W) {
+                        const int64_t k = row_index(T.n_pushed, H, p);
+                        if (k >= 0) {
+                            const int slot = P.state ? slot_of(k, H) : p;
+                            const int width = P.state ? sw[slot] : W;
+                            if (c < width) {
+                                v = ring[(int64_t)slot * P.pitch + c];
+                                if (!isfinite(v)) raise_status(P.status, AP_ENUMERIC);
+                            }
+                        }
+                    }
+                    xs[xr * XC + xc] = v;
+                }
+                __syncthreads();
+                // ---- 2. conv1 + ReLU -> a1 tile (zero outside the H x W grid)
+                const int a1pix = (nb + 2) * A1C;
+                for (int i = tid; i < a1pix; i += NTHREADS) {
+                    const int ar = i / A1C, ac = i % A1C;
+                    const int p = r0 - 1 + ar, c = w0 - 1 + ac;
+                    const bool valid = p >= 0 && p < H && c >= 0 && c < W;
+                    float x9[9];
+#pragma unroll
+                    for (int di = 0; di < 3; ++di)
+#pragma unroll
+                        for (int dj = 0; dj < 3; ++dj) x9[di * 3 + dj] = xs[(ar + di) * XC + ac + dj];
+                    float a[16];
+#pragma unroll
+                    for (int ch = 0; ch < 16; ++ch) {
+                        float acc = c_w[OFF_B1 + ch];
+#pragma unroll
+                        for (int q = 0; q < 9; ++q) acc = fmaf(c_w[OFF_W1 + ch * 9 + q], x9[q], acc);
+                        a[ch] = valid ? fmaxf(acc, 0.f) : 0.f;
+                    }
+                    if constexpr (kTC) {
+#pragma unroll
+                        for (int g = 0; g < 2; ++g) {
+                            __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                hi[q] = __float2bfloat16_rn(a[g * 8 + q]);
+                                lo[q] = __float2bfloat16_rn(a[g * 8 + q] - __bfloat162float(hi[q]));
+                            }
+                            *reinterpret_cast<uint4*>(smem + L::off_a1 + (0 * 2 + g) * PLANE + i * 16) =
+                                *reinterpret_cast<uint4*>(hi);
+                            if constexpr (PREC == AP_PREC_BF16X3)
+                                *reinterpret_cast<uint4*>(smem + L::off_a1 + (1 * 2 + g) * PLANE + i * 16) =
+                                    *reinterpret_cast<uint4*>(lo);
+                        }
+                    } else {
+                        float4* d = reinterpret_cast<float4*>(smem + L::off_a1 + i * 64);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) d[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+                    }
+                }
+                if constexpr (kTC) fence_async_smem();
+                __syncthreads();
+
+                // ---- 3. conv2 + epilogue -> r for rows r0..r1-1
+                float rvals[BAND];
+                if constexpr (kTC) {
+                    if (tid == 0) {
+                        tc_fence_after();
+                        constexpr uint32_t idesc = idesc_bf16_f32(TW, 32);
+                        const uint32_t a1_addr = smem_u32(smem + L::off_a1);
+                        const uint32_t b_addr = smem_u32(smem + L::off_bpack);
+                        for (int j = 0; j < nb; ++j) {
+                            const uint32_t d_tmem = tmem_base + j * 32;
+                            uint32_t acc = 0;
+#pragma unroll
+                            for (int tap = 0; tap < 9; ++tap) {
+                                const int di = tap / 3, dj = tap % 3;
+                                const uint32_t pix = (uint32_t)((j + di) * A1C + dj);
+                                const uint64_t a_hi = umma_desc(a1_addr + 0 * 2 * PLANE + pix * 16, PLANE, 128);
+                                const uint64_t b_hi = umma_desc(b_addr + (0 * 9 + tap) * BTILE_BYTES, 512, 128);
+                                mma_bf16(d_tmem, a_hi, b_hi, idesc, acc);
+                                acc = 1;
+                                if constexpr (PREC == AP_PREC_BF16X3) {
+                                    const uint64_t a_lo = umma_desc(a1_addr + 1 * 2 * PLANE + pix * 16, PLANE, 128);
+                                    const uint64_t b_lo = umma_desc(b_addr + (1 * 9 + tap) * BTILE_BYTES, 512, 128);
+                                    mma_bf16(d_tmem, a_hi, b_lo, idesc, 1);
+                                    mma_bf16(d_tmem, a_lo, b_hi, idesc, 1);
+                                }
+                            }
+                        }
+                        mma_commit(mbar);
+                    }
+                    __syncwarp();
+                    mbar_wait(mbar, phase);
+                    phase ^= 1u;
+                    tc_fence_after();
+                    for (int j = 0; j < nb; ++j) {
+                        float acc[32];
+                        tmem_ld32(tmem_base + ((uint32_t)(warp * 32) << 16) + j * 32, acc);
+                        float r = 0.f;
+#pragma unroll
+                        for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n] + c_w[OFF_B2 + n], 0.f), r);
+                        rvals[j] = r;
+                    }
+                    tc_fence_before();
+                } else {
+                    const float* a1 = reinterpret_cast<const float*>(smem + L::off_a1);
+                    for (int j = 0; j < nb; ++j) {
+                        float acc[32];
+#pragma unroll
+                        for (int n = 0; n < 32; ++n) acc[n] = c_w[OFF_B2 + n];
+                        for (int tap = 0; tap < 9; ++tap) {
+                            const int di = tap / 3, dj = tap % 3;
+                            const float4* ap4 = reinterpret_cast<const float4*>(a1 + ((j + di) * A1C + tid + dj) * 16);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float4 v = ap4[q];
+                                const float av[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const int k = q * 4 + e;
+#pragma unroll
+                                    for (int n = 0; n < 32; ++n) acc[n] = fmaf(c_w[OFF_W2 + n * 144 + k * 9 + tap], av[e], acc[n]);
+                                }
+                            }
+                        }
+                        float r = 0.f;
+#pragma unroll
+                        for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n], 0.f), r);
+                        rvals[j] = r;
+                    }
+                }
+                const int col = w0 + tid;
+                if (col < W) {
+                    for (int j = 0; j < nb; ++j) {
+                        const int p = r0 + j;
+                        const int slot = P.state ? slot_of(row_index(T.n_pushed, H, p), H) : p;
+                        rmap[(int64_t)slot * P.pitch + col] = rvals[j];
+                    }
+                }
+                __syncthreads();  // x / a1 tiles and TMEM columns are reused by the next band
+            }
+        }
+        // ---- 4. forecast for this chunk: b3 + (1/H) sum_p r[p] in fixed position order
+        const int col = w0 + tid;
+        if (col < W) {
+            float sum = 0.f;
+            const float* rc = rmap + col;
+            if (P.state) {
+                int slot = slot_of(row_index(T.n_pushed, H, 0), H);
+#pragma unroll 8
+                for (int p = 0; p < H; ++p) {
+                    sum += rc[(int64_t)slot * P.pitch];
+                    slot = (slot + 1 == H) ? 0 : slot + 1;
+                }
+            } else {
+#pragma unroll 8
+                for (int p = 0; p < H; ++p) sum += rc[(int64_t)p * P.pitch];
+            }
+            P.scores[(int64_t)map * P.score_stride + col] = c_w[OFF_B3] + sum / (float)H;
+        }
+    }
+
+    if constexpr (kTC) {
+        tc_fence_before();
+        __syncthreads();
+        if (warp == 0) tmem_dealloc(tmem_base, BAND * 32);
+    }
+}
+
+template <int PREC>
+static int grid_ctas() {
+    static int cached = 0;
+    if (!cached) {
+        int per_sm = 0;
+        cudaFuncSetAttribute(conv_forecast_kernel<PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SmemLayout<PREC>::total);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_forecast_kernel<PREC>, NTHREADS,
+                                                      SmemLayout<PREC>::total);
+        if (per_sm < 1) per_sm = 1;
+        if (PREC != AP_PREC_FP32 && per_sm * BAND * 32 > 512) per_sm = 512 / (BAND * 32);  // TMEM columns
+        cached = ap_device_sm_count() * per_sm;
+    }
+    return cached;
+}
+
+static int launch_conv(const ConvParams& P, int precision, cudaStream_t st) {
+    const int n_tasks = P.n_maps * P.n_chunks;
+    if (n_tasks == 0) return AP_OK;
+    switch (precision) {
+        case AP_PREC_FP32: {
+            int g = grid_ctas<AP_PREC_FP32>();
+            conv_forecast_kernel<AP_PREC_FP32><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_FP32>::total, st>>>(P);
+            break;
+        }
+        case AP_PREC_BF16X3: {
+            int g = grid_ctas<AP_PREC_BF16X3>();
+            conv_forecast_kernel<AP_PREC_BF16X3><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_BF16X3>::total, st>>>(P);
+            break;
+        }
+        case AP_PREC_BF16: {
+            int g = grid_ctas<AP_PREC_BF16>();
+            conv_forecast_kernel<AP_PREC_BF16><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_BF16>::total, st>>>(P);
+            break;
+        }
+        default:
+            AP_REQUIRE(false, AP_EPARAM, "unknown precision %d", precision);
+    }
+    return launch_status("conv_forecast_kernel");
+}
+
+void launch_sel_topk(const ap_selector& s, cudaStream_t stream);
+
+}  // namespace ap
+
+using namespace ap;
+
+extern "C" {
+
+int ap_set_weights(const float* weights4833, void* stream) {
+    AP_REQUIRE(weights4833 != nullptr, AP_EPARAM, "weights pointer is null");
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = cudaMemcpyToSymbolAsync(c_w, weights4833, sizeof(float) * AP_PARAM_COUNT, 0,
+                                            cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+        set_last_error("ap_set_weights: %s", cudaGetErrorString(e));
+        return AP_ECUDA;
+    }
+    pack_weights_kernel<<<(9 * 32 * 16 + 255) / 256, 256, 0, st>>>();
+    return launch_status("ap_set_weights");
+}
+
+int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W, int64_t grid_stride, float* out,
+                       int64_t out_stride, float* rscratch, int precision, int32_t* status, void* stream) {
+    AP_REQUIRE(H >= 1 && W >= 1 && n_grids >= 0, AP_EPARAM, "bad grid shape");
+    AP_REQUIRE(grid_stride >= (int64_t)H * W, AP_EPARAM, "grid_stride too small");
+    ConvParams P{};
+    P.ring = grids;
+    P.map_stride = grid_stride;
+    P.pitch = W;
+    P.rmap = rscratch;
+    P.scores = out;
+    P.score_stride = out_stride;
+    P.slot_width = nullptr;
+    P.state = nullptr;
+    P.n_maps = n_grids;
+    P.H = H;
+    P.W_explicit = W;
+    P.n_chunks = (W + TW - 1) / TW;
+    P.update_interval = 1;
+    P.k_mid = 1;
+    P.status = status;
+    // rscratch uses the same geometry as the grids
+    return launch_conv(P, precision, as_stream(stream));
+}
+
+int ap_sel_step(const ap_selector* s, int precision, void* stream) {
+    AP_REQUIRE(s && s->n_maps > 0, AP_EPARAM, "bad selector descriptor");
+    AP_REQUIRE(s->update_interval >= 1 && s->calib_period >= 1, AP_ECONFIG, "bad selector config");
+    cudaStream_t st = as_stream(stream);
+    if (s->k_mid > 0) {
+        ConvParams P{};
+        P.ring = s->ring;
+        P.map_stride = (int64_t)s->history * s->w_max;
+        P.pitch = s->w_max;
+        P.rmap = s->rmap;
+        P.scores = s->scores;
+        P.score_stride = s->w_max;
+        P.slot_width = s->slot_width;
+        P.state = s->state;
+        P.n_maps = s->n_maps;
+        P.H = s->history;
+        P.W_explicit = 0;
+        P.n_chunks = (s->w_max + TW - 1) / TW;
+        P.update_interval = s->update_interval;
+        P.k_mid = s->k_mid;
+        P.status = s->status;
+        int rc = launch_conv(P, precision, st);
+        if (rc != AP_OK) return rc;
+    }
+    launch_sel_topk(*s, st);
+    return launch_status("sel_topk_kernel");
+}
+
+int ap_sel_grid_ctas(int precision) {
+    switch (precision) {
+        case AP_PREC_FP32: return grid_ctas<AP_PREC_FP32>();
+        case AP_PREC_BF16X3: return grid_ctas<AP_PREC_BF16X3>();
+        case AP_PREC_BF16: return grid_ctas<AP_PREC_BF16>();
+    }
+    return 0;
+}
+
+}  // extern "C"

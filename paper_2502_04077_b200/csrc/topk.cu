@@ -1,0 +1,230 @@
+// Kernel (3): per-row top-k block selection as a block-wide radix select.
+//
+// Reference: selector.topk (selector.py:73-81) — the k largest values,
+// descending, ties broken toward the lower index (lexsort on (index,
+// -value)), -0.0 == +0.0 — and the sink/local masking + min(K, available)
+// of selector.step (selector.py:134-145).
+//
+// Values map to order-preserving unsigned keys; an 8-bit-digit radix select
+// finds the k-th largest key T; then one ordered pass takes every key > T and
+// the lowest-index keys == T until k are taken.  Output ids are ascending,
+// which is the set the reference returns.  Bit-exact on identical inputs.
+#include "common.cuh"
+
+namespace ap {
+
+template <typename KeyT>
+struct KeyTraits;
+template <> struct KeyTraits<uint32_t> { static constexpr int kPasses = 4; };
+template <> struct KeyTraits<unsigned long long> { static constexpr int kPasses = 8; };
+
+// keyfn(i) -> KeyT for i in [0, n).  Returns T and the number of keys == T to take.
+template <int NT, typename KeyT, typename KeyFn>
+__device__ void radix_select(KeyFn keyfn, int n, int k, int* hist /*[256]*/, int* scan_tmp, KeyT& T_out,
+                             int& take_eq_out) {
+    KeyT prefix = 0, hi_mask = 0;
+    int remaining = k;
+#pragma unroll 1
+    for (int pass = KeyTraits<KeyT>::kPasses - 1; pass >= 0; --pass) {
+        const int shift = pass * 8;
+        for (int d = threadIdx.x; d < 256; d += NT) hist[d] = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += NT) {
+            KeyT key = keyfn(i);
+            if (((key ^ prefix) & hi_mask) == 0) atomicAdd(&hist[(int)((key >> shift) & 0xFF)], 1);
+        }
+        __syncthreads();
+        // suffix scan over digits 255..0: thread d (<256) owns digit 255-d
+        int c = threadIdx.x < 256 ? hist[255 - threadIdx.x] : 0;
+        int total = 0;
+        int excl = block_excl_scan<NT>(c, scan_tmp, total);
+        // the digit where the cumulative count first reaches `remaining`
+        if (threadIdx.x < 256 && excl < remaining && excl + c >= remaining) {
+            scan_tmp[NT / 32] = 255 - threadIdx.x;
+            scan_tmp[NT / 32 + 1] = excl;
+        }
+        __syncthreads();
+        const int digit = scan_tmp[NT / 32];
+        remaining -= scan_tmp[NT / 32 + 1];
+        prefix |= (KeyT)digit << shift;
+        hi_mask |= (KeyT)0xFF << shift;
+        __syncthreads();
+    }
+    T_out = prefix;
+    take_eq_out = remaining;
+}
+
+// Ordered emission: ids of keys > T plus the first take_eq keys == T, ascending.
+// Returns the count (== k).  emit(rank, id) is called once per selected id.
+template <int NT, typename KeyT, typename KeyFn, typename Emit>
+__device__ int ordered_emit(KeyFn keyfn, int n, KeyT T, int take_eq, int* scan_tmp, Emit emit) {
+    const int per = (n + NT - 1) / NT;
+    const int lo = threadIdx.x * per;
+    const int hi = lo + per < n ? lo + per : n;
+    int n_eq = 0;
+    for (int i = lo; i < hi; ++i) n_eq += (keyfn(i) == T);
+    int tot = 0;
+    int eq_base = block_excl_scan<NT>(n_eq, scan_tmp, tot);
+    int n_sel = 0;
+    int eq_rank = eq_base;
+    for (int i = lo; i < hi; ++i) {
+        KeyT key = keyfn(i);
+        if (key > T) {
+            ++n_sel;
+        } else if (key == T) {
+            n_sel += (eq_rank < take_eq);
+            ++eq_rank;
+        }
+    }
+    int total = 0;
+    int out_base = block_excl_scan<NT>(n_sel, scan_tmp, total);
+    eq_rank = eq_base;
+    int pos = out_base;
+    for (int i = lo; i < hi; ++i) {
+        KeyT key = keyfn(i);
+        bool take = false;
+        if (key > T) {
+            take = true;
+        } else if (key == T) {
+            take = eq_rank < take_eq;
+            ++eq_rank;
+        }
+        if (take) emit(pos++, i);
+    }
+    return total;
+}
+
+template <typename V>
+struct ValueKey {
+    const V* v;
+    __device__ auto operator()(int i) const { return order_key(v[i]); }
+};
+
+template <int NT, typename V>
+__global__ void __launch_bounds__(NT) topk_rows_kernel(const V* __restrict__ values, int64_t row_stride, int n,
+                                                       int k, int32_t* __restrict__ out_ids, int64_t out_stride,
+                                                       int32_t* __restrict__ out_count) {
+    using KeyT = decltype(order_key(V(0)));
+    __shared__ int hist[256];
+    __shared__ int scan_tmp[NT / 32 + 2];
+    const int64_t r = blockIdx.x;
+    ValueKey<V> kf{values + r * row_stride};
+    int32_t* ids = out_ids + r * out_stride;
+    if (k <= 0) {
+        if (threadIdx.x == 0) out_count[r] = 0;
+        return;
+    }
+    KeyT T;
+    int take_eq;
+    radix_select<NT, KeyT>(kf, n, k, hist, scan_tmp, T, take_eq);
+    int total = ordered_emit<NT, KeyT>(kf, n, T, take_eq, scan_tmp, [&](int pos, int i) { ids[pos] = i; });
+    if (threadIdx.x == 0) out_count[r] = total;
+}
+
+// ------------------------------------------------------ selector tail kernel
+struct MaskedScoreKey {
+    const float* scores;
+    int sink_lo, sink_hi, local_lo, local_hi;  // masked covering block ranges [lo, hi)
+    __device__ uint32_t operator()(int i) const {
+        bool masked = (i >= sink_lo && i < sink_hi) || (i >= local_lo && i < local_hi);
+        return masked ? order_key(-INFINITY) : order_key(scores[i]);
+    }
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s) {
+    __shared__ int hist[256];
+    __shared__ int scan_tmp[NT / 32 + 2];
+    __shared__ int s_nan;
+    const int m = blockIdx.x;
+    ap_map_state st = s.state[m];
+    const bool update = (st.counter % s.update_interval) == 0;
+    const int words = (s.w_max + 31) / 32;
+    uint32_t* mask = s.mid_mask + (int64_t)m * words;
+    int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
+    if (threadIdx.x == 0) s_nan = 0;
+    __syncthreads();
+    int count = st.n_mid;
+    if (update && s.k_mid > 0 && st.width > 0) {
+        const int W = st.width;
+        const int b = s.block;
+        const int64_t t = st.row_len;
+        const int64_t nl = t + 1;
+        // covering blocks of sink [0, min(sink, nl)) and local [max(0, nl-local), nl) — selector.py:84-88,134-142
+        MaskedScoreKey kf;
+        kf.scores = s.scores + (int64_t)m * s.w_max;
+        const int64_t sink_end = s.sink < nl ? s.sink : nl;
+        kf.sink_lo = 0;
+        kf.sink_hi = sink_end > 0 ? (int)cdiv64(sink_end, b) : 0;
+        const int64_t ls = nl - s.local > 0 ? nl - s.local : 0;
+        kf.local_lo = ls < nl ? (int)(ls / b) : 0;
+        kf.local_hi = ls < nl ? (int)cdiv64(nl, b) : 0;
+        if (kf.sink_hi > W) kf.sink_hi = W;
+        if (kf.local_hi > W) kf.local_hi = W;
+        // available = #finite after masking (selector.py:143)
+        int n_masked_local = 0;
+        for (int i = threadIdx.x; i < W; i += NT) {
+            bool masked = (i >= kf.sink_lo && i < kf.sink_hi) || (i >= kf.local_lo && i < kf.local_hi);
+            float v = kf.scores[i];
+            if (v != v) s_nan = 1;
+            n_masked_local += masked || (v == -INFINITY);
+        }
+        int n_masked = 0;
+        block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
+        if (s_nan) raise_status(s.status, AP_ENUMERIC);
+        const int available = W - n_masked;
+        const int k = s.k_mid < available ? s.k_mid : available;
+        for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
+        __syncthreads();
+        if (k > 0) {
+            uint32_t T;
+            int take_eq;
+            radix_select<NT, uint32_t>(kf, W, k, hist, scan_tmp, T, take_eq);
+            count = ordered_emit<NT, uint32_t>(kf, W, T, take_eq, scan_tmp, [&](int pos, int i) {
+                mid[pos] = i;
+                atomicOr(&mask[i >> 5], 1u << (i & 31));
+            });
+        } else {
+            count = 0;
+        }
+        if (threadIdx.x == 0) {
+            st.n_mid = count;
+            st.mid_clip = t;
+            st.r_pushed = st.n_pushed;
+            st.r_width = st.width;
+        }
+    } else if (update && s.k_mid <= 0) {
+        for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
+        if (threadIdx.x == 0) st.n_mid = 0;
+    }
+    if (threadIdx.x == 0) {
+        st.counter += 1;
+        s.state[m] = st;
+    }
+}
+
+void launch_sel_topk(const ap_selector& s, cudaStream_t stream) {
+    sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s);
+}
+
+}  // namespace ap
+
+using namespace ap;
+
+extern "C" int ap_topk(const void* values, int dtype, int64_t n_rows, int64_t row_stride, int32_t n, int32_t k,
+                       int32_t* out_ids, int64_t out_stride, int32_t* out_count, int32_t* status, void* stream) {
+    (void)status;
+    AP_REQUIRE(k <= n, AP_EPARAM, "k=%d exceeds vector length %d", k, n);
+    AP_REQUIRE(n >= 0 && n_rows >= 0 && n_rows <= 0x7fffffff, AP_EPARAM, "bad sizes");
+    if (n_rows == 0) return AP_OK;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == AP_F32)
+        topk_rows_kernel<512, float><<<(unsigned)n_rows, 512, 0, st>>>((const float*)values, row_stride, n, k,
+                                                                       out_ids, out_stride, out_count);
+    else if (dtype == AP_F64)
+        topk_rows_kernel<512, double><<<(unsigned)n_rows, 512, 0, st>>>((const double*)values, row_stride, n, k,
+                                                                        out_ids, out_stride, out_count);
+    else
+        AP_REQUIRE(false, AP_EPARAM, "values must be float32 or float64");
+    return launch_status("ap_topk");
+}
