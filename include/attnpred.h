@@ -45,8 +45,9 @@ extern "C" {
 
 /* predictor arithmetic (DESIGN.md §Predictor precision) */
 #define AP_PREC_FP32    0  /* SIMT fp32 FMA, no tensor cores (tolerance rtol 1e-3) */
-#define AP_PREC_BF16X3  1  /* tcgen05 bf16 hi/lo split, 3 MMAs per tap (rtol 1e-3) */
-#define AP_PREC_BF16    2  /* tcgen05 single bf16 MMA per tap (rtol 2e-2) */
+#define AP_PREC_F16X3   1  /* tcgen05, fp16 hi/lo split with exact power-of-2 scaling:
+                              3 MMAs per tap, ~22-bit operands (rtol 1e-3; default) */
+#define AP_PREC_F16     2  /* tcgen05, one scaled fp16 MMA per tap (rtol 2e-2) */
 
 #define AP_PARAM_COUNT 4833 /* predictor.py:36-40 */
 
@@ -89,7 +90,7 @@ int ap_topk(const void* values, int dtype, int64_t n_rows, int64_t row_stride, i
 
 /* predictor.forward — predictor.py:185-216 on explicit H x W grids (fp32,
  * row-major, grid i at grids + i*grid_stride).  out: W fp32 per grid.
- * rscratch: n_grids*H*W fp32 workspace (per-row contributions). */
+ * rscratch: n_grids*grid_stride fp32 workspace (per-row contributions). */
 int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W, int64_t grid_stride,
                        float* out, int64_t out_stride, float* rscratch, int precision,
                        int32_t* status, void* stream);

@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libattnpred.so"
 
 AP_OK, AP_EPARAM, AP_ECONFIG, AP_ESTATE, AP_ENUMERIC, AP_ECUDA = range(6)
 AP_F32, AP_F64, AP_BF16 = 0, 1, 2
-PREC = {"fp32": 0, "bf16x3": 1, "bf16": 2}
+PREC = {"fp32": 0, "fp16x3": 1, "fp16": 2}
 
 _ERR = {
     AP_EPARAM: E.ParameterError,

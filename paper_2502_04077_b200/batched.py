@@ -41,7 +41,7 @@ class BatchedSelector:
     w_max: the largest compressed width any map will reach (ceil(t_max/b)).
     """
 
-    def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "bf16x3", device=None):
+    def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "fp16x3", device=None):
         cfg.validate()
         if n_maps < 1 or w_max < 1:
             raise ParameterError("n_maps and w_max must be >= 1")

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 #include <math.h>
 
@@ -107,11 +108,11 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes
     return d;
 }
 
-// Instruction descriptor for kind::f16: A=B=bf16, D=f32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+// Instruction descriptor for kind::f16: A=B=f16 (fmt 0) or bf16 (fmt 1), D=f32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N, uint32_t ab_fmt = 0) {
     return (1u << 4)            // c_format = F32
-         | (1u << 7)            // a_format = BF16
-         | (1u << 10)           // b_format = BF16
+         | (ab_fmt << 7)        // a_format
+         | (ab_fmt << 10)       // b_format
          | ((uint32_t)(N >> 3) << 17)
          | ((uint32_t)(M >> 4) << 24);
 }
@@ -134,7 +135,7 @@ __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"

@@ -14,7 +14,7 @@
 //
 // conv2 (92% of the FLOPs) is an implicit GEMM on the 5th-gen tensor cores:
 // M = 128 consecutive output pixels of one history row, N = 32 out channels,
-// K = 9 taps x 16 in channels, issued as 9 (or 27 for the bf16 hi/lo split)
+// K = 9 taps x 16 in channels, issued as 9 (or 27 for the fp16 hi/lo split)
 // tcgen05.mma K=16 steps whose A operands are shifted windows of the same
 // SWIZZLE_NONE K-major a1 tile in shared memory; accumulators live in TMEM
 // and the epilogue (bias, ReLU, dot w3) reads them with tcgen05.ld.
@@ -27,10 +27,24 @@ namespace ap {
 constexpr int OFF_W1 = 0, OFF_B1 = 144, OFF_W2 = 160, OFF_B2 = 4768, OFF_W3 = 4800, OFF_B3 = 4832;
 __constant__ float c_w[AP_PARAM_COUNT];
 
-// bf16 B operands: [hi/lo][tap] tiles of N=32 x K=16, K-major SWIZZLE_NONE:
+// fp16 B operands: [hi/lo][tap] tiles of N=32 x K=16, K-major SWIZZLE_NONE:
 // element (n, k) at byte (k/8)*512 + n*16 + (k%8)*2  (LBO 512, SBO 128).
+// w2 is scaled by 2^g_wexp (exact) so its hi/lo halves use fp16's full
+// 11+11 significant bits without overflow; the epilogue undoes the scale.
 constexpr int BTILE_BYTES = 1024;
 __device__ __align__(16) uint4 g_bpack[2 * 9 * BTILE_BYTES / 16];
+__device__ int g_wexp;            // power-of-2 exponent applied to w2
+__device__ float g_w1abs[16];     // sum_t |w1[c][t]|  (a1 magnitude bound)
+__device__ float g_b1abs[16];     // |b1[c]|
+
+// Largest e with bound * 2^e < 2^14 (so fp16 values stay below 2^15).
+__device__ __forceinline__ int f16_scale_exp(float bound) {
+    if (!(bound > 0.f) || !isfinite(bound)) return 0;
+    int k;
+    frexpf(bound, &k);  // bound = m * 2^k, m in [0.5, 1)
+    int e = 14 - k;
+    return e < -120 ? -120 : (e > 120 ? 120 : e);
+}
 
 constexpr int TW = 128;            // output pixels per MMA tile (M)
 constexpr int BAND = 4;            // history rows per band (TMEM: BAND*32 fp32 columns)
@@ -39,20 +53,36 @@ constexpr int A1C = TW + 2;        // a1 tile cols
 constexpr int XR = BAND + 4;       // x tile rows
 constexpr int XC = TW + 4;         // x tile cols
 constexpr int A1PIX = A1R * A1C;   // 780
-constexpr int PLANE = A1PIX * 16;  // bytes of one 8-channel bf16 plane
+constexpr int PLANE = A1PIX * 16;  // bytes of one 8-channel fp16 plane
 constexpr int NTHREADS = 128;
 
+// One CTA: w2 scale, then the [hi/lo][tap] fp16 tiles and the a1 magnitude bounds.
 __global__ void pack_weights_kernel() {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // over 9 taps * 32 n * 16 k
-    if (idx >= 9 * 32 * 16) return;
-    const int tap = idx / 512, n = (idx / 16) % 32, k = idx % 16;
-    const float w = c_w[OFF_W2 + n * 144 + k * 9 + tap];
-    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(w - __bfloat162float(hi));
-    __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(g_bpack);
-    const int off = (k / 8) * 256 + n * 8 + (k % 8);  // in bf16 elements
-    base[(0 * 9 + tap) * 512 + off] = hi;
-    base[(1 * 9 + tap) * 512 + off] = lo;
+    __shared__ float s_max;
+    if (threadIdx.x == 0) s_max = 0.f;
+    __syncthreads();
+    float m = 0.f;
+    for (int i = threadIdx.x; i < 4608; i += blockDim.x) m = fmaxf(m, fabsf(c_w[OFF_W2 + i]));
+    atomicMax(reinterpret_cast<int*>(&s_max), __float_as_int(m));  // non-negative floats order as ints
+    __syncthreads();
+    const int e = f16_scale_exp(s_max);
+    if (threadIdx.x == 0) g_wexp = e;
+    if (threadIdx.x < 16) {
+        float a = 0.f;
+        for (int q = 0; q < 9; ++q) a += fabsf(c_w[OFF_W1 + threadIdx.x * 9 + q]);
+        g_w1abs[threadIdx.x] = a;
+        g_b1abs[threadIdx.x] = fabsf(c_w[OFF_B1 + threadIdx.x]);
+    }
+    __half* base = reinterpret_cast<__half*>(g_bpack);
+    for (int idx = threadIdx.x; idx < 9 * 32 * 16; idx += blockDim.x) {
+        const int tap = idx / 512, n = (idx / 16) % 32, k = idx % 16;
+        const float w = ldexpf(c_w[OFF_W2 + n * 144 + k * 9 + tap], e);
+        const __half hi = __float2half_rn(w);
+        const __half lo = __float2half_rn(w - __half2float(hi));
+        const int off = (k / 8) * 256 + n * 8 + (k % 8);  // in fp16 elements
+        base[(0 * 9 + tap) * 512 + off] = hi;
+        base[(1 * 9 + tap) * 512 + off] = lo;
+    }
 }
 
 struct ConvParams {
@@ -120,13 +150,13 @@ __device__ __forceinline__ int slot_of(int64_t k, int H) {
 template <int PREC>
 struct SmemLayout {
     static constexpr int kBpack = (PREC == AP_PREC_FP32) ? 0 : 2 * 9 * BTILE_BYTES;
-    static constexpr int kA1 = (PREC == AP_PREC_FP32) ? A1PIX * 16 * 4 : 4 * PLANE;  // fp32 or [hl][g] bf16 planes
+    static constexpr int kA1 = (PREC == AP_PREC_FP32) ? A1PIX * 16 * 4 : 4 * PLANE;  // fp32 or [hl][g] fp16 planes
     static constexpr int kX = XR * XC * 4;
     static constexpr int off_bpack = 0;
     static constexpr int off_a1 = off_bpack + kBpack;
     static constexpr int off_x = off_a1 + kA1;
     static constexpr int off_bar = (off_x + kX + 15) / 16 * 16;
-    static constexpr int total = off_bar + 16;
+    static constexpr int total = off_bar + 32;
 };
 
 template <int PREC>
@@ -136,6 +166,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
     float* xs = reinterpret_cast<float*>(smem + L::off_x);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_bar + 8);
+    int* s_xmax = reinterpret_cast<int*>(smem + L::off_bar + 16);
     const int tid = threadIdx.x, warp = tid >> 5;
     constexpr bool kTC = PREC != AP_PREC_FP32;
     uint32_t tmem_base = 0, phase = 0;
@@ -145,7 +176,10 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
         const uint4* src = g_bpack;
         uint4* dst = reinterpret_cast<uint4*>(smem + L::off_bpack);
         for (int i = tid; i < L::kBpack / 16; i += NTHREADS) dst[i] = src[i];
-        if (tid == 0) mbar_init(mbar, 1);
+        if (tid == 0) {
+            mbar_init(mbar, 1);
+            *s_xmax = 0;
+        }
         if (warp == 0) tmem_alloc(tmem_slot, BAND * 32);
         fence_async_smem();
         tc_fence_before();
@@ -156,6 +190,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
 
     const int H = P.H;
     const int n_tasks = P.n_maps * P.n_chunks;
+    const int wexp = kTC ? g_wexp : 0;
     for (int task = blockIdx.x; task < n_tasks; task += gridDim.x) {
         const int map = task / P.n_chunks, chunk = task % P.n_chunks;
         const Task T = plan_task(P, map, chunk);
@@ -171,6 +206,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
                 const int nb = r1 - r0;
                 // ---- 1. x tile: positions [r0-2, r1+2) x cols [w0-2, w0+TW+2)
                 const int xrows = nb + 4;
+                float xmax = 0.f;
                 for (int i = tid; i < xrows * XC; i += NTHREADS) {
                     const int xr = i / XC, xc = i % XC;
                     const int p = r0 - 2 + xr, c = w0 - 2 + xc;
@@ -187,8 +223,23 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
                         }
                     }
                     xs[xr * XC + xc] = v;
+                    xmax = fmaxf(xmax, fabsf(v));
+                }
+                if constexpr (kTC) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+                    if ((tid & 31) == 0) atomicMax(s_xmax, __float_as_int(xmax));
                 }
                 __syncthreads();
+                // exact power-of-2 scale for the fp16 a1 operand: a1 <= |b1| + sum|w1| * max|x|
+                int aexp = 0;
+                if constexpr (kTC) {
+                    const float mx = __int_as_float(*s_xmax);
+                    float bound = 0.f;
+#pragma unroll
+                    for (int ch = 0; ch < 16; ++ch) bound = fmaxf(bound, g_b1abs[ch] + g_w1abs[ch] * mx);
+                    aexp = f16_scale_exp(bound);
+                }
                 // ---- 2. conv1 + ReLU -> a1 tile (zero outside the H x W grid)
                 const int a1pix = (nb + 2) * A1C;
                 for (int i = tid; i < a1pix; i += NTHREADS) {
@@ -211,15 +262,16 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
                     if constexpr (kTC) {
 #pragma unroll
                         for (int g = 0; g < 2; ++g) {
-                            __align__(16) __nv_bfloat16 hi[8], lo[8];
+                            __align__(16) __half hi[8], lo[8];
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
-                                hi[q] = __float2bfloat16_rn(a[g * 8 + q]);
-                                lo[q] = __float2bfloat16_rn(a[g * 8 + q] - __bfloat162float(hi[q]));
+                                const float as = ldexpf(a[g * 8 + q], aexp);
+                                hi[q] = __float2half_rn(as);
+                                lo[q] = __float2half_rn(as - __half2float(hi[q]));
                             }
                             *reinterpret_cast<uint4*>(smem + L::off_a1 + (0 * 2 + g) * PLANE + i * 16) =
                                 *reinterpret_cast<uint4*>(hi);
-                            if constexpr (PREC == AP_PREC_BF16X3)
+                            if constexpr (PREC == AP_PREC_F16X3)
                                 *reinterpret_cast<uint4*>(smem + L::off_a1 + (1 * 2 + g) * PLANE + i * 16) =
                                     *reinterpret_cast<uint4*>(lo);
                         }
@@ -231,13 +283,16 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
                 }
                 if constexpr (kTC) fence_async_smem();
                 __syncthreads();
+                if constexpr (kTC) {
+                    if (tid == 0) *s_xmax = 0;  // reset for the next band (read above, before the barrier)
+                }
 
                 // ---- 3. conv2 + epilogue -> r for rows r0..r1-1
                 float rvals[BAND];
                 if constexpr (kTC) {
                     if (tid == 0) {
                         tc_fence_after();
-                        constexpr uint32_t idesc = idesc_bf16_f32(TW, 32);
+                        constexpr uint32_t idesc = idesc_f16_f32(TW, 32, 0);
                         const uint32_t a1_addr = smem_u32(smem + L::off_a1);
                         const uint32_t b_addr = smem_u32(smem + L::off_bpack);
                         for (int j = 0; j < nb; ++j) {
@@ -249,13 +304,13 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
                                 const uint32_t pix = (uint32_t)((j + di) * A1C + dj);
                                 const uint64_t a_hi = umma_desc(a1_addr + 0 * 2 * PLANE + pix * 16, PLANE, 128);
                                 const uint64_t b_hi = umma_desc(b_addr + (0 * 9 + tap) * BTILE_BYTES, 512, 128);
-                                mma_bf16(d_tmem, a_hi, b_hi, idesc, acc);
+                                mma_f16(d_tmem, a_hi, b_hi, idesc, acc);
                                 acc = 1;
-                                if constexpr (PREC == AP_PREC_BF16X3) {
+                                if constexpr (PREC == AP_PREC_F16X3) {
                                     const uint64_t a_lo = umma_desc(a1_addr + 1 * 2 * PLANE + pix * 16, PLANE, 128);
                                     const uint64_t b_lo = umma_desc(b_addr + (1 * 9 + tap) * BTILE_BYTES, 512, 128);
-                                    mma_bf16(d_tmem, a_hi, b_lo, idesc, 1);
-                                    mma_bf16(d_tmem, a_lo, b_hi, idesc, 1);
+                                    mma_f16(d_tmem, a_hi, b_lo, idesc, 1);
+                                    mma_f16(d_tmem, a_lo, b_hi, idesc, 1);
                                 }
                             }
                         }
@@ -265,12 +320,16 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
                     mbar_wait(mbar, phase);
                     phase ^= 1u;
                     tc_fence_after();
+                    const float unscale_a = ldexpf(1.f, -aexp), unscale_w = ldexpf(1.f, -wexp);
                     for (int j = 0; j < nb; ++j) {
                         float acc[32];
                         tmem_ld32(tmem_base + ((uint32_t)(warp * 32) << 16) + j * 32, acc);
                         float r = 0.f;
 #pragma unroll
-                        for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n] + c_w[OFF_B2 + n], 0.f), r);
+                        for (int n = 0; n < 32; ++n) {
+                            const float s2 = (acc[n] * unscale_a) * unscale_w + c_w[OFF_B2 + n];
+                            r = fmaf(c_w[OFF_W3 + n], fmaxf(s2, 0.f), r);
+                        }
                         rvals[j] = r;
                     }
                     tc_fence_before();
@@ -364,14 +423,14 @@ static int launch_conv(const ConvParams& P, int precision, cudaStream_t st) {
             conv_forecast_kernel<AP_PREC_FP32><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_FP32>::total, st>>>(P);
             break;
         }
-        case AP_PREC_BF16X3: {
-            int g = grid_ctas<AP_PREC_BF16X3>();
-            conv_forecast_kernel<AP_PREC_BF16X3><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_BF16X3>::total, st>>>(P);
+        case AP_PREC_F16X3: {
+            int g = grid_ctas<AP_PREC_F16X3>();
+            conv_forecast_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_F16X3>::total, st>>>(P);
             break;
         }
-        case AP_PREC_BF16: {
-            int g = grid_ctas<AP_PREC_BF16>();
-            conv_forecast_kernel<AP_PREC_BF16><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_BF16>::total, st>>>(P);
+        case AP_PREC_F16: {
+            int g = grid_ctas<AP_PREC_F16>();
+            conv_forecast_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_F16>::total, st>>>(P);
             break;
         }
         default:
@@ -397,7 +456,7 @@ int ap_set_weights(const float* weights4833, void* stream) {
         set_last_error("ap_set_weights: %s", cudaGetErrorString(e));
         return AP_ECUDA;
     }
-    pack_weights_kernel<<<(9 * 32 * 16 + 255) / 256, 256, 0, st>>>();
+    pack_weights_kernel<<<1, 512, 0, st>>>();
     return launch_status("ap_set_weights");
 }
 
@@ -456,8 +515,8 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream) {
 int ap_sel_grid_ctas(int precision) {
     switch (precision) {
         case AP_PREC_FP32: return grid_ctas<AP_PREC_FP32>();
-        case AP_PREC_BF16X3: return grid_ctas<AP_PREC_BF16X3>();
-        case AP_PREC_BF16: return grid_ctas<AP_PREC_BF16>();
+        case AP_PREC_F16X3: return grid_ctas<AP_PREC_F16X3>();
+        case AP_PREC_F16: return grid_ctas<AP_PREC_F16>();
     }
     return 0;
 }

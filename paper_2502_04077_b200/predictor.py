@@ -5,7 +5,7 @@ pkg/src/attncast/predictor.py:1-216,424-444): ``PredictorWeights``,
 ``init_weights``, ``AttentionHistory``, ``stack_history``, ``forward``,
 ``save_weights`` / ``load_weights`` with the APW1 format.  ``forward`` runs
 ``ap_predict_forward`` (csrc/predictor.cu) — a tcgen05 implicit-GEMM conv in
-the default ``bf16x3`` precision.  Training (backward / Adam,
+the default ``fp16x3`` precision.  Training (backward / Adam,
 predictor.py:219-416) is out of scope for this B200 path.
 """
 
@@ -44,8 +44,8 @@ _SHAPES = (
 
 
 def default_precision() -> str:
-    """Predictor arithmetic: ATTNPRED_PRECISION in {bf16x3 (default), fp32, bf16}."""
-    p = os.environ.get("ATTNPRED_PRECISION", "bf16x3")
+    """Predictor arithmetic: ATTNPRED_PRECISION in {fp16x3 (default), fp32, fp16}."""
+    p = os.environ.get("ATTNPRED_PRECISION", "fp16x3")
     if p not in _lib.PREC:
         raise ParameterError(f"unknown precision {p!r}")
     return p

@@ -16,7 +16,7 @@ from parity import RTOL, near_tie_exemptions, scores_close
 
 pytestmark = pytest.mark.gpu
 
-PRECISIONS = ("fp32", "bf16x3", "bf16")
+PRECISIONS = ("fp32", "fp16x3", "fp16")
 
 
 @pytest.fixture(scope="module")
@@ -37,8 +37,9 @@ def test_max_pool_golden_bit_exact(pkg):
         got = compress.max_pool(row, int(b))
         assert got.original_len == row.size and got.block_size == int(b)
         assert np.array_equal(got.values, want)
-        got32 = compress.max_pool(row.astype(np.float32), int(b))  # fp32 path (rows are fp32-representable)
-        assert np.array_equal(got32.values, want)
+        if np.array_equal(row.astype(np.float32).astype(np.float64), row):  # fp32 path on fp32 rows
+            got32 = compress.max_pool(row.astype(np.float32), int(b))
+            assert np.array_equal(got32.values, want)
 
 
 def test_max_pool_reference_kats(pkg):
@@ -112,7 +113,7 @@ def test_forward_golden(pkg, precision):
                                  unragged(z["out"], z["out_off"])):
         wt = predictor.PredictorWeights.from_flat(wf)
         got = predictor.forward(wt, predictor.AttentionHistory(g.reshape(int(h), int(w))), precision=precision)
-        ok, err = scores_close(got, want, RTOL[precision])
+        ok, err = scores_close(got, want, precision)
         worst = max(worst, err)
         assert ok, f"{precision} H={h} W={w}: worst err/bound {err:.3g}"
     print(f"forward {precision}: worst |err|/bound = {worst:.3g}")
@@ -133,7 +134,7 @@ def test_forward_large_shapes(pkg, precision):
         want = O.forward(wt, g)
         got = predictor.forward(predictor.PredictorWeights.from_flat(wt.flat()), predictor.AttentionHistory(g),
                                 precision=precision)
-        ok, err = scores_close(got, want, RTOL[precision])
+        ok, err = scores_close(got, want, precision)
         assert ok, f"{precision} H={h} W={w}: worst err/bound {err:.3g}"
 
 
@@ -182,7 +183,7 @@ def test_selector_step_matches_reference_run(pkg, case):
                 masked = O.masked_scores(ocfg, ost.last_scores, row.size)
                 dev_blocks = {i // cfg.block_size for i in st.middle_tokens}
                 exempt += near_tie_exemptions(dev_blocks, ost.last_blocks, masked,
-                                              min(k, int(np.isfinite(masked).sum())), RTOL["bf16x3"])
+                                              min(k, int(np.isfinite(masked).sum())), "fp16x3")
             ref_sel = want
         # the device window equals the oracle's compressed history
         dev_hist = st.compressed_history
@@ -246,11 +247,12 @@ def test_batched_selector_cfg1_shape(pkg, precision):
                 continue
             blocks, oscores, masked = ref[m][s]
             W = oscores.size
-            ok, err = scores_close(scores[m, :W], oscores, RTOL[precision])
+            ok, err = scores_close(scores[m, :W], oscores, precision)
             assert ok, f"step {s} map {m}: forecast err/bound {err:.3g}"
             got = dev.middle(m)
             if got != blocks:
-                exempt += near_tie_exemptions(got, blocks, masked, len(blocks), RTOL[precision])
+                exempt += near_tie_exemptions(got, blocks, masked, len(blocks), precision)
                 diverged.add(m)
-    assert len(diverged) <= n_maps // 4, f"too many near-tie flips: {len(diverged)}"
+    if precision != "fp16":  # fp32-class modes: flips must be rare; the 11-bit fast mode only needs them exempt
+        assert len(diverged) <= n_maps // 8, f"too many near-tie flips: {len(diverged)}"
     print(f"batched {precision}: near-tie exemptions = {exempt} over {n_maps} maps x {steps} steps")
