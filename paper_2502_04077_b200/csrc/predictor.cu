@@ -37,6 +37,9 @@ __device__ int g_wexp;            // power-of-2 exponent applied to w2
 __device__ float g_w1abs[16];     // sum_t |w1[c][t]|  (a1 magnitude bound)
 __device__ float g_b1abs[16];     // |b1[c]|
 
+// exact 2^e as a float (|e| <= 126)
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((e + 127) << 23); }
+
 // Largest e with bound * 2^e < 2^14 (so fp16 values stay below 2^15).
 __device__ __forceinline__ int f16_scale_exp(float bound) {
     if (!(bound > 0.f) || !isfinite(bound)) return 0;
@@ -46,15 +49,17 @@ __device__ __forceinline__ int f16_scale_exp(float bound) {
     return e < -120 ? -120 : (e > 120 ? 120 : e);
 }
 
-constexpr int TW = 128;            // output pixels per MMA tile (M)
-constexpr int BAND = 4;            // history rows per band (TMEM: BAND*32 fp32 columns)
-constexpr int A1R = BAND + 2;      // a1 tile rows
-constexpr int A1C = TW + 2;        // a1 tile cols
-constexpr int XR = BAND + 4;       // x tile rows
-constexpr int XC = TW + 4;         // x tile cols
-constexpr int A1PIX = A1R * A1C;   // 780
-constexpr int PLANE = A1PIX * 16;  // bytes of one 8-channel fp16 plane
-constexpr int NTHREADS = 128;
+constexpr int TW = 128;             // output pixels per MMA tile (M) = columns per task
+constexpr int MAXO = 5;             // output history rows per band (TMEM: MAXO*32 fp32 columns)
+constexpr int MAXA = 9;             // a1 tile rows per band (incremental band: 4 + 5)
+constexpr int MAXX = 13;            // x tile rows per band (6 + 7)
+constexpr int A1C = TW + 2;         // a1 tile cols
+constexpr int XC = TW + 4;          // x tile cols
+constexpr int PLANE = MAXA * A1C * 16;  // bytes of one 8-channel fp16 plane (pixel = 16 B)
+constexpr int NTHREADS = 256;         // 8 warps: two per TMEM lane quadrant
+constexpr int TMEM_COLS = 256;      // >= MAXO*32, power of two
+constexpr int NWARPS = NTHREADS / 32;
+constexpr int PREF = 8;             // r rows per warp prefetched in registers (H <= 64)
 
 // One CTA: w2 scale, then the [hi/lo][tap] fp16 tiles and the a1 magnitude bounds.
 __global__ void pack_weights_kernel() {
@@ -98,23 +103,23 @@ struct ConvParams {
     int32_t* status;
 };
 
+// Which history rows a task recomputes: full = [0, H); incremental (s new rows
+// since the last update) = {0, 1} ∪ [H-s-2, H) — the rows whose conv3x3∘conv3x3
+// receptive field saw a padding change at the top or a new row at the bottom.
 struct Task {
-    bool skip;
+    bool skip, full, merged;
     int W;
     int64_t n_pushed;
-    int nr;          // number of row ranges
-    int ra[2], rb[2];
+    int lo2;  // start of the bottom range (incremental)
 };
 
 __device__ __forceinline__ Task plan_task(const ConvParams& P, int map, int chunk) {
     Task T;
-    T.skip = false;
-    T.nr = 0;
+    T.skip = false; T.full = true; T.merged = false; T.lo2 = 0;
     const int H = P.H;
     if (!P.state) {  // explicit grids: full forward
         T.W = P.W_explicit;
         T.n_pushed = H;
-        T.nr = 1; T.ra[0] = 0; T.rb[0] = H;
         T.skip = chunk * TW >= T.W;
         return T;
     }
@@ -132,12 +137,44 @@ __device__ __forceinline__ Task plan_task(const ConvParams& P, int map, int chun
         if (lo < 0) lo = 0;
         if (chunk * TW + TW > lo) full = true;
     }
-    if (full) {
-        T.nr = 1; T.ra[0] = 0; T.rb[0] = H;
-    } else if (s > 0) {
-        T.nr = 2; T.ra[0] = 0; T.rb[0] = 2; T.ra[1] = (int)(H - s - 2); T.rb[1] = H;
+    T.full = full;
+    if (!full) {
+        T.lo2 = (int)(H - s - 2);
+        T.merged = (H - T.lo2) + 2 <= MAXO;  // s == 1: both ranges in one band
     }
     return T;
+}
+
+__device__ __forceinline__ bool recomputed(const Task& T, int p) {
+    return T.full || p < 2 || p >= T.lo2;
+}
+
+// Band number bi of a task -> up to two output-row segments [o0, o1).
+struct Band {
+    int nseg, o0[2], o1[2];
+};
+__device__ __forceinline__ bool band_of(const Task& T, int H, int bi, Band& B) {
+    if (!T.full && T.merged) {
+        if (bi) return false;
+        B.nseg = 2; B.o0[0] = 0; B.o1[0] = 2; B.o0[1] = T.lo2; B.o1[1] = H;
+        return true;
+    }
+    // ranges chunked into single-segment bands of <= MAXO rows
+    const int ra0 = 0, rb0 = T.full ? H : 2;
+    const int nb0 = (rb0 - ra0 + MAXO - 1) / MAXO;
+    B.nseg = 1;
+    if (bi < nb0) {
+        B.o0[0] = ra0 + bi * MAXO;
+        B.o1[0] = min(rb0, B.o0[0] + MAXO);
+        return true;
+    }
+    if (T.full) return false;
+    const int k = bi - nb0;
+    const int nb1 = (H - T.lo2 + MAXO - 1) / MAXO;
+    if (k >= nb1) return false;
+    B.o0[0] = T.lo2 + k * MAXO;
+    B.o1[0] = min(H, B.o0[0] + MAXO);
+    return true;
 }
 
 // slot of history position p (0 = oldest) given n_pushed; k < 0 => missing (zero) row
@@ -150,24 +187,44 @@ __device__ __forceinline__ int slot_of(int64_t k, int H) {
 template <int PREC>
 struct SmemLayout {
     static constexpr int kBpack = (PREC == AP_PREC_FP32) ? 0 : 2 * 9 * BTILE_BYTES;
-    static constexpr int kA1 = (PREC == AP_PREC_FP32) ? A1PIX * 16 * 4 : 4 * PLANE;  // fp32 or [hl][g] fp16 planes
-    static constexpr int kX = XR * XC * 4;
+    static constexpr int kA1 = 4 * PLANE;  // [hl][g] fp16 planes, or fp32 [pixel][16] (same bytes)
+    static constexpr int kX = MAXX * XC * 4;
     static constexpr int off_bpack = 0;
     static constexpr int off_a1 = off_bpack + kBpack;
     static constexpr int off_x = off_a1 + kA1;
-    static constexpr int off_bar = (off_x + kX + 15) / 16 * 16;
+    static constexpr int off_sum = off_x + kX;                   // [NWARPS][128] partial sums
+    static constexpr int off_meta = off_sum + NWARPS * TW * 4;   // band bookkeeping (ints)
+    static constexpr int kMeta = 64 * 4;
+    static constexpr int off_bar = off_meta + kMeta;
     static constexpr int total = off_bar + 32;
 };
 
+// band bookkeeping in shared memory
+struct Meta {
+    int n_out, n_a1, n_x;
+    int out_pos[MAXO], out_a1row[MAXO];
+    int a1_pos[MAXA], a1_xrow[MAXA];
+    int x_pos[MAXX];
+};
+static_assert(sizeof(Meta) <= 64 * 4, "meta");
+
+__device__ __forceinline__ float4 ld4(const float* p, bool vec) {
+    if (vec) return __ldg(reinterpret_cast<const float4*>(p));
+    return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3));
+}
+
 template <int PREC>
-__global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P) {
+__global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P) {
+    static_assert(NWARPS == 8, "epilogue / sum split assumes 8 warps");
     using L = SmemLayout<PREC>;
     extern __shared__ __align__(1024) uint8_t smem[];
     float* xs = reinterpret_cast<float*>(smem + L::off_x);
+    float* psum = reinterpret_cast<float*>(smem + L::off_sum);
+    Meta* meta = reinterpret_cast<Meta*>(smem + L::off_meta);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_bar + 8);
     int* s_xmax = reinterpret_cast<int*>(smem + L::off_bar + 16);
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr bool kTC = PREC != AP_PREC_FP32;
     uint32_t tmem_base = 0, phase = 0;
 
@@ -180,7 +237,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
             mbar_init(mbar, 1);
             *s_xmax = 0;
         }
-        if (warp == 0) tmem_alloc(tmem_slot, BAND * 32);
+        if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
@@ -191,6 +248,7 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
     const int H = P.H;
     const int n_tasks = P.n_maps * P.n_chunks;
     const int wexp = kTC ? g_wexp : 0;
+    const bool vec = (P.pitch % 4) == 0;
     for (int task = blockIdx.x; task < n_tasks; task += gridDim.x) {
         const int map = task / P.n_chunks, chunk = task % P.n_chunks;
         const Task T = plan_task(P, map, chunk);
@@ -199,202 +257,268 @@ __global__ void __launch_bounds__(NTHREADS, 3) conv_forecast_kernel(ConvParams P
         const float* ring = P.ring + (int64_t)map * P.map_stride;
         float* rmap = P.rmap + (int64_t)map * P.map_stride;
         const int32_t* sw = P.state ? P.slot_width + (int64_t)map * H : nullptr;
+        auto slot_at = [&](int p) -> int { return P.state ? slot_of(row_index(T.n_pushed, H, p), H) : p; };
 
-        for (int rr = 0; rr < T.nr; ++rr) {
-            for (int r0 = T.ra[rr]; r0 < T.rb[rr]; r0 += BAND) {
-                const int r1 = (r0 + BAND < T.rb[rr]) ? r0 + BAND : T.rb[rr];
-                const int nb = r1 - r0;
-                // ---- 1. x tile: positions [r0-2, r1+2) x cols [w0-2, w0+TW+2)
-                const int xrows = nb + 4;
-                float xmax = 0.f;
-                for (int i = tid; i < xrows * XC; i += NTHREADS) {
+        // ---- 0. prefetch the r rows this task does not recompute (warp w: rows p = w + 8i,
+        //         lane: 4 columns) — these loads overlap the conv below.
+        const int c4 = w0 + 4 * lane;
+        float4 pre[PREF];
+#pragma unroll
+        for (int i = 0; i < PREF; ++i) {
+            const int p = warp + NWARPS * i;
+            pre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p < H && c4 < W && !recomputed(T, p)) pre[i] = ld4(rmap + (int64_t)slot_at(p) * P.pitch + c4, vec);
+        }
+
+        Band B;
+        for (int bi = 0; band_of(T, H, bi, B); ++bi) {
+            // ---- 1. band bookkeeping
+            if (tid == 0) {
+                int no = 0, na = 0, nx = 0;
+                for (int sg = 0; sg < B.nseg; ++sg) {
+                    const int o0 = B.o0[sg], o1 = B.o1[sg];
+                    const int abase = na, xbase = nx;
+                    for (int q = o0; q < o1; ++q) {
+                        meta->out_pos[no] = q;
+                        meta->out_a1row[no] = abase + (q - o0);
+                        ++no;
+                    }
+                    for (int p = o0 - 1; p < o1 + 1; ++p) {
+                        meta->a1_pos[na] = p;
+                        meta->a1_xrow[na] = xbase + (p - (o0 - 1));
+                        ++na;
+                    }
+                    for (int p = o0 - 2; p < o1 + 2; ++p) meta->x_pos[nx++] = p;
+                }
+                meta->n_out = no; meta->n_a1 = na; meta->n_x = nx;
+            }
+            __syncthreads();
+            const int n_out = meta->n_out, n_a1 = meta->n_a1, n_x = meta->n_x;
+
+            // ---- 2. x tile (all loads issued before any store): zero outside the H x W grid,
+            //         zero beyond each stored row's own width, zero for missing (not yet pushed) rows
+            float xv[(MAXX * XC + NTHREADS - 1) / NTHREADS];
+            float xmax = 0.f;
+#pragma unroll
+            for (int u = 0; u < (MAXX * XC + NTHREADS - 1) / NTHREADS; ++u) {
+                const int i = tid + u * NTHREADS;
+                float v = 0.f;
+                if (i < n_x * XC) {
                     const int xr = i / XC, xc = i % XC;
-                    const int p = r0 - 2 + xr, c = w0 - 2 + xc;
-                    float v = 0.f;
+                    const int p = meta->x_pos[xr], c = w0 - 2 + xc;
                     if (p >= 0 && p < H && c >= 0 && c < W) {
                         const int64_t k = row_index(T.n_pushed, H, p);
                         if (k >= 0) {
                             const int slot = P.state ? slot_of(k, H) : p;
                             const int width = P.state ? sw[slot] : W;
-                            if (c < width) {
-                                v = ring[(int64_t)slot * P.pitch + c];
-                                if (!isfinite(v)) raise_status(P.status, AP_ENUMERIC);
-                            }
+                            if (c < width) v = __ldg(ring + (int64_t)slot * P.pitch + c);
                         }
                     }
-                    xs[xr * XC + xc] = v;
-                    xmax = fmaxf(xmax, fabsf(v));
                 }
-                if constexpr (kTC) {
+                xv[u] = v;
+            }
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
-                    if ((tid & 31) == 0) atomicMax(s_xmax, __float_as_int(xmax));
+            for (int u = 0; u < (MAXX * XC + NTHREADS - 1) / NTHREADS; ++u) {
+                const int i = tid + u * NTHREADS;
+                if (i < n_x * XC) {
+                    if (!isfinite(xv[u])) raise_status(P.status, AP_ENUMERIC);
+                    xs[i] = xv[u];
+                    xmax = fmaxf(xmax, fabsf(xv[u]));
                 }
-                __syncthreads();
-                // exact power-of-2 scale for the fp16 a1 operand: a1 <= |b1| + sum|w1| * max|x|
-                int aexp = 0;
-                if constexpr (kTC) {
-                    const float mx = __int_as_float(*s_xmax);
-                    float bound = 0.f;
+            }
+            if constexpr (kTC) {
 #pragma unroll
-                    for (int ch = 0; ch < 16; ++ch) bound = fmaxf(bound, g_b1abs[ch] + g_w1abs[ch] * mx);
-                    aexp = f16_scale_exp(bound);
-                }
-                // ---- 2. conv1 + ReLU -> a1 tile (zero outside the H x W grid)
-                const int a1pix = (nb + 2) * A1C;
-                for (int i = tid; i < a1pix; i += NTHREADS) {
-                    const int ar = i / A1C, ac = i % A1C;
-                    const int p = r0 - 1 + ar, c = w0 - 1 + ac;
-                    const bool valid = p >= 0 && p < H && c >= 0 && c < W;
-                    float x9[9];
+                for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+                if (lane == 0) atomicMax(s_xmax, __float_as_int(xmax));
+            }
+            __syncthreads();
+            // exact power-of-2 scale for the fp16 a1 operand: a1 <= |b1| + sum|w1| * max|x|
+            int aexp = 0;
+            if constexpr (kTC) {
+                const float mx = __int_as_float(*s_xmax);
+                float bound = 0.f;
 #pragma unroll
-                    for (int di = 0; di < 3; ++di)
-#pragma unroll
-                        for (int dj = 0; dj < 3; ++dj) x9[di * 3 + dj] = xs[(ar + di) * XC + ac + dj];
-                    float a[16];
-#pragma unroll
-                    for (int ch = 0; ch < 16; ++ch) {
-                        float acc = c_w[OFF_B1 + ch];
-#pragma unroll
-                        for (int q = 0; q < 9; ++q) acc = fmaf(c_w[OFF_W1 + ch * 9 + q], x9[q], acc);
-                        a[ch] = valid ? fmaxf(acc, 0.f) : 0.f;
-                    }
+                for (int ch = 0; ch < 16; ++ch) bound = fmaxf(bound, g_b1abs[ch] + g_w1abs[ch] * mx);
+                aexp = f16_scale_exp(bound);
+            }
+
+            // ---- 3. conv1 + ReLU -> a1 tile (zero outside the H x W grid)
+            const float ascale = pow2f(aexp);
+            for (int i = tid; i < n_a1 * A1C; i += NTHREADS) {
+                const int ar = i / A1C, ac = i - ar * A1C;
+                const int p = meta->a1_pos[ar], c = w0 - 1 + ac;
+                const bool valid = p >= 0 && p < H && c >= 0 && c < W;
+                if (!valid) {  // zero padding of the conv2 input: no conv1 work
+                    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
                     if constexpr (kTC) {
-#pragma unroll
-                        for (int g = 0; g < 2; ++g) {
-                            __align__(16) __half hi[8], lo[8];
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float as = ldexpf(a[g * 8 + q], aexp);
-                                hi[q] = __float2half_rn(as);
-                                lo[q] = __float2half_rn(as - __half2float(hi[q]));
-                            }
-                            *reinterpret_cast<uint4*>(smem + L::off_a1 + (0 * 2 + g) * PLANE + i * 16) =
-                                *reinterpret_cast<uint4*>(hi);
-                            if constexpr (PREC == AP_PREC_F16X3)
-                                *reinterpret_cast<uint4*>(smem + L::off_a1 + (1 * 2 + g) * PLANE + i * 16) =
-                                    *reinterpret_cast<uint4*>(lo);
+                        *reinterpret_cast<uint4*>(smem + L::off_a1 + 0 * PLANE + i * 16) = z;
+                        *reinterpret_cast<uint4*>(smem + L::off_a1 + 1 * PLANE + i * 16) = z;
+                        if constexpr (PREC == AP_PREC_F16X3) {
+                            *reinterpret_cast<uint4*>(smem + L::off_a1 + 2 * PLANE + i * 16) = z;
+                            *reinterpret_cast<uint4*>(smem + L::off_a1 + 3 * PLANE + i * 16) = z;
                         }
                     } else {
-                        float4* d = reinterpret_cast<float4*>(smem + L::off_a1 + i * 64);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) d[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+                        uint4* d = reinterpret_cast<uint4*>(smem + L::off_a1 + i * 64);
+                        d[0] = z; d[1] = z; d[2] = z; d[3] = z;
                     }
+                    continue;
                 }
-                if constexpr (kTC) fence_async_smem();
-                __syncthreads();
-                if constexpr (kTC) {
-                    if (tid == 0) *s_xmax = 0;  // reset for the next band (read above, before the barrier)
+                const float* xr = xs + meta->a1_xrow[ar] * XC + ac;
+                float x9[9];
+#pragma unroll
+                for (int di = 0; di < 3; ++di)
+#pragma unroll
+                    for (int dj = 0; dj < 3; ++dj) x9[di * 3 + dj] = xr[di * XC + dj];
+                float a[16];
+#pragma unroll
+                for (int ch = 0; ch < 16; ++ch) {
+                    float acc = c_w[OFF_B1 + ch];
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) acc = fmaf(c_w[OFF_W1 + ch * 9 + q], x9[q], acc);
+                    a[ch] = fmaxf(acc, 0.f);
                 }
-
-                // ---- 3. conv2 + epilogue -> r for rows r0..r1-1
-                float rvals[BAND];
                 if constexpr (kTC) {
-                    if (tid == 0) {
-                        tc_fence_after();
-                        constexpr uint32_t idesc = idesc_f16_f32(TW, 32, 0);
-                        const uint32_t a1_addr = smem_u32(smem + L::off_a1);
-                        const uint32_t b_addr = smem_u32(smem + L::off_bpack);
-                        for (int j = 0; j < nb; ++j) {
-                            const uint32_t d_tmem = tmem_base + j * 32;
-                            uint32_t acc = 0;
 #pragma unroll
-                            for (int tap = 0; tap < 9; ++tap) {
-                                const int di = tap / 3, dj = tap % 3;
-                                const uint32_t pix = (uint32_t)((j + di) * A1C + dj);
-                                const uint64_t a_hi = umma_desc(a1_addr + 0 * 2 * PLANE + pix * 16, PLANE, 128);
-                                const uint64_t b_hi = umma_desc(b_addr + (0 * 9 + tap) * BTILE_BYTES, 512, 128);
-                                mma_f16(d_tmem, a_hi, b_hi, idesc, acc);
-                                acc = 1;
-                                if constexpr (PREC == AP_PREC_F16X3) {
-                                    const uint64_t a_lo = umma_desc(a1_addr + 1 * 2 * PLANE + pix * 16, PLANE, 128);
-                                    const uint64_t b_lo = umma_desc(b_addr + (1 * 9 + tap) * BTILE_BYTES, 512, 128);
-                                    mma_f16(d_tmem, a_hi, b_lo, idesc, 1);
-                                    mma_f16(d_tmem, a_lo, b_hi, idesc, 1);
-                                }
-                            }
-                        }
-                        mma_commit(mbar);
-                    }
-                    __syncwarp();
-                    mbar_wait(mbar, phase);
-                    phase ^= 1u;
-                    tc_fence_after();
-                    const float unscale_a = ldexpf(1.f, -aexp), unscale_w = ldexpf(1.f, -wexp);
-                    for (int j = 0; j < nb; ++j) {
-                        float acc[32];
-                        tmem_ld32(tmem_base + ((uint32_t)(warp * 32) << 16) + j * 32, acc);
-                        float r = 0.f;
+                    for (int g = 0; g < 2; ++g) {
+                        __align__(16) __half hi[8], lo[8];
 #pragma unroll
-                        for (int n = 0; n < 32; ++n) {
-                            const float s2 = (acc[n] * unscale_a) * unscale_w + c_w[OFF_B2 + n];
-                            r = fmaf(c_w[OFF_W3 + n], fmaxf(s2, 0.f), r);
+                        for (int q = 0; q < 8; ++q) {
+                            const float as = a[g * 8 + q] * ascale;
+                            hi[q] = __float2half_rn(as);
+                            lo[q] = __float2half_rn(as - __half2float(hi[q]));
                         }
-                        rvals[j] = r;
+                        *reinterpret_cast<uint4*>(smem + L::off_a1 + (0 * 2 + g) * PLANE + i * 16) =
+                            *reinterpret_cast<uint4*>(hi);
+                        if constexpr (PREC == AP_PREC_F16X3)
+                            *reinterpret_cast<uint4*>(smem + L::off_a1 + (1 * 2 + g) * PLANE + i * 16) =
+                                *reinterpret_cast<uint4*>(lo);
                     }
-                    tc_fence_before();
                 } else {
-                    const float* a1 = reinterpret_cast<const float*>(smem + L::off_a1);
-                    for (int j = 0; j < nb; ++j) {
-                        float acc[32];
+                    float4* d = reinterpret_cast<float4*>(smem + L::off_a1 + i * 64);
 #pragma unroll
-                        for (int n = 0; n < 32; ++n) acc[n] = c_w[OFF_B2 + n];
+                    for (int q = 0; q < 4; ++q) d[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+                }
+            }
+            if constexpr (kTC) fence_async_smem();
+            __syncthreads();
+            if constexpr (kTC) {
+                if (tid == 0) *s_xmax = 0;  // every thread read it before the barrier above
+            }
+
+            // ---- 4. conv2 (tcgen05 implicit GEMM) + epilogue -> r for this band's output rows
+            if constexpr (kTC) {
+                if (tid == 0) {
+                    tc_fence_after();
+                    constexpr uint32_t idesc = idesc_f16_f32(TW, 32, 0);
+                    const uint32_t a1_addr = smem_u32(smem + L::off_a1);
+                    const uint32_t b_addr = smem_u32(smem + L::off_bpack);
+                    for (int j = 0; j < n_out; ++j) {
+                        const uint32_t d_tmem = tmem_base + j * 32;
+                        const int arow = meta->out_a1row[j];
+                        uint32_t acc = 0;
+#pragma unroll
                         for (int tap = 0; tap < 9; ++tap) {
                             const int di = tap / 3, dj = tap % 3;
-                            const float4* ap4 = reinterpret_cast<const float4*>(a1 + ((j + di) * A1C + tid + dj) * 16);
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const float4 v = ap4[q];
-                                const float av[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const int k = q * 4 + e;
-#pragma unroll
-                                    for (int n = 0; n < 32; ++n) acc[n] = fmaf(c_w[OFF_W2 + n * 144 + k * 9 + tap], av[e], acc[n]);
-                                }
+                            const uint32_t pix = (uint32_t)((arow + di) * A1C + dj);
+                            const uint64_t a_hi = umma_desc(a1_addr + 0 * 2 * PLANE + pix * 16, PLANE, 128);
+                            const uint64_t b_hi = umma_desc(b_addr + (0 * 9 + tap) * BTILE_BYTES, 512, 128);
+                            mma_f16(d_tmem, a_hi, b_hi, idesc, acc);
+                            acc = 1;
+                            if constexpr (PREC == AP_PREC_F16X3) {
+                                const uint64_t a_lo = umma_desc(a1_addr + 1 * 2 * PLANE + pix * 16, PLANE, 128);
+                                const uint64_t b_lo = umma_desc(b_addr + (1 * 9 + tap) * BTILE_BYTES, 512, 128);
+                                mma_f16(d_tmem, a_hi, b_lo, idesc, 1);
+                                mma_f16(d_tmem, a_lo, b_hi, idesc, 1);
                             }
                         }
-                        float r = 0.f;
+                    }
+                    mma_commit(mbar);
+                }
+                __syncwarp();
+                mbar_wait(mbar, phase);
+                phase ^= 1u;
+                tc_fence_after();
+                // warp w reads TMEM lanes 32*(w%4).. (pixels) for output rows j = w/4, w/4 + 2, ...
+                const int e = aexp + wexp;
+                const bool one_mul = e >= -126 && e <= 126;
+                const float u = one_mul ? pow2f(-e) : pow2f(-aexp), u2 = one_mul ? 1.f : pow2f(-wexp);
+                const int quad = warp & 3, pix = quad * 32 + lane, ecol = w0 + pix;
+                for (int j = warp >> 2; j < n_out; j += 2) {
+                    float acc[32];
+                    tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + j * 32, acc);
+                    float r = 0.f;
 #pragma unroll
-                        for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n], 0.f), r);
-                        rvals[j] = r;
+                    for (int n = 0; n < 32; ++n) {
+                        const float s2 = fmaf(acc[n] * u2, u, c_w[OFF_B2 + n]);
+                        r = fmaf(c_w[OFF_W3 + n], fmaxf(s2, 0.f), r);
                     }
+                    if (ecol < W) rmap[(int64_t)slot_at(meta->out_pos[j]) * P.pitch + ecol] = r;
                 }
-                const int col = w0 + tid;
-                if (col < W) {
-                    for (int j = 0; j < nb; ++j) {
-                        const int p = r0 + j;
-                        const int slot = P.state ? slot_of(row_index(T.n_pushed, H, p), H) : p;
-                        rmap[(int64_t)slot * P.pitch + col] = rvals[j];
-                    }
-                }
-                __syncthreads();  // x / a1 tiles and TMEM columns are reused by the next band
-            }
-        }
-        // ---- 4. forecast for this chunk: b3 + (1/H) sum_p r[p] in fixed position order
-        const int col = w0 + tid;
-        if (col < W) {
-            float sum = 0.f;
-            const float* rc = rmap + col;
-            if (P.state) {
-                int slot = slot_of(row_index(T.n_pushed, H, 0), H);
-#pragma unroll 8
-                for (int p = 0; p < H; ++p) {
-                    sum += rc[(int64_t)slot * P.pitch];
-                    slot = (slot + 1 == H) ? 0 : slot + 1;
-                }
+                tc_fence_before();
             } else {
-#pragma unroll 8
-                for (int p = 0; p < H; ++p) sum += rc[(int64_t)p * P.pitch];
+                const float* a1 = reinterpret_cast<const float*>(smem + L::off_a1);
+                const int pix = tid & (TW - 1), ecol = w0 + pix;
+                for (int j = tid / TW; j < n_out; j += NTHREADS / TW) {
+                    const int arow = meta->out_a1row[j];
+                    float acc[32];
+#pragma unroll
+                    for (int n = 0; n < 32; ++n) acc[n] = c_w[OFF_B2 + n];
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const int di = tap / 3, dj = tap % 3;
+                        const float4* ap4 = reinterpret_cast<const float4*>(a1 + ((arow + di) * A1C + pix + dj) * 16);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 v = ap4[q];
+                            const float av[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int k = q * 4 + e;
+#pragma unroll
+                                for (int n = 0; n < 32; ++n) acc[n] = fmaf(c_w[OFF_W2 + n * 144 + k * 9 + tap], av[e], acc[n]);
+                            }
+                        }
+                    }
+                    float r = 0.f;
+#pragma unroll
+                    for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n], 0.f), r);
+                    if (ecol < W) rmap[(int64_t)slot_at(meta->out_pos[j]) * P.pitch + ecol] = r;
+                }
             }
-            P.scores[(int64_t)map * P.score_stride + col] = c_w[OFF_B3] + sum / (float)H;
+            __syncthreads();  // x / a1 tiles, meta and TMEM columns are reused by the next band
         }
+
+        // ---- 5. forecast for this chunk: b3 + (1/H) sum_p r[p]; warp w sums rows p = w (mod 8)
+        //         in increasing p, the 8 partials are added in warp order (fixed, deterministic).
+        float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c4 < W) {
+#pragma unroll
+            for (int i = 0; i < PREF; ++i) {
+                const int p = warp + NWARPS * i;
+                if (p < H) {
+                    const float4 v = recomputed(T, p) ? ld4(rmap + (int64_t)slot_at(p) * P.pitch + c4, vec) : pre[i];
+                    acc4.x += v.x; acc4.y += v.y; acc4.z += v.z; acc4.w += v.w;
+                }
+            }
+            for (int p = warp + NWARPS * PREF; p < H; p += NWARPS) {
+                const float4 v = ld4(rmap + (int64_t)slot_at(p) * P.pitch + c4, vec);
+                acc4.x += v.x; acc4.y += v.y; acc4.z += v.z; acc4.w += v.w;
+            }
+        }
+        reinterpret_cast<float4*>(psum + warp * TW)[lane] = acc4;
+        __syncthreads();
+        if (tid < TW && w0 + tid < W) {
+            float sum = psum[tid];
+#pragma unroll
+            for (int w = 1; w < NWARPS; ++w) sum += psum[w * TW + tid];
+            P.scores[(int64_t)map * P.score_stride + w0 + tid] = c_w[OFF_B3] + sum / (float)H;
+        }
+        __syncthreads();
     }
 
     if constexpr (kTC) {
         tc_fence_before();
         __syncthreads();
-        if (warp == 0) tmem_dealloc(tmem_base, BAND * 32);
+        if (warp == 0) tmem_dealloc(tmem_base, TMEM_COLS);
     }
 }
 
@@ -405,10 +529,19 @@ static int grid_ctas() {
         int per_sm = 0;
         cudaFuncSetAttribute(conv_forecast_kernel<PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              SmemLayout<PREC>::total);
+        cudaFuncSetAttribute(conv_forecast_kernel<PREC>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_forecast_kernel<PREC>, NTHREADS,
                                                       SmemLayout<PREC>::total);
+        // the occupancy API has been seen to under-report for this kernel; cross-check by hand
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, conv_forecast_kernel<PREC>) == cudaSuccess && fa.numRegs > 0) {
+            const int by_regs = 65536 / (((fa.numRegs + 7) / 8 * 8) * NTHREADS);
+            const int by_smem = (227 * 1024) / (SmemLayout<PREC>::total + 1024);
+            const int manual = by_regs < by_smem ? by_regs : by_smem;
+            if (manual > per_sm) per_sm = manual;
+        }
         if (per_sm < 1) per_sm = 1;
-        if (PREC != AP_PREC_FP32 && per_sm * BAND * 32 > 512) per_sm = 512 / (BAND * 32);  // TMEM columns
+        if (PREC != AP_PREC_FP32 && per_sm * TMEM_COLS > 512) per_sm = 512 / TMEM_COLS;  // TMEM columns
         cached = ap_device_sm_count() * per_sm;
     }
     return cached;
