@@ -166,6 +166,43 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream);
 /* Number of persistent CTAs the predictor kernels use (for reporting). */
 int ap_sel_grid_ctas(int precision);
 
+/* ---------------------------------------------------------------------------
+ * Decode attention for one layer (kernel 4).  No reference implementation
+ * exists; the math follows attntap/model.py:70-74 and the
+ * selection structure selector.py:122-149.  head_dim 128, bf16 q/K/V,
+ * 16-token blocks; K/V cache laid out [seq][kv_head][t_max][128].
+ * seq_len[s] = number of keys the current query attends (t, incl. itself).
+ * Workspaces: partial = n_seq*n_q_heads*n_splits*130 floats;
+ * bmax = n_seq*n_q_heads*w_max floats, initialised to -inf once.
+ * ------------------------------------------------------------------------- */
+typedef struct ap_attn_layer {
+    int32_t n_seq, n_q_heads, n_kv_heads, head_dim, t_max, n_splits, block, w_max;
+    const void* q;          /* bf16 [n_seq][n_q_heads][128]           */
+    const void* k_cache;    /* bf16 [n_seq][n_kv_heads][t_max][128]   */
+    const void* v_cache;    /* bf16 [n_seq][n_kv_heads][t_max][128]   */
+    const int32_t* seq_len; /* [n_seq]                                */
+    void* out;              /* bf16 [n_seq][n_q_heads][128]           */
+    float* lse;             /* [n_seq][n_q_heads] log2-domain LSE, may be NULL */
+    float* partial;
+    float* bmax;
+} ap_attn_layer;
+
+/* Dense decode attention over keys [0, t) (with_v = 1: output + LSE, the
+ * full-attention comparator and the first decode step) and/or the
+ * calibration pass (emit = 1): every block's max logit -> the map's
+ * compressed dense row exp(blockmax - LSE) = max_pool(softmax row, b)
+ * appended to the selector ring (selector.py:112-120).  K-only when
+ * with_v = 0.  map(s, h) = s*maps_per_seq + map_base + h/group. */
+int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, int32_t map_base,
+                  int32_t maps_per_seq, int32_t group, int emit, void* stream);
+
+/* Sparse decode attention over the map's current selection (sink ∪ local ∪
+ * middle blocks, selector.py:122-149), gathering only those 16-token
+ * blocks.  emit = 1 appends the observed compressed row (sparse_renorm:
+ * exp(blockmax - LSE_S) on touched blocks, 0 elsewhere) to the ring. */
+int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                   int32_t group, int emit, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,19 @@ class Selector(ctypes.Structure):
     ]
 
 
+class AttnLayerDesc(ctypes.Structure):
+    """ap_attn_layer (include/attnpred.h)."""
+
+    _fields_ = [
+        ("n_seq", ctypes.c_int32), ("n_q_heads", ctypes.c_int32), ("n_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32), ("t_max", ctypes.c_int32), ("n_splits", ctypes.c_int32),
+        ("block", ctypes.c_int32), ("w_max", ctypes.c_int32),
+        ("q", ctypes.c_void_p), ("k_cache", ctypes.c_void_p), ("v_cache", ctypes.c_void_p),
+        ("seq_len", ctypes.c_void_p), ("out", ctypes.c_void_p), ("lse", ctypes.c_void_p),
+        ("partial", ctypes.c_void_p), ("bmax", ctypes.c_void_p),
+    ]
+
+
 MAP_STATE_BYTES = ctypes.sizeof(MapState)  # 56
 
 _P = ctypes.c_void_p
@@ -73,6 +86,10 @@ SIGNATURES = {
     "ap_sel_push_compressed": (ctypes.c_int, [ctypes.POINTER(Selector), _P, _I64, _I64, ctypes.c_int, _P]),
     "ap_sel_step": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.c_int, _P]),
     "ap_sel_grid_ctas": (ctypes.c_int, [ctypes.c_int]),
+    "ap_attn_dense": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.c_int, ctypes.POINTER(Selector),
+                                     _I32, _I32, _I32, ctypes.c_int, _P]),
+    "ap_attn_sparse": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.POINTER(Selector), _I32, _I32, _I32,
+                                      ctypes.c_int, _P]),
 }
 
 _lib = None

@@ -1,0 +1,447 @@
+// Kernel (4a) sparse decode attention over the selected blocks and (4b) the
+// dense pass used for calibration rows and for the full-attention comparator.
+//
+// Semantics (SURVEY §8c "kernels with no reference implementation"):
+//   scores = q . k / sqrt(d), softmax, . V          (attntap/model.py:70-74)
+//   selection S = sink ∪ local ∪ middle blocks      (selector.py:122-149)
+//   calibration row = max_pool(dense softmax row, b) (selector.py:112-117),
+//     computed as exp(blockmax_logit - LSE) — exact by monotonicity of exp;
+//   observed (fed-back) row on non-calibration steps: sparse_renorm mode —
+//     probability under the sparse softmax over S at selected positions,
+//     0 elsewhere (DESIGN.md §Observed-row semantics).
+// Both kernels push the compressed row straight into the selector's history
+// ring (the append of selector.py:117-120), so compression never re-reads a
+// t-length row from HBM.
+//
+// Layout: K/V cache per layer [seq][kv_head][t_max][128] bf16 — a 16-token
+// block of one head is 4 KiB contiguous.  A warp processes one block: lane =
+// (token parity, 8-dim slice), 16-byte loads, half-warp shuffle reductions.
+// Flash-decoding split over blocks; a combine kernel merges the splits.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace ap {
+
+constexpr int HD = 128;                 // head dim
+constexpr int ATT_THREADS = 256;        // 8 warps
+constexpr int ATT_WARPS = ATT_THREADS / 32;
+constexpr float LOG2E = 1.4426950408889634f;
+
+struct AttnParams {
+    int32_t n_seq, n_q_heads, n_kv_heads, t_max, n_splits, block;
+    const __nv_bfloat16* q;       // [S][Hq][D]
+    const __nv_bfloat16* k;       // [S][Hkv][t_max][D]
+    const __nv_bfloat16* v;
+    const int32_t* seq_len;       // [S]
+    __nv_bfloat16* out;           // [S][Hq][D]
+    float* lse;                   // [S][Hq] log2 units (nullable)
+    float* partial;               // [S][Hq][n_splits][D+2]
+    float* bmax;                  // [S][Hq][w_max] log2-unit block max logits (-inf = untouched)
+    int32_t w_max;
+    // selector binding
+    ap_selector sel;
+    int32_t map_base, maps_per_seq, group;  // map(s, h) = s*maps_per_seq + map_base + h/group
+};
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float2 t = __bfloat1622float2(p[i]);
+        f[2 * i] = t.x;
+        f[2 * i + 1] = t.y;
+    }
+}
+
+// Per-warp running softmax state for NH heads; lane holds 8 dims (slice) of
+// the accumulators for the tokens of its half-warp.
+template <int NH, bool WITH_V>
+struct WarpState {
+    float m[NH], l[NH], acc[NH][8];
+    __device__ void init() {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            m[h] = -INFINITY;
+            l[h] = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[h][i] = 0.f;
+        }
+    }
+};
+
+// Process one 16-token block j for NH heads.  take(p) decides token membership.
+// Writes the block max (log2 logits) of each head through bm_out(h, value) when EMIT.
+template <int NH, bool WITH_V, bool EMIT, typename Take, typename BmOut>
+__device__ __forceinline__ void process_block(const __nv_bfloat16* kh, const __nv_bfloat16* vh, int64_t j, int b,
+                                              const float (&qf)[NH][8], WarpState<NH, WITH_V>& st, Take take,
+                                              BmOut bm_out) {
+    const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
+    float s[NH][8];
+    uint4 kv[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        const int64_t p = j * b + jj * 2 + half;
+        kv[jj] = __ldg(reinterpret_cast<const uint4*>(kh + p * HD + sub * 8));
+    }
+    uint4 vv[8];
+    if constexpr (WITH_V) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int64_t p = j * b + jj * 2 + half;
+            vv[jj] = __ldg(reinterpret_cast<const uint4*>(vh + p * HD + sub * 8));
+        }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        float kf[8];
+        bf16x8_to_f32(kv[jj], kf);
+        const int64_t p = j * b + jj * 2 + half;
+        const bool sel = take(p);
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            float d = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d = fmaf(qf[h][i], kf[i], d);
+            d += __shfl_xor_sync(0xffffffffu, d, 8);
+            d += __shfl_xor_sync(0xffffffffu, d, 4);
+            d += __shfl_xor_sync(0xffffffffu, d, 2);
+            d += __shfl_xor_sync(0xffffffffu, d, 1);
+            s[h][jj] = sel ? d : -INFINITY;
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        float mx = s[h][0];
+#pragma unroll
+        for (int jj = 1; jj < 8; ++jj) mx = fmaxf(mx, s[h][jj]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        if constexpr (EMIT) bm_out(h, mx);
+        if (mx == -INFINITY) continue;  // nothing selected in this block (uniform across the warp)
+        const float m_new = fmaxf(st.m[h], mx);
+        const float corr = exp2f(st.m[h] - m_new);
+        float psum = 0.f;
+        float pj[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            pj[jj] = exp2f(s[h][jj] - m_new);
+            psum += pj[jj];
+        }
+        psum += __shfl_xor_sync(0xffffffffu, psum, 16);
+        st.l[h] = st.l[h] * corr + psum;
+        st.m[h] = m_new;
+        if constexpr (WITH_V) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) st.acc[h][i] *= corr;
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                if (s[h][jj] == -INFINITY) continue;  // unselected / beyond t: never touch its V (may be garbage)
+                float vf[8];
+                bf16x8_to_f32(vv[jj], vf);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) st.acc[h][i] = fmaf(pj[jj], vf[i], st.acc[h][i]);
+            }
+        }
+    }
+}
+
+// Merge the 8 warps' states of a CTA and write the split partial (m, l, acc[128]).
+template <int NH, bool WITH_V>
+__device__ void write_partial(WarpState<NH, WITH_V>& st, float* smem, float* part_base /*[NH] stride*/,
+                              int64_t head_stride) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane >> 4, sub = lane & 15;
+    // combine the two half-warps (same dims, different tokens): they share m and l already
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st.acc[h][i] += __shfl_xor_sync(0xffffffffu, st.acc[h][i], 16);
+    // smem: [warp][h][2 + 128]
+    float* w = smem + warp * NH * (HD + 2);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        if (lane == 0) {
+            w[h * (HD + 2) + 0] = st.m[h];
+            w[h * (HD + 2) + 1] = st.l[h];
+        }
+        if (WITH_V && half == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[h * (HD + 2) + 2 + sub * 8 + i] = st.acc[h][i];
+        }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < NH * (HD + 2); idx += ATT_THREADS) {
+        const int h = idx / (HD + 2), e = idx % (HD + 2);
+        float M = -INFINITY;
+        for (int ww = 0; ww < ATT_WARPS; ++ww) M = fmaxf(M, smem[(ww * NH + h) * (HD + 2)]);
+        float val = 0.f;
+        if (e == 0) {
+            val = M;
+        } else if (M != -INFINITY) {
+            for (int ww = 0; ww < ATT_WARPS; ++ww) {
+                const float mw = smem[(ww * NH + h) * (HD + 2)];
+                if (mw == -INFINITY) continue;
+                val += smem[(ww * NH + h) * (HD + 2) + e] * exp2f(mw - M);
+            }
+        }
+        if (e >= 2 && !WITH_V) continue;
+        part_base[h * head_stride + e] = val;
+    }
+}
+
+// ------------------------------------------------------------------ dense
+// grid (n_splits, Hkv, S); NH = Hq/Hkv q-heads per CTA share every K/V load.
+template <int NH, bool WITH_V, bool EMIT>
+__global__ void __launch_bounds__(ATT_THREADS) dense_partial_kernel(AttnParams P) {
+    extern __shared__ float sm_att[];
+    const int split = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane & 15;
+    const int64_t t = P.seq_len[s];
+    const int b = P.block;
+    const int64_t nblk = (t + b - 1) / b;
+    const int64_t blk_per_split = (((int64_t)P.t_max + b - 1) / b + P.n_splits - 1) / P.n_splits;
+    const int64_t j0 = split * blk_per_split, j1 = min(nblk, j0 + blk_per_split);
+    const __nv_bfloat16* kh = P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
+    const __nv_bfloat16* vh = P.v + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
+    const int h0 = kvh * NH;
+    const float qscale = LOG2E * rsqrtf((float)HD);
+    float qf[NH][8];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(P.q + ((int64_t)s * P.n_q_heads + h0 + h) * HD + sub * 8));
+        bf16x8_to_f32(u, qf[h]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qf[h][i] *= qscale;
+    }
+    WarpState<NH, WITH_V> st;
+    st.init();
+    float* bm = P.bmax + ((int64_t)s * P.n_q_heads + h0) * P.w_max;
+    for (int64_t j = j0 + warp; j < j1; j += ATT_WARPS) {
+        process_block<NH, WITH_V, EMIT>(kh, vh, j, b, qf, st, [&](int64_t p) { return p < t; },
+                                        [&](int h, float v) { if (lane == 0) bm[h * (int64_t)P.w_max + j] = v; });
+    }
+    float* part = P.partial + (((int64_t)s * P.n_q_heads + h0) * P.n_splits + split) * (HD + 2);
+    write_partial<NH, WITH_V>(st, sm_att, part, (int64_t)P.n_splits * (HD + 2));
+}
+
+// ------------------------------------------------------------------ sparse
+// grid (n_splits, maps per seq-layer, S); the NH = group q-heads of one map share its selection.
+template <int NH, bool EMIT>
+__global__ void __launch_bounds__(ATT_THREADS) sparse_partial_kernel(AttnParams P) {
+    extern __shared__ float sm_att[];
+    const int split = blockIdx.x, g = blockIdx.y, s = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane & 15;
+    const int64_t t = P.seq_len[s];
+    const int b = P.block;
+    const int map = s * P.maps_per_seq + P.map_base + g;
+    const ap_map_state ms = P.sel.state[map];
+    // selection over the row of length t (selector.py:122-147 with next_len = t)
+    const int64_t sink_end = P.sel.sink < t ? P.sel.sink : t;
+    const int64_t local_start = t - P.sel.local > 0 ? t - P.sel.local : 0;
+    const int64_t sb = (sink_end + b - 1) / b;
+    const int64_t eb = (t + b - 1) / b;
+    int64_t lb = local_start / b;
+    if (lb < sb) lb = sb;
+    const int n_local = (int)(eb - lb);
+    const int n_mid = ms.n_mid;
+    const int n_units = (int)sb + n_local + n_mid;
+    const int per = (n_units + P.n_splits - 1) / P.n_splits;
+    const int u0 = split * per, u1 = min(n_units, u0 + per);
+    const int32_t* mid = P.sel.mid_blocks + (int64_t)map * (P.sel.k_mid > 0 ? P.sel.k_mid : 1);
+    const int h0 = g * NH;
+    const int kvh = h0 / (P.n_q_heads / P.n_kv_heads);
+    const __nv_bfloat16* kh = P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
+    const __nv_bfloat16* vh = P.v + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
+    const float qscale = LOG2E * rsqrtf((float)HD);
+    float qf[NH][8];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(P.q + ((int64_t)s * P.n_q_heads + h0 + h) * HD + sub * 8));
+        bf16x8_to_f32(u, qf[h]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qf[h][i] *= qscale;
+    }
+    WarpState<NH, true> st;
+    st.init();
+    const int64_t mid_clip = ms.mid_clip;
+    float* bm = P.bmax + ((int64_t)s * P.n_q_heads + h0) * P.w_max;
+    for (int u = u0 + warp; u < u1; u += ATT_WARPS) {
+        int64_t j;
+        bool is_mid = false;
+        if (u < sb) {
+            j = u;
+        } else if (u < sb + n_local) {
+            j = lb + (u - sb);
+        } else {
+            j = mid[u - sb - n_local];
+            is_mid = true;
+        }
+        auto take = [&](int64_t p) {
+            if (p >= t) return false;
+            if (p < sink_end || p >= local_start) return true;
+            return is_mid && p < mid_clip;
+        };
+        process_block<NH, true, EMIT>(kh, vh, j, b, qf, st, take,
+                                      [&](int h, float v) { if (lane == 0) bm[h * (int64_t)P.w_max + j] = v; });
+    }
+    float* part = P.partial + (((int64_t)s * P.n_q_heads + h0) * P.n_splits + split) * (HD + 2);
+    write_partial<NH, true>(st, sm_att, part, (int64_t)P.n_splits * (HD + 2));
+}
+
+// ------------------------------------------------------------------ combine
+// grid (S * Hq / group): merge the splits of every head of one map; write out
+// (bf16) and lse; when EMIT, write the group's compressed row
+// max_h exp2(bm_h[j] - lse_h) (0 where untouched) into the ring slot and
+// advance the map's ring state (selector.py:117-120).
+template <bool WITH_V, bool EMIT>
+__global__ void __launch_bounds__(ATT_THREADS) combine_kernel(AttnParams P) {
+    __shared__ float s_lse[8];
+    __shared__ float s_w[8][64];
+    const int gm = blockIdx.x;
+    const int maps_per_layer = P.n_q_heads / P.group;
+    const int s = gm / maps_per_layer, g = gm % maps_per_layer;
+    const int64_t t = P.seq_len[s];
+    for (int hh = 0; hh < P.group; ++hh) {
+        const int h = g * P.group + hh;
+        const float* part = P.partial + ((int64_t)s * P.n_q_heads + h) * P.n_splits * (HD + 2);
+        // global max and weights per split (n_splits <= 64)
+        float M = -INFINITY;
+        for (int sp = 0; sp < P.n_splits; ++sp) M = fmaxf(M, part[sp * (HD + 2)]);
+        if (threadIdx.x < P.n_splits) {
+            const float m = part[threadIdx.x * (HD + 2)];
+            s_w[hh][threadIdx.x] = (m == -INFINITY) ? 0.f : exp2f(m - M);
+        }
+        __syncthreads();
+        float L = 0.f;
+        for (int sp = 0; sp < P.n_splits; ++sp) L += part[sp * (HD + 2) + 1] * s_w[hh][sp];
+        if (threadIdx.x == 0) {
+            const float lse = M + log2f(L);
+            s_lse[hh] = lse;
+            if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h] = lse;
+        }
+        if constexpr (WITH_V) {
+            for (int d = threadIdx.x; d < HD; d += ATT_THREADS) {
+                float o = 0.f;
+                for (int sp = 0; sp < P.n_splits; ++sp) o += part[sp * (HD + 2) + 2 + d] * s_w[hh][sp];
+                P.out[((int64_t)s * P.n_q_heads + h) * HD + d] = __float2bfloat16_rn(o / L);
+            }
+        }
+        __syncthreads();
+    }
+    if constexpr (EMIT) {
+        const int map = s * P.maps_per_seq + P.map_base + g;
+        const ap_map_state ms = P.sel.state[map];
+        const int H = P.sel.history;
+        const int slot = (int)(ms.n_pushed % H);
+        const int64_t W = (t + P.block - 1) / P.block;
+        float* dst = P.sel.ring + ((int64_t)map * H + slot) * P.sel.w_max;
+        float* bm0 = P.bmax + ((int64_t)s * P.n_q_heads + g * P.group) * P.w_max;
+        for (int64_t j = threadIdx.x; j < W; j += ATT_THREADS) {
+            float v = 0.f;
+            for (int hh = 0; hh < P.group; ++hh) {
+                const float lg = bm0[hh * (int64_t)P.w_max + j];
+                if (lg != -INFINITY) v = fmaxf(v, exp2f(lg - s_lse[hh]));
+                bm0[hh * (int64_t)P.w_max + j] = -INFINITY;  // untouched marker for the next step
+            }
+            dst[j] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            ap_map_state st = ms;
+            P.sel.slot_width[(int64_t)map * H + slot] = (int32_t)W;
+            st.n_pushed += 1;
+            st.row_len = t;
+            st.width = (int32_t)W;
+            P.sel.state[map] = st;
+        }
+    }
+}
+
+template <int NH>
+static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream_t st) {
+    dim3 grid(P.n_splits, P.n_kv_heads, P.n_seq);
+    const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
+    if (with_v && emit) dense_partial_kernel<NH, true, true><<<grid, ATT_THREADS, sm, st>>>(P);
+    else if (with_v) dense_partial_kernel<NH, true, false><<<grid, ATT_THREADS, sm, st>>>(P);
+    else dense_partial_kernel<NH, false, true><<<grid, ATT_THREADS, sm, st>>>(P);
+}
+
+template <int NH>
+static void launch_sparse(const AttnParams& P, bool emit, cudaStream_t st) {
+    dim3 grid(P.n_splits, P.n_q_heads / NH, P.n_seq);
+    const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
+    if (emit) sparse_partial_kernel<NH, true><<<grid, ATT_THREADS, sm, st>>>(P);
+    else sparse_partial_kernel<NH, false><<<grid, ATT_THREADS, sm, st>>>(P);
+}
+
+static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                       int32_t group, AttnParams& P) {
+    AP_REQUIRE(a && a->head_dim == HD, AP_EPARAM, "head_dim must be 128");
+    AP_REQUIRE(a->n_q_heads % a->n_kv_heads == 0, AP_EPARAM, "n_q_heads must be a multiple of n_kv_heads");
+    AP_REQUIRE(a->n_splits >= 1 && a->n_splits <= 64, AP_EPARAM, "n_splits must be in [1, 64]");
+    AP_REQUIRE(a->block == 16, AP_EPARAM, "attention kernels assume 16-token blocks");
+    AP_REQUIRE(a->t_max % a->block == 0, AP_EPARAM, "t_max must be a multiple of the block size");
+    P.n_seq = a->n_seq; P.n_q_heads = a->n_q_heads; P.n_kv_heads = a->n_kv_heads; P.t_max = a->t_max;
+    P.n_splits = a->n_splits; P.block = a->block;
+    P.q = (const __nv_bfloat16*)a->q; P.k = (const __nv_bfloat16*)a->k_cache; P.v = (const __nv_bfloat16*)a->v_cache;
+    P.seq_len = a->seq_len; P.out = (__nv_bfloat16*)a->out; P.lse = a->lse; P.partial = a->partial;
+    P.bmax = a->bmax; P.w_max = a->w_max;
+    if (sel) P.sel = *sel; else memset(&P.sel, 0, sizeof(P.sel));
+    P.map_base = map_base; P.maps_per_seq = maps_per_seq; P.group = group < 1 ? 1 : group;
+    const int G = a->n_q_heads / a->n_kv_heads;
+    AP_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, AP_EPARAM, "q-heads per kv-head must be 1, 2, 4 or 8");
+    AP_REQUIRE(G % P.group == 0, AP_EPARAM, "selection group must divide the GQA group");
+    return AP_OK;
+}
+
+}  // namespace ap
+
+using namespace ap;
+
+extern "C" {
+
+int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                  int32_t group, int emit, void* stream) {
+    AttnParams P;
+    int rc = make_params(a, sel, map_base, maps_per_seq, group, P);
+    if (rc != AP_OK) return rc;
+    AP_REQUIRE(with_v || emit, AP_EPARAM, "dense pass without V must emit the calibration row");
+    AP_REQUIRE(!emit || sel, AP_EPARAM, "emit needs a selector");
+    cudaStream_t st = as_stream(stream);
+    const int G = a->n_q_heads / a->n_kv_heads;
+    switch (G) {
+        case 1: launch_dense<1>(P, with_v, emit, st); break;
+        case 2: launch_dense<2>(P, with_v, emit, st); break;
+        case 4: launch_dense<4>(P, with_v, emit, st); break;
+        default: launch_dense<8>(P, with_v, emit, st); break;
+    }
+    rc = launch_status("dense_partial_kernel");
+    if (rc != AP_OK) return rc;
+    const int n_comb = a->n_seq * a->n_q_heads / P.group;
+    if (with_v && emit) combine_kernel<true, true><<<n_comb, ATT_THREADS, 0, st>>>(P);
+    else if (with_v) combine_kernel<true, false><<<n_comb, ATT_THREADS, 0, st>>>(P);
+    else combine_kernel<false, true><<<n_comb, ATT_THREADS, 0, st>>>(P);
+    return launch_status("combine_kernel");
+}
+
+int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                   int32_t group, int emit, void* stream) {
+    AttnParams P;
+    int rc = make_params(a, sel, map_base, maps_per_seq, group, P);
+    if (rc != AP_OK) return rc;
+    AP_REQUIRE(sel != nullptr, AP_EPARAM, "sparse attention needs a selector");
+    cudaStream_t st = as_stream(stream);
+    switch (P.group) {
+        case 1: launch_sparse<1>(P, emit, st); break;
+        case 2: launch_sparse<2>(P, emit, st); break;
+        case 4: launch_sparse<4>(P, emit, st); break;
+        default: launch_sparse<8>(P, emit, st); break;
+    }
+    rc = launch_status("sparse_partial_kernel");
+    if (rc != AP_OK) return rc;
+    const int n_comb = a->n_seq * a->n_q_heads / P.group;
+    if (emit) combine_kernel<true, true><<<n_comb, ATT_THREADS, 0, st>>>(P);
+    else combine_kernel<true, false><<<n_comb, ATT_THREADS, 0, st>>>(P);
+    return launch_status("combine_kernel");
+}
+
+}  // extern "C"
