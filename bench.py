@@ -1,0 +1,343 @@
+"""Benchmark: decode tok/s at 32K context with a 1K-token budget (BASELINE.json configs[1]).
+
+Workload (N=1): LLaMA-3.1-8B-shape model, random-init bf16 weights, synthetic
+N(0,1) KV cache prefilled to 32,768 tokens, batch 1, budget B=1024 (b=16,
+H=64, M=5, sink=local=64).  One "step" = one decode token of the whole model
+through the AttentionPredictor path: sparse attention over the predicted
+blocks (+ the dense calibration pass every M-th step), observed-row emission
+into every history ring, and one batched forecast + top-k for all layers and
+heads.  Steps are CUDA-graph replays with device-resident positions.
+
+Reported (one JSON line on rank 0):
+  value     decode tok/s, device-timed (CUDA events, K steps, max over ranks)
+  e2e       same metric through the host API: per step the input token is
+            copied H2D from pinned memory and the sampled token read back D2H
+  roofline  the fused forecast + top-k launch (ap_sel_step), HBM-bound:
+            algorithmic bytes per launch / CUDA-event launch time vs the
+            measured copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the CPU oracle's selector.step per (layer, head) map at the
+            same shape, timed on this host (bounded sample, extrapolated)
+  dense_tok_s   the full-attention comparator arm on the same weights/KV
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (replicas: weak scaling)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = "decode tok/s @32K ctx, 1K-token budget; predict+top-k us/layer; % HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="llama-3.1-8b")
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--budget", type=int, default=1024)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--group", choices=["head", "kv"], default="head",
+                    help="selection map per q-head (reference semantics) or per KV-head group")
+    ap.add_argument("--precision", default="fp16x3")
+    ap.add_argument("--no-dense", action="store_true", help="skip the full-attention comparator arm")
+    ap.add_argument("--cpu-sample", type=int, default=48, help="oracle map-steps timed for cpu_baseline")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self._stop = gpu, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+def profiled_traffic():
+    p = ROOT / "profiles" / "roofline_traffic.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_rate(ctx: int, budget: int, n_map_steps: int, seed: int = 0):
+    """Time the oracle's selector.step (selector.py:91-154: max_pool + forward + mask + topk) for one
+    (layer, head) map at context ctx, H=64, b=16 on this host.  Returns (seconds per map-step, cores)."""
+    import numpy as np
+    from oracle import hotpath as O
+    rng = np.random.default_rng(seed)
+    cfg = O.Config(budget=budget)
+    w = O.init_weights(0)
+    prefill = [rng.dirichlet(np.full(ctx - 63 + i, 0.05)).astype(np.float32) for i in range(63)]
+    st = O.init_state(cfg, prefill)
+    rows = [rng.dirichlet(np.full(ctx + 1 + i, 0.05)).astype(np.float32) for i in range(n_map_steps)]
+    t0 = time.perf_counter()
+    for r in rows:
+        O.step(st, cfg, w, r, full_row=r)
+    dt = (time.perf_counter() - t0) / n_map_steps
+    cores = len(os.sched_getaffinity(0))
+    return dt, cores
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world):
+    import torch
+    from paper_2502_04077_b200 import _lib
+    from paper_2502_04077_b200.decode import SHAPES, DecodeEngine
+    from paper_2502_04077_b200.selector import SelectorConfig
+
+    shape = SHAPES[args.model]
+    G = shape.n_q_heads // shape.n_kv_heads
+    group = 1 if args.group == "head" else G
+    cfg = SelectorConfig(budget=args.budget)
+    total_steps = args.warmup + args.steps
+    eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
+                       precision=args.precision, seed=rank)
+    eng.init_history()
+    eng.step(use_graph=False)  # first decode token: dense attention + emission, no prior selection
+    torch.cuda.synchronize()
+
+    def timed_steps(n):
+        barrier(world)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        variants = [eng.step() for _ in range(n)]
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / 1e3, variants
+
+    eng.capture_all()
+    for _ in range(args.warmup):
+        eng.step()
+    gpu_id = torch.cuda.current_device()
+    with ClockSampler(gpu_id) as clk:
+        elapsed, variants = timed_steps(args.steps)
+    elapsed = max_over_ranks(elapsed, world)
+    value = args.batch * args.steps * world / elapsed
+    launches = sum(eng.kernels_per_step(v) for v in variants)
+
+    # e2e through the host API: token in (pinned H2D), token out (D2H), every step
+    host_in = torch.zeros(args.batch, dtype=torch.int64).pin_memory()
+    host_out = torch.zeros(args.batch, dtype=torch.int64).pin_memory()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.tok.copy_(host_in, non_blocking=True)
+        eng.step()
+        host_out.copy_(eng.tok, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        host_in.copy_(host_out)
+    e2e_elapsed = max_over_ranks(time.perf_counter() - t0, world)
+    e2e = {"value": args.batch * args.steps * world / e2e_elapsed, "unit": "tok/s",
+           "h2d_bytes_per_step": 8 * args.batch, "d2h_bytes_per_step": 8 * args.batch}
+
+    # roofline of the fused forecast + top-k launch, in its steady-state form: one new row per map
+    # since the last update (incremental), width unchanged.  Decode state is snapshotted and restored.
+    snap = eng._snapshot()
+    ring, rmap = eng.sel.ring.clone(), eng.sel.rmap.clone()
+    st = eng.sel.states()
+    t_now = int(st["row_len"].max())
+    comp = torch.rand(eng.sel.n_maps, eng.sel.w_max, device="cuda") ** 8
+    reps = 20
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for i in range(reps):
+        eng._restore(snap)
+        eng.sel.ring.copy_(ring)
+        eng.sel.rmap.copy_(rmap)
+        eng.sel.push_compressed(comp, t_now)
+        ev[i][0].record()
+        eng.sel.step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    sel_us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in ev)
+    eng._restore(snap)
+    eng.sel.ring.copy_(ring)
+    eng.sel.rmap.copy_(rmap)
+    del ring, rmap
+    n_maps = eng.sel.n_maps
+    W = int(st["width"].max())
+    H, K = cfg.history, cfg.middle_blocks
+    b_alg = n_maps * ((H + 1) * W * 4 + 4 * K)  # history window + new row + block ids, per launch
+    peak, peak_kind = measured_peak()
+    achieved = b_alg / (sel_us * 1e-6) / 1e9
+    traffic = profiled_traffic().get(f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "ap_sel_step (conv_forecast_kernel + sel_topk_kernel)",
+                "us_per_launch": round(sel_us, 2), "us_per_layer": round(sel_us / shape.n_layers, 3),
+                "algorithmic_bytes_per_launch": b_alg}
+
+    dense = None
+    if not args.no_dense:
+        eng.set_mode("dense")
+        eng.capture_all()
+        for _ in range(args.warmup):
+            eng.step()
+        d_elapsed, _ = timed_steps(args.steps)
+        d_elapsed = max_over_ranks(d_elapsed, world)
+        dense = args.batch * args.steps * world / d_elapsed
+
+    cpu = None
+    if rank == 0 and world == 1:
+        dt, cores = cpu_oracle_rate(args.ctx, args.budget, args.cpu_sample)
+        per_token = dt * n_maps
+        cpu = {"value": round(args.batch / per_token, 6), "unit": "tok/s", "cores": cores, "kind": "port",
+               "sample": f"{args.cpu_sample} oracle selector.step map-steps (max_pool+forward+mask+topk, "
+                         f"H=64, W={-(-args.ctx // 16)}) x {n_maps} maps per token, extrapolated; "
+                         f"OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}",
+               "s_per_map_step": round(dt, 4)}
+
+    plain = sum(1 for v in variants if v == "plain")
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) KV)",
+        "config": {"workload": f"{shape.name} decode, ctx {args.ctx}, budget {args.budget}, batch {args.batch}/GPU",
+                   "model_shape": shape.name, "ctx": args.ctx, "budget": args.budget, "block": 16, "history": 64,
+                   "calibration_period": 5, "batch_per_gpu": args.batch, "selection": args.group,
+                   "forecaster_precision": args.precision, "parallelism": f"replicas x{world}",
+                   "steps_plain_vs_calibration": [plain, len(variants) - plain],
+                   "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+        "dense_tok_s": None if dense is None else round(dense, 2),
+        "sparse_over_dense": None if dense is None else round(value / dense, 4),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2502_04077_b200.decode import SHAPES
+    shape = SHAPES[args.model]
+    G = shape.n_q_heads // shape.n_kv_heads
+    maps = args.batch * shape.n_layers * (shape.n_q_heads if args.group == "head" else shape.n_kv_heads)
+    del G
+    # warm-up then K steps; each step = one oracle map-step (a bounded sample of one token's 1024 map-steps)
+    cpu_oracle_rate(args.ctx, args.budget, max(1, args.warmup))
+    dt, cores = cpu_oracle_rate(args.ctx, args.budget, args.steps, seed=1)
+    value = args.batch / (dt * maps)
+    out = {"metric": METRIC, "value": round(value, 6), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(dt * maps * 1e3, 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic Dirichlet attention rows",
+           "impl": "reference",
+           "config": {"workload": f"{shape.name} decode, ctx {args.ctx}, budget {args.budget}, batch {args.batch}",
+                      "selection": args.group, "maps_per_token": maps},
+           "cpu_baseline": {"value": round(value, 6), "unit": "tok/s", "cores": cores, "kind": "port",
+                            "sample": f"{args.steps} oracle selector.step map-steps per run, x{maps} maps/token"},
+           "e2e": {"value": round(value, 6), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world = dist_init()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -89,10 +89,11 @@ int ap_topk(const void* values, int dtype, int64_t n_rows, int64_t row_stride, i
             int32_t* out_ids, int64_t out_stride, int32_t* out_count, int32_t* status, void* stream);
 
 /* predictor.forward — predictor.py:185-216 on explicit H x W grids (fp32,
- * row-major, grid i at grids + i*grid_stride).  out: W fp32 per grid.
+ * rows row_pitch floats apart (multiple of 4, >= W), grid i at
+ * grids + i*grid_stride, 16-byte aligned).  out: W fp32 per grid.
  * rscratch: n_grids*grid_stride fp32 workspace (per-row contributions). */
-int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W, int64_t grid_stride,
-                       float* out, int64_t out_stride, float* rscratch, int precision,
+int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W, int32_t row_pitch,
+                       int64_t grid_stride, float* out, int64_t out_stride, float* rscratch, int precision,
                        int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------------------
@@ -116,7 +117,7 @@ typedef struct ap_selector {
     int32_t n_maps;
     int32_t history;          /* H   (SelectorConfig.history)            */
     int32_t block;            /* b   (SelectorConfig.block_size)         */
-    int32_t w_max;            /* ring / r-map row pitch in blocks       */
+    int32_t w_max;            /* ring / r-map row pitch in blocks (multiple of 4) */
     int32_t k_mid;            /* SelectorConfig.middle_blocks           */
     int32_t sink;             /* SelectorConfig.sink_tokens             */
     int32_t local;            /* SelectorConfig.local_tokens            */
@@ -202,6 +203,23 @@ int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, in
  * exp(blockmax - LSE_S) on touched blocks, 0 elsewhere) to the ring. */
 int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
                    int32_t group, int emit, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Decode-engine helpers around the path (not reference functions: the
+ * reference has no model; these exist so a whole LLaMA-shape decode step runs
+ * from one CUDA graph).  bf16 tensors, row-major.
+ * ------------------------------------------------------------------------- */
+/* residual (if non-NULL) += x; y = rmsnorm(residual or x) * weight */
+int ap_rmsnorm(const void* x, void* residual, const void* weight, void* y, int32_t rows, int32_t dim, float eps,
+               void* stream);
+/* qkv [n_seq][(Hq+2Hkv)*128] -> rotated q_out [n_seq][Hq][128]; rotated k and v appended to the
+ * caches at position seq_len[s]-1 */
+int ap_rope_append(const void* qkv, int32_t n_seq, int32_t n_q_heads, int32_t n_kv_heads, const int32_t* seq_len,
+                   void* q_out, void* k_cache, void* v_cache, int32_t t_max, float theta, void* stream);
+/* out [rows][ffn] = silu(gate_up[:, :ffn]) * gate_up[:, ffn:] */
+int ap_silu_mul(const void* gate_up, void* out, int32_t rows, int32_t ffn, void* stream);
+/* seq_len[i] += by */
+int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream);
 
 #ifdef __cplusplus
 }

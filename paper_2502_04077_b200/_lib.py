@@ -80,7 +80,7 @@ SIGNATURES = {
     "ap_max_pool": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I64, _I32, _P, ctypes.c_int, _I64, _P]),
     "ap_expand_indices": (ctypes.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _P]),
     "ap_topk": (ctypes.c_int, [_P, ctypes.c_int, _I64, _I64, _I32, _I32, _P, _I64, _P, _P, _P]),
-    "ap_predict_forward": (ctypes.c_int, [_P, _I32, _I32, _I32, _I64, _P, _I64, _P, ctypes.c_int, _P, _P]),
+    "ap_predict_forward": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _P, _I64, _P, ctypes.c_int, _P, _P]),
     "ap_sel_reset": (ctypes.c_int, [ctypes.POINTER(Selector), _P]),
     "ap_sel_push_rows": (ctypes.c_int, [ctypes.POINTER(Selector), _P, ctypes.c_int, _I64, _I64, ctypes.c_int, _P]),
     "ap_sel_push_compressed": (ctypes.c_int, [ctypes.POINTER(Selector), _P, _I64, _I64, ctypes.c_int, _P]),
@@ -90,6 +90,10 @@ SIGNATURES = {
                                      _I32, _I32, _I32, ctypes.c_int, _P]),
     "ap_attn_sparse": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.POINTER(Selector), _I32, _I32, _I32,
                                       ctypes.c_int, _P]),
+    "ap_rmsnorm": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, ctypes.c_float, _P]),
+    "ap_rope_append": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _I32, ctypes.c_float, _P]),
+    "ap_silu_mul": (ctypes.c_int, [_P, _P, _I32, _I32, _P]),
+    "ap_advance": (ctypes.c_int, [_P, _I32, _I32, _P]),
 }
 
 _lib = None

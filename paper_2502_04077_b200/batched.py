@@ -49,6 +49,7 @@ class BatchedSelector:
             raise ParameterError(f"unknown precision {precision!r}")
         torch = D.torch()
         dev = device or D.device()
+        w_max = -(-int(w_max) // 4) * 4  # 16-byte ring rows (bulk-copy alignment)
         self.cfg = cfg
         self.n_maps, self.w_max, self.precision = int(n_maps), int(w_max), precision
         H = cfg.history

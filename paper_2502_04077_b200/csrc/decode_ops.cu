@@ -1,0 +1,144 @@
+// Small fused ops of the decode engine around the critical-token path:
+// residual-add + RMSNorm, RoPE + KV-cache append, SiLU-gate, sequence advance.
+// (The model's GEMMs are plain library GEMMs; attention and selection are the
+// hot path in attention.cu / predictor.cu / topk.cu.)
+#include "common.cuh"
+
+namespace ap {
+
+// h = x + residual (if residual), y = h * rsqrt(mean(h^2) + eps) * w.  One CTA per row.
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      __nv_bfloat16* __restrict__ residual, const __nv_bfloat16* __restrict__ w,
+                                                      __nv_bfloat16* __restrict__ y, int D, float eps) {
+    __shared__ float red[8];
+    const int row = blockIdx.x;
+    const __nv_bfloat16* xr = x + (int64_t)row * D;
+    __nv_bfloat16* rr = residual ? residual + (int64_t)row * D : nullptr;
+    float ss = 0.f;
+    // D is a multiple of 8 * 256 for the shapes we serve (4096); fall back to scalar otherwise
+    for (int i = threadIdx.x * 8; i < D; i += 256 * 8) {
+        uint4 u = *reinterpret_cast<const uint4*>(xr + i);
+        __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+        if (rr) {
+            uint4 ru = *reinterpret_cast<const uint4*>(rr + i);
+            __nv_bfloat162* rp = reinterpret_cast<__nv_bfloat162*>(&ru);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float2 a = __bfloat1622float2(p[k]), b = __bfloat1622float2(rp[k]);
+                p[k] = __floats2bfloat162_rn(a.x + b.x, a.y + b.y);
+            }
+            *reinterpret_cast<uint4*>(rr + i) = u;  // updated residual stream
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float2 a = __bfloat1622float2(p[k]);
+            ss += a.x * a.x + a.y * a.y;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot += red[k];
+    const float inv = rsqrtf(tot / (float)D + eps);
+    const __nv_bfloat16* src = rr ? rr + 0 : xr;
+    for (int i = threadIdx.x * 8; i < D; i += 256 * 8) {
+        uint4 u = *reinterpret_cast<const uint4*>(src + i);
+        uint4 wu = *reinterpret_cast<const uint4*>(w + i);
+        __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+        __nv_bfloat162* wp = reinterpret_cast<__nv_bfloat162*>(&wu);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float2 a = __bfloat1622float2(p[k]), b = __bfloat1622float2(wp[k]);
+            p[k] = __floats2bfloat162_rn(a.x * inv * b.x, a.y * inv * b.y);
+        }
+        *reinterpret_cast<uint4*>(y + (int64_t)row * D + i) = u;
+    }
+}
+
+// qkv: [S][(Hq + 2*Hkv) * 128] -> q_out [S][Hq][128] (rotated), K/V cache at position seq_len[s]-1.
+// Rotary embedding with rotate-half pairing (i, i+64), theta^(-2i/128).
+__global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq, int Hkv,
+                                   const int32_t* __restrict__ seq_len, __nv_bfloat16* __restrict__ q_out,
+                                   __nv_bfloat16* __restrict__ k_cache, __nv_bfloat16* __restrict__ v_cache, int t_max,
+                                   float theta) {
+    const int s = blockIdx.y;
+    const int head = blockIdx.x;  // [0, Hq + 2*Hkv)
+    const int i = threadIdx.x;    // 0..63
+    const int pos = seq_len[s] - 1;
+    const __nv_bfloat16* src = qkv + ((int64_t)s * (Hq + 2 * Hkv) + head) * 128;
+    float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + 64]);
+    if (head < Hq + Hkv) {
+        const float inv_freq = exp2f(-(float)(2 * i) / 128.f * log2f(theta));
+        float sn, cs;
+        sincosf((float)pos * inv_freq, &sn, &cs);
+        const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
+        x1 = y1;
+        x2 = y2;
+    }
+    __nv_bfloat16* dst;
+    if (head < Hq) {
+        dst = q_out + ((int64_t)s * Hq + head) * 128;
+    } else if (head < Hq + Hkv) {
+        dst = k_cache + (((int64_t)s * Hkv + (head - Hq)) * t_max + pos) * 128;
+    } else {
+        dst = v_cache + (((int64_t)s * Hkv + (head - Hq - Hkv)) * t_max + pos) * 128;
+    }
+    dst[i] = __float2bfloat16_rn(x1);
+    dst[i + 64] = __float2bfloat16_rn(x2);
+}
+
+// gu: [S][2*F] (gate | up) -> out [S][F] = silu(gate) * up
+__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int F,
+                                int64_t n) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = idx / F, f = idx % F;
+        const float g = __bfloat162float(gu[s * 2 * F + f]), u = __bfloat162float(gu[s * 2 * F + F + f]);
+        out[idx] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * u);
+    }
+}
+
+__global__ void advance_kernel(int32_t* seq_len, int n, int by) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) seq_len[i] += by;
+}
+
+}  // namespace ap
+
+using namespace ap;
+
+extern "C" {
+
+int ap_rmsnorm(const void* x, void* residual, const void* weight, void* y, int32_t rows, int32_t dim, float eps,
+               void* stream) {
+    AP_REQUIRE(dim % 8 == 0, AP_EPARAM, "dim must be a multiple of 8");
+    rmsnorm_kernel<<<rows, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)residual,
+                                                        (const __nv_bfloat16*)weight, (__nv_bfloat16*)y, dim, eps);
+    return launch_status("ap_rmsnorm");
+}
+
+int ap_rope_append(const void* qkv, int32_t n_seq, int32_t n_q_heads, int32_t n_kv_heads, const int32_t* seq_len,
+                   void* q_out, void* k_cache, void* v_cache, int32_t t_max, float theta, void* stream) {
+    dim3 grid(n_q_heads + 2 * n_kv_heads, n_seq);
+    rope_append_kernel<<<grid, 64, 0, as_stream(stream)>>>((const __nv_bfloat16*)qkv, n_q_heads, n_kv_heads, seq_len,
+                                                           (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
+                                                           (__nv_bfloat16*)v_cache, t_max, theta);
+    return launch_status("ap_rope_append");
+}
+
+int ap_silu_mul(const void* gate_up, void* out, int32_t rows, int32_t ffn, void* stream) {
+    const int64_t n = (int64_t)rows * ffn;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    silu_mul_kernel<<<blocks, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)gate_up, (__nv_bfloat16*)out, ffn, n);
+    return launch_status("ap_silu_mul");
+}
+
+int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream) {
+    advance_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(seq_len, n, by);
+    return launch_status("ap_advance");
+}
+
+}  // extern "C"

@@ -50,14 +50,19 @@ __device__ __forceinline__ int f16_scale_exp(float bound) {
 }
 
 constexpr int TW = 128;             // output pixels per MMA tile (M) = columns per task
-constexpr int MAXO = 5;             // output history rows per band (TMEM: MAXO*32 fp32 columns)
-constexpr int MAXA = 9;             // a1 tile rows per band (incremental band: 4 + 5)
-constexpr int MAXX = 13;            // x tile rows per band (6 + 7)
+constexpr int MAXO = 3;             // output history rows per band (TMEM: MAXO*32 fp32 accumulator columns)
+constexpr int MAXA = MAXO + 2;      // a1 tile rows per band
+constexpr int MAXX = MAXO + 4;      // x tile rows per band
 constexpr int A1C = TW + 2;         // a1 tile cols
-constexpr int XC = TW + 4;          // x tile cols
+
 constexpr int PLANE = MAXA * A1C * 16;  // bytes of one 8-channel fp16 plane (pixel = 16 B)
 constexpr int NTHREADS = 256;         // 8 warps: two per TMEM lane quadrant
-constexpr int TMEM_COLS = 256;      // >= MAXO*32, power of two
+// TMEM per CTA (2 CTAs/SM): conv2 A-operand ring [3 a1 rows][3 dj shifts][hi, lo] x 8 columns
+// (tcgen05.cp'd from the smem a1 tile) + MAXO x 32 fp32 accumulator columns.
+constexpr int TMEM_COLS = 256;
+constexpr int RING_COLS = 3 * 3 * 2 * 8;   // 144
+constexpr int ACC_BASE = RING_COLS;        // accumulators at [144, 144 + 96)
+static_assert(ACC_BASE + MAXO * 32 <= TMEM_COLS, "TMEM budget");
 constexpr int NWARPS = NTHREADS / 32;
 constexpr int PREF = 8;             // r rows per warp prefetched in registers (H <= 64)
 
@@ -72,11 +77,16 @@ __global__ void pack_weights_kernel() {
     __syncthreads();
     const int e = f16_scale_exp(s_max);
     if (threadIdx.x == 0) g_wexp = e;
-    if (threadIdx.x < 16) {
-        float a = 0.f;
-        for (int q = 0; q < 9; ++q) a += fabsf(c_w[OFF_W1 + threadIdx.x * 9 + q]);
-        g_w1abs[threadIdx.x] = a;
-        g_b1abs[threadIdx.x] = fabsf(c_w[OFF_B1 + threadIdx.x]);
+    if (threadIdx.x == 0) {  // a1 <= max_c |b1_c| + max_c sum_t |w1_ct| * max|x|  (slot 0 holds the maxima)
+        float wm = 0.f, bm = 0.f;
+        for (int c = 0; c < 16; ++c) {
+            float a = 0.f;
+            for (int q = 0; q < 9; ++q) a += fabsf(c_w[OFF_W1 + c * 9 + q]);
+            wm = fmaxf(wm, a);
+            bm = fmaxf(bm, fabsf(c_w[OFF_B1 + c]));
+        }
+        g_w1abs[0] = wm;
+        g_b1abs[0] = bm;
     }
     __half* base = reinterpret_cast<__half*>(g_bpack);
     for (int idx = threadIdx.x; idx < 9 * 32 * 16; idx += blockDim.x) {
@@ -140,7 +150,7 @@ __device__ __forceinline__ Task plan_task(const ConvParams& P, int map, int chun
     T.full = full;
     if (!full) {
         T.lo2 = (int)(H - s - 2);
-        T.merged = (H - T.lo2) + 2 <= MAXO;  // s == 1: both ranges in one band
+        T.merged = false;  // separate bands keep the TMEM footprint within 256 columns
     }
     return T;
 }
@@ -184,33 +194,122 @@ __device__ __forceinline__ int slot_of(int64_t k, int H) {
     return (int)(r < 0 ? r + H : r);
 }
 
+constexpr int XC4 = TW + 8;  // x tile columns [w0-4, w0+TW+4): 16-byte aligned for cp.async.bulk
+
+// Everything a band needs, computed once by thread 0 and published in shared memory.
+struct BandMeta {
+    int valid;                        // 0: this CTA has no more work
+    int map, chunk, W, first, last;   // task identity; first / last band of the task
+    int full, lo2;                    // rows recomputed by the task (see recomputed())
+    int base_slot, first_real;        // position -> ring slot mapping
+    int o0, n_out;                    // output rows [o0, o0 + n_out)
+    int out_slot[MAXO];
+    int x_lim[MAXX];                  // x tile row q (position o0-2+q): valid columns are [0, x_lim)
+};
+
+__device__ __forceinline__ bool recomputed_m(const BandMeta& m, int p) { return m.full || p < 2 || p >= m.lo2; }
+__device__ __forceinline__ int slot_m(const BandMeta& m, int H, bool sel, int p) {
+    if (!sel) return p;
+    const int s2 = m.base_slot + p;
+    return s2 >= H ? s2 - H : s2;
+}
+
 template <int PREC>
 struct SmemLayout {
     static constexpr int kBpack = (PREC == AP_PREC_FP32) ? 0 : 2 * 9 * BTILE_BYTES;
     static constexpr int kA1 = 4 * PLANE;  // [hl][g] fp16 planes, or fp32 [pixel][16] (same bytes)
-    static constexpr int kX = MAXX * XC * 4;
+    static constexpr int kX = 2 * MAXX * XC4 * 4;
     static constexpr int off_bpack = 0;
     static constexpr int off_a1 = off_bpack + kBpack;
-    static constexpr int off_x = off_a1 + kA1;
+    static constexpr int off_x = off_a1 + kA1;                   // [2 buffers][MAXX][XC4] fp32
     static constexpr int off_sum = off_x + kX;                   // [NWARPS][128] partial sums
-    static constexpr int off_meta = off_sum + NWARPS * TW * 4;   // band bookkeeping (ints)
-    static constexpr int kMeta = 64 * 4;
-    static constexpr int off_bar = off_meta + kMeta;
-    static constexpr int total = off_bar + 32;
+    static constexpr int off_meta = off_sum + NWARPS * TW * 4;   // [2] BandMeta
+    static constexpr int off_bar = (off_meta + 2 * (int)sizeof(BandMeta) + 15) / 16 * 16;
+    static constexpr int total = off_bar + 48;  // mbar(mma), mbar_x[2], tmem slot, xmax
 };
-
-// band bookkeeping in shared memory
-struct Meta {
-    int n_out, n_a1, n_x;
-    int out_pos[MAXO], out_a1row[MAXO];
-    int a1_pos[MAXA], a1_xrow[MAXA];
-    int x_pos[MAXX];
-};
-static_assert(sizeof(Meta) <= 64 * 4, "meta");
 
 __device__ __forceinline__ float4 ld4(const float* p, bool vec) {
     if (vec) return __ldg(reinterpret_cast<const float4*>(p));
     return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3));
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Thread 0's work-list iterator: tasks blockIdx.x, +gridDim.x, ...; bands within a task.
+struct Iter {
+    int task, bi;
+    Task T;
+};
+
+// Advance to the next band, fill its BandMeta and start the TMA bulk copies of its x rows.
+__device__ void next_band(const ConvParams& P, Iter& it, BandMeta& m, float* xdst, uint64_t* bar) {
+    const int H = P.H;
+    const int n_tasks = P.n_maps * P.n_chunks;
+    Band B;
+    for (;;) {
+        if (it.task >= n_tasks) {
+            m.valid = 0;
+            mbar_arrive_tx(bar, 0);
+            return;
+        }
+        if (it.bi == 0) {
+            it.T = plan_task(P, it.task / P.n_chunks, it.task % P.n_chunks);
+            if (it.T.skip) {
+                it.task += gridDim.x;
+                continue;
+            }
+        }
+        if (band_of(it.T, H, it.bi, B)) break;
+        it.task += gridDim.x;
+        it.bi = 0;
+    }
+    const Task& T = it.T;
+    const bool sel = P.state != nullptr;
+    Band nb;
+    m.valid = 1;
+    m.map = it.task / P.n_chunks;
+    m.chunk = it.task % P.n_chunks;
+    m.W = T.W;
+    m.first = it.bi == 0;
+    m.last = !band_of(T, H, it.bi + 1, nb);
+    m.full = T.full;
+    m.lo2 = T.lo2;
+    m.base_slot = sel ? slot_of(row_index(T.n_pushed, H, 0), H) : 0;
+    m.first_real = (!sel || T.n_pushed >= H) ? 0 : (int)(H - T.n_pushed);
+    m.o0 = B.o0[0];
+    m.n_out = B.o1[0] - B.o0[0];
+    for (int j = 0; j < m.n_out; ++j) m.out_slot[j] = slot_m(m, H, sel, m.o0 + j);
+    const int w0 = m.chunk * TW;
+    const int c_lo = max(0, w0 - 4), c_hi = min(P.pitch, w0 + TW + 4);
+    const float* ring = P.ring + (int64_t)m.map * P.map_stride;
+    uint32_t bytes = 0;
+    int lims[MAXX];
+    for (int q = 0; q < m.n_out + 4; ++q) {
+        const int p = m.o0 - 2 + q;
+        int lim = 0;
+        if (p >= 0 && p < H && p >= m.first_real) {
+            const int slot = slot_m(m, H, sel, p);
+            const int width = sel ? P.slot_width[(int64_t)m.map * H + slot] : T.W;
+            lim = min(width, T.W);
+            if (lim > 0 && c_hi > c_lo) bytes += (uint32_t)(c_hi - c_lo) * 4;
+        }
+        lims[q] = lim;
+        m.x_lim[q] = lim;
+    }
+    mbar_arrive_tx(bar, bytes);
+    for (int q = 0; q < m.n_out + 4; ++q) {
+        if (lims[q] <= 0 || c_hi <= c_lo) continue;
+        const int slot = slot_m(m, H, sel, m.o0 - 2 + q);
+        bulk_g2s(xdst + q * XC4 + (c_lo - (w0 - 4)), ring + (int64_t)slot * P.pitch + c_lo,
+                 (uint32_t)(c_hi - c_lo) * 4, bar);
+    }
+    it.bi += 1;
 }
 
 template <int PREC>
@@ -218,301 +317,282 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
     static_assert(NWARPS == 8, "epilogue / sum split assumes 8 warps");
     using L = SmemLayout<PREC>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    float* xs = reinterpret_cast<float*>(smem + L::off_x);
+    float* xbuf = reinterpret_cast<float*>(smem + L::off_x);
     float* psum = reinterpret_cast<float*>(smem + L::off_sum);
-    Meta* meta = reinterpret_cast<Meta*>(smem + L::off_meta);
+    BandMeta* metas = reinterpret_cast<BandMeta*>(smem + L::off_meta);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_bar + 8);
-    int* s_xmax = reinterpret_cast<int*>(smem + L::off_bar + 16);
+    uint64_t* mbar_x = reinterpret_cast<uint64_t*>(smem + L::off_bar + 8);   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::off_bar + 24);
+    int* s_xmax = reinterpret_cast<int*>(smem + L::off_bar + 28);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr bool kTC = PREC != AP_PREC_FP32;
     uint32_t tmem_base = 0, phase = 0;
+    const int H = P.H;
+    const bool sel = P.state != nullptr;
+    const bool vec = (P.pitch % 4) == 0;
 
-    if constexpr (kTC) {
-        // B operands once per persistent CTA
+    if constexpr (kTC) {  // B operands once per persistent CTA
         const uint4* src = g_bpack;
         uint4* dst = reinterpret_cast<uint4*>(smem + L::off_bpack);
         for (int i = tid; i < L::kBpack / 16; i += NTHREADS) dst[i] = src[i];
-        if (tid == 0) {
-            mbar_init(mbar, 1);
-            *s_xmax = 0;
-        }
         if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
         fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        tmem_base = *tmem_slot;
     }
-
-    const int H = P.H;
-    const int n_tasks = P.n_maps * P.n_chunks;
+    Iter it;
+    if (tid == 0) {
+        mbar_init(mbar, 1);
+        mbar_init(&mbar_x[0], 1);
+        mbar_init(&mbar_x[1], 1);
+        *s_xmax = 0;
+        it.task = blockIdx.x;
+        it.bi = 0;
+        next_band(P, it, metas[0], xbuf, &mbar_x[0]);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if constexpr (kTC) tmem_base = *tmem_slot;
     const int wexp = kTC ? g_wexp : 0;
-    const bool vec = (P.pitch % 4) == 0;
-    for (int task = blockIdx.x; task < n_tasks; task += gridDim.x) {
-        const int map = task / P.n_chunks, chunk = task % P.n_chunks;
-        const Task T = plan_task(P, map, chunk);
-        if (T.skip) continue;
-        const int W = T.W, w0 = chunk * TW;
-        const float* ring = P.ring + (int64_t)map * P.map_stride;
-        float* rmap = P.rmap + (int64_t)map * P.map_stride;
-        const int32_t* sw = P.state ? P.slot_width + (int64_t)map * H : nullptr;
-        auto slot_at = [&](int p) -> int { return P.state ? slot_of(row_index(T.n_pushed, H, p), H) : p; };
+    const float b1max = kTC ? g_b1abs[0] : 0.f, w1max = kTC ? g_w1abs[0] : 0.f;  // packed maxima (see pack)
+    uint32_t xphase[2] = {0u, 0u};
+    float4 pre[PREF];
+    int buf = 0;
 
-        // ---- 0. prefetch the r rows this task does not recompute (warp w: rows p = w + 8i,
-        //         lane: 4 columns) — these loads overlap the conv below.
+    for (;;) {
+        const BandMeta& m = metas[buf];
+        if (!m.valid) break;
+        const int W = m.W, w0 = m.chunk * TW;
         const int c4 = w0 + 4 * lane;
-        float4 pre[PREF];
+        float* rmap = P.rmap + (int64_t)m.map * P.map_stride;
+        // ---- 0. first band of a task: prefetch the r rows it does not recompute
+        //         (warp w: rows p = w + 8i, lane: 4 columns) — overlaps everything below
+        if (m.first) {
 #pragma unroll
-        for (int i = 0; i < PREF; ++i) {
-            const int p = warp + NWARPS * i;
-            pre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (p < H && c4 < W && !recomputed(T, p)) pre[i] = ld4(rmap + (int64_t)slot_at(p) * P.pitch + c4, vec);
+            for (int i = 0; i < PREF; ++i) {
+                const int p = warp + NWARPS * i;
+                pre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (p < H && c4 < W && !recomputed_m(m, p))
+                    pre[i] = ld4(rmap + (int64_t)slot_m(m, H, sel, p) * P.pitch + c4, vec);
+            }
         }
+        // ---- 1. thread 0 starts the next band's x-row copies into the other buffer
+        if (tid == 0) next_band(P, it, metas[buf ^ 1], xbuf + (buf ^ 1) * MAXX * XC4, &mbar_x[buf ^ 1]);
+        mbar_wait(&mbar_x[buf], xphase[buf]);
+        xphase[buf] ^= 1u;
+        const float* xs = xbuf + buf * MAXX * XC4;
+        const int n_out = m.n_out, n_a1 = n_out + 2, n_x = n_out + 4;
 
-        Band B;
-        for (int bi = 0; band_of(T, H, bi, B); ++bi) {
-            // ---- 1. band bookkeeping
-            if (tid == 0) {
-                int no = 0, na = 0, nx = 0;
-                for (int sg = 0; sg < B.nseg; ++sg) {
-                    const int o0 = B.o0[sg], o1 = B.o1[sg];
-                    const int abase = na, xbase = nx;
-                    for (int q = o0; q < o1; ++q) {
-                        meta->out_pos[no] = q;
-                        meta->out_a1row[no] = abase + (q - o0);
-                        ++no;
-                    }
-                    for (int p = o0 - 1; p < o1 + 1; ++p) {
-                        meta->a1_pos[na] = p;
-                        meta->a1_xrow[na] = xbase + (p - (o0 - 1));
-                        ++na;
-                    }
-                    for (int p = o0 - 2; p < o1 + 2; ++p) meta->x_pos[nx++] = p;
-                }
-                meta->n_out = no; meta->n_a1 = na; meta->n_x = nx;
-            }
-            __syncthreads();
-            const int n_out = meta->n_out, n_a1 = meta->n_a1, n_x = meta->n_x;
-
-            // ---- 2. x tile (all loads issued before any store): zero outside the H x W grid,
-            //         zero beyond each stored row's own width, zero for missing (not yet pushed) rows
-            float xv[(MAXX * XC + NTHREADS - 1) / NTHREADS];
+        // ---- 2. fp16 operand scale from max|x| over the tile (TC paths) + finiteness check
+        int aexp = 0;
+        {
             float xmax = 0.f;
-#pragma unroll
-            for (int u = 0; u < (MAXX * XC + NTHREADS - 1) / NTHREADS; ++u) {
-                const int i = tid + u * NTHREADS;
-                float v = 0.f;
-                if (i < n_x * XC) {
-                    const int xr = i / XC, xc = i % XC;
-                    const int p = meta->x_pos[xr], c = w0 - 2 + xc;
-                    if (p >= 0 && p < H && c >= 0 && c < W) {
-                        const int64_t k = row_index(T.n_pushed, H, p);
-                        if (k >= 0) {
-                            const int slot = P.state ? slot_of(k, H) : p;
-                            const int width = P.state ? sw[slot] : W;
-                            if (c < width) v = __ldg(ring + (int64_t)slot * P.pitch + c);
-                        }
-                    }
-                }
-                xv[u] = v;
-            }
-#pragma unroll
-            for (int u = 0; u < (MAXX * XC + NTHREADS - 1) / NTHREADS; ++u) {
-                const int i = tid + u * NTHREADS;
-                if (i < n_x * XC) {
-                    if (!isfinite(xv[u])) raise_status(P.status, AP_ENUMERIC);
-                    xs[i] = xv[u];
-                    xmax = fmaxf(xmax, fabsf(xv[u]));
+            for (int i = tid; i < n_x * (TW + 4); i += NTHREADS) {
+                const int xr = i / (TW + 4), xc = i - xr * (TW + 4);
+                const int c = w0 - 2 + xc;
+                if ((unsigned)c < (unsigned)m.x_lim[xr]) {
+                    const float v = xs[xr * XC4 + xc + 2];
+                    if (!isfinite(v)) raise_status(P.status, AP_ENUMERIC);
+                    xmax = fmaxf(xmax, fabsf(v));
                 }
             }
             if constexpr (kTC) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
                 if (lane == 0) atomicMax(s_xmax, __float_as_int(xmax));
+                __syncthreads();
+                aexp = f16_scale_exp(fmaf(w1max, __int_as_float(*s_xmax), b1max));
             }
-            __syncthreads();
-            // exact power-of-2 scale for the fp16 a1 operand: a1 <= |b1| + sum|w1| * max|x|
-            int aexp = 0;
-            if constexpr (kTC) {
-                const float mx = __int_as_float(*s_xmax);
-                float bound = 0.f;
-#pragma unroll
-                for (int ch = 0; ch < 16; ++ch) bound = fmaxf(bound, g_b1abs[ch] + g_w1abs[ch] * mx);
-                aexp = f16_scale_exp(bound);
-            }
-
-            // ---- 3. conv1 + ReLU -> a1 tile (zero outside the H x W grid)
-            const float ascale = pow2f(aexp);
-            for (int i = tid; i < n_a1 * A1C; i += NTHREADS) {
-                const int ar = i / A1C, ac = i - ar * A1C;
-                const int p = meta->a1_pos[ar], c = w0 - 1 + ac;
-                const bool valid = p >= 0 && p < H && c >= 0 && c < W;
-                if (!valid) {  // zero padding of the conv2 input: no conv1 work
-                    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-                    if constexpr (kTC) {
-                        *reinterpret_cast<uint4*>(smem + L::off_a1 + 0 * PLANE + i * 16) = z;
-                        *reinterpret_cast<uint4*>(smem + L::off_a1 + 1 * PLANE + i * 16) = z;
-                        if constexpr (PREC == AP_PREC_F16X3) {
-                            *reinterpret_cast<uint4*>(smem + L::off_a1 + 2 * PLANE + i * 16) = z;
-                            *reinterpret_cast<uint4*>(smem + L::off_a1 + 3 * PLANE + i * 16) = z;
-                        }
-                    } else {
-                        uint4* d = reinterpret_cast<uint4*>(smem + L::off_a1 + i * 64);
-                        d[0] = z; d[1] = z; d[2] = z; d[3] = z;
-                    }
-                    continue;
-                }
-                const float* xr = xs + meta->a1_xrow[ar] * XC + ac;
-                float x9[9];
-#pragma unroll
-                for (int di = 0; di < 3; ++di)
-#pragma unroll
-                    for (int dj = 0; dj < 3; ++dj) x9[di * 3 + dj] = xr[di * XC + dj];
-                float a[16];
-#pragma unroll
-                for (int ch = 0; ch < 16; ++ch) {
-                    float acc = c_w[OFF_B1 + ch];
-#pragma unroll
-                    for (int q = 0; q < 9; ++q) acc = fmaf(c_w[OFF_W1 + ch * 9 + q], x9[q], acc);
-                    a[ch] = fmaxf(acc, 0.f);
-                }
-                if constexpr (kTC) {
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) {
-                        __align__(16) __half hi[8], lo[8];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float as = a[g * 8 + q] * ascale;
-                            hi[q] = __float2half_rn(as);
-                            lo[q] = __float2half_rn(as - __half2float(hi[q]));
-                        }
-                        *reinterpret_cast<uint4*>(smem + L::off_a1 + (0 * 2 + g) * PLANE + i * 16) =
-                            *reinterpret_cast<uint4*>(hi);
-                        if constexpr (PREC == AP_PREC_F16X3)
-                            *reinterpret_cast<uint4*>(smem + L::off_a1 + (1 * 2 + g) * PLANE + i * 16) =
-                                *reinterpret_cast<uint4*>(lo);
-                    }
-                } else {
-                    float4* d = reinterpret_cast<float4*>(smem + L::off_a1 + i * 64);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) d[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
-                }
-            }
-            if constexpr (kTC) fence_async_smem();
-            __syncthreads();
-            if constexpr (kTC) {
-                if (tid == 0) *s_xmax = 0;  // every thread read it before the barrier above
-            }
-
-            // ---- 4. conv2 (tcgen05 implicit GEMM) + epilogue -> r for this band's output rows
-            if constexpr (kTC) {
-                if (tid == 0) {
-                    tc_fence_after();
-                    constexpr uint32_t idesc = idesc_f16_f32(TW, 32, 0);
-                    const uint32_t a1_addr = smem_u32(smem + L::off_a1);
-                    const uint32_t b_addr = smem_u32(smem + L::off_bpack);
-                    for (int j = 0; j < n_out; ++j) {
-                        const uint32_t d_tmem = tmem_base + j * 32;
-                        const int arow = meta->out_a1row[j];
-                        uint32_t acc = 0;
-#pragma unroll
-                        for (int tap = 0; tap < 9; ++tap) {
-                            const int di = tap / 3, dj = tap % 3;
-                            const uint32_t pix = (uint32_t)((arow + di) * A1C + dj);
-                            const uint64_t a_hi = umma_desc(a1_addr + 0 * 2 * PLANE + pix * 16, PLANE, 128);
-                            const uint64_t b_hi = umma_desc(b_addr + (0 * 9 + tap) * BTILE_BYTES, 512, 128);
-                            mma_f16(d_tmem, a_hi, b_hi, idesc, acc);
-                            acc = 1;
-                            if constexpr (PREC == AP_PREC_F16X3) {
-                                const uint64_t a_lo = umma_desc(a1_addr + 1 * 2 * PLANE + pix * 16, PLANE, 128);
-                                const uint64_t b_lo = umma_desc(b_addr + (1 * 9 + tap) * BTILE_BYTES, 512, 128);
-                                mma_f16(d_tmem, a_hi, b_lo, idesc, 1);
-                                mma_f16(d_tmem, a_lo, b_hi, idesc, 1);
-                            }
-                        }
-                    }
-                    mma_commit(mbar);
-                }
-                __syncwarp();
-                mbar_wait(mbar, phase);
-                phase ^= 1u;
-                tc_fence_after();
-                // warp w reads TMEM lanes 32*(w%4).. (pixels) for output rows j = w/4, w/4 + 2, ...
-                const int e = aexp + wexp;
-                const bool one_mul = e >= -126 && e <= 126;
-                const float u = one_mul ? pow2f(-e) : pow2f(-aexp), u2 = one_mul ? 1.f : pow2f(-wexp);
-                const int quad = warp & 3, pix = quad * 32 + lane, ecol = w0 + pix;
-                for (int j = warp >> 2; j < n_out; j += 2) {
-                    float acc[32];
-                    tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + j * 32, acc);
-                    float r = 0.f;
-#pragma unroll
-                    for (int n = 0; n < 32; ++n) {
-                        const float s2 = fmaf(acc[n] * u2, u, c_w[OFF_B2 + n]);
-                        r = fmaf(c_w[OFF_W3 + n], fmaxf(s2, 0.f), r);
-                    }
-                    if (ecol < W) rmap[(int64_t)slot_at(meta->out_pos[j]) * P.pitch + ecol] = r;
-                }
-                tc_fence_before();
-            } else {
-                const float* a1 = reinterpret_cast<const float*>(smem + L::off_a1);
-                const int pix = tid & (TW - 1), ecol = w0 + pix;
-                for (int j = tid / TW; j < n_out; j += NTHREADS / TW) {
-                    const int arow = meta->out_a1row[j];
-                    float acc[32];
-#pragma unroll
-                    for (int n = 0; n < 32; ++n) acc[n] = c_w[OFF_B2 + n];
-                    for (int tap = 0; tap < 9; ++tap) {
-                        const int di = tap / 3, dj = tap % 3;
-                        const float4* ap4 = reinterpret_cast<const float4*>(a1 + ((arow + di) * A1C + pix + dj) * 16);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const float4 v = ap4[q];
-                            const float av[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const int k = q * 4 + e;
-#pragma unroll
-                                for (int n = 0; n < 32; ++n) acc[n] = fmaf(c_w[OFF_W2 + n * 144 + k * 9 + tap], av[e], acc[n]);
-                            }
-                        }
-                    }
-                    float r = 0.f;
-#pragma unroll
-                    for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n], 0.f), r);
-                    if (ecol < W) rmap[(int64_t)slot_at(meta->out_pos[j]) * P.pitch + ecol] = r;
-                }
-            }
-            __syncthreads();  // x / a1 tiles, meta and TMEM columns are reused by the next band
         }
 
-        // ---- 5. forecast for this chunk: b3 + (1/H) sum_p r[p]; warp w sums rows p = w (mod 8)
-        //         in increasing p, the 8 partials are added in warp order (fixed, deterministic).
-        float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (c4 < W) {
+        // ---- 3. conv1 + ReLU -> a1 tile (zero outside the H x W grid)
+        const float ascale = pow2f(aexp);
+        for (int i = tid; i < n_a1 * A1C; i += NTHREADS) {
+            const int ar = i / A1C, ac = i - ar * A1C;
+            const int p = m.o0 - 1 + ar, c = w0 - 1 + ac;
+            const bool valid = p >= 0 && p < H && c >= 0 && c < W;
+            if (!valid) {  // zero padding of the conv2 input: no conv1 work
+                const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+                if constexpr (kTC) {
+                    *reinterpret_cast<uint4*>(smem + L::off_a1 + 0 * PLANE + i * 16) = z;
+                    *reinterpret_cast<uint4*>(smem + L::off_a1 + 1 * PLANE + i * 16) = z;
+                    if constexpr (PREC == AP_PREC_F16X3) {
+                        *reinterpret_cast<uint4*>(smem + L::off_a1 + 2 * PLANE + i * 16) = z;
+                        *reinterpret_cast<uint4*>(smem + L::off_a1 + 3 * PLANE + i * 16) = z;
+                    }
+                } else {
+                    uint4* d = reinterpret_cast<uint4*>(smem + L::off_a1 + i * 64);
+                    d[0] = z; d[1] = z; d[2] = z; d[3] = z;
+                }
+                continue;
+            }
+            float x9[9];
 #pragma unroll
-            for (int i = 0; i < PREF; ++i) {
-                const int p = warp + NWARPS * i;
-                if (p < H) {
-                    const float4 v = recomputed(T, p) ? ld4(rmap + (int64_t)slot_at(p) * P.pitch + c4, vec) : pre[i];
+            for (int di = 0; di < 3; ++di) {
+                const int lim = m.x_lim[ar + di];
+                const float* xr = xs + (ar + di) * XC4 + ac + 2;
+#pragma unroll
+                for (int dj = 0; dj < 3; ++dj) {
+                    const int cc = c - 1 + dj;
+                    x9[di * 3 + dj] = ((unsigned)cc < (unsigned)lim) ? xr[dj] : 0.f;
+                }
+            }
+            float a[16];
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch) {
+                float acc = c_w[OFF_B1 + ch];
+#pragma unroll
+                for (int q = 0; q < 9; ++q) acc = fmaf(c_w[OFF_W1 + ch * 9 + q], x9[q], acc);
+                a[ch] = fmaxf(acc, 0.f);
+            }
+            if constexpr (kTC) {
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    __align__(16) __half hi[8], lo[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float as = a[g * 8 + q] * ascale;
+                        hi[q] = __float2half_rn(as);
+                        lo[q] = __float2half_rn(as - __half2float(hi[q]));
+                    }
+                    *reinterpret_cast<uint4*>(smem + L::off_a1 + (0 * 2 + g) * PLANE + i * 16) =
+                        *reinterpret_cast<uint4*>(hi);
+                    if constexpr (PREC == AP_PREC_F16X3)
+                        *reinterpret_cast<uint4*>(smem + L::off_a1 + (1 * 2 + g) * PLANE + i * 16) =
+                            *reinterpret_cast<uint4*>(lo);
+                }
+            } else {
+                float4* d = reinterpret_cast<float4*>(smem + L::off_a1 + i * 64);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+            }
+        }
+        if constexpr (kTC) fence_async_smem();
+        __syncthreads();
+        if constexpr (kTC) {
+            if (tid == 0) *s_xmax = 0;  // every thread read it before the barrier above
+        }
+
+        // ---- 4. conv2 + epilogue -> r for this band's output rows
+        if constexpr (kTC) {
+            if (tid == 0) {
+                tc_fence_after();
+                constexpr uint32_t idesc = idesc_f16_f32(TW, 32, 0);
+                const uint32_t a1_addr = smem_u32(smem + L::off_a1);
+                const uint32_t b_addr = smem_u32(smem + L::off_bpack);
+                constexpr int NPART = (PREC == AP_PREC_F16X3) ? 2 : 1;
+                // ring slot s holds a1 tile row held[s] as 3 dj-shifted [hi, lo] A operands in TMEM
+                int held[3] = {-1, -1, -1};
+                for (int j = 0; j < n_out; ++j) {
+                    for (int di = 0; di < 3; ++di) {
+                        const int ar = j + di, slot = ar % 3;
+                        if (held[slot] == ar) continue;
+                        held[slot] = ar;
+                        for (int dj = 0; dj < 3; ++dj)
+                            for (int part = 0; part < NPART; ++part) {
+                                const uint64_t src = umma_desc(a1_addr + part * 2 * PLANE + (uint32_t)(ar * A1C + dj) * 16,
+                                                               PLANE, 128);
+                                tmem_cp_128x256b(tmem_base + slot * 48 + dj * 16 + part * 8, src);
+                            }
+                    }
+                    const uint32_t d_tmem = tmem_base + ACC_BASE + j * 32;
+                    uint32_t acc = 0;
+#pragma unroll
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const int di = tap / 3, dj = tap % 3;
+                        const uint32_t a_col = tmem_base + ((j + di) % 3) * 48 + dj * 16;
+                        const uint64_t b_hi = umma_desc(b_addr + (0 * 9 + tap) * BTILE_BYTES, 512, 128);
+                        mma_f16_ts(d_tmem, a_col, b_hi, idesc, acc);
+                        acc = 1;
+                        if constexpr (PREC == AP_PREC_F16X3) {
+                            const uint64_t b_lo = umma_desc(b_addr + (1 * 9 + tap) * BTILE_BYTES, 512, 128);
+                            mma_f16_ts(d_tmem, a_col, b_lo, idesc, 1);
+                            mma_f16_ts(d_tmem, a_col + 8, b_hi, idesc, 1);
+                        }
+                    }
+                }
+                mma_commit(mbar);
+            }
+            __syncwarp();
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+            tc_fence_after();
+            // warp w reads TMEM lanes 32*(w%4).. (pixels) for output rows j = w/4, w/4 + 2, ...
+            const int e = aexp + wexp;
+            const bool one_mul = e >= -126 && e <= 126;
+            const float u = one_mul ? pow2f(-e) : pow2f(-aexp), u2 = one_mul ? 1.f : pow2f(-wexp);
+            const int quad = warp & 3, pix = quad * 32 + lane, ecol = w0 + pix;
+            for (int j = warp >> 2; j < n_out; j += 2) {
+                float acc[32];
+                tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + ACC_BASE + j * 32, acc);
+                float r = 0.f;
+#pragma unroll
+                for (int n = 0; n < 32; ++n) {
+                    const float s2 = fmaf(acc[n] * u2, u, c_w[OFF_B2 + n]);
+                    r = fmaf(c_w[OFF_W3 + n], fmaxf(s2, 0.f), r);
+                }
+                if (ecol < W) rmap[(int64_t)m.out_slot[j] * P.pitch + ecol] = r;
+            }
+            tc_fence_before();
+        } else {
+            const float* a1 = reinterpret_cast<const float*>(smem + L::off_a1);
+            const int pix = tid & (TW - 1), ecol = w0 + pix;
+            for (int j = tid / TW; j < n_out; j += NTHREADS / TW) {
+                float acc[32];
+#pragma unroll
+                for (int n = 0; n < 32; ++n) acc[n] = c_w[OFF_B2 + n];
+                for (int tap = 0; tap < 9; ++tap) {
+                    const int di = tap / 3, dj = tap % 3;
+                    const float4* ap4 = reinterpret_cast<const float4*>(a1 + ((j + di) * A1C + pix + dj) * 16);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 v = ap4[q];
+                        const float av[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int k = q * 4 + e;
+#pragma unroll
+                            for (int n = 0; n < 32; ++n) acc[n] = fmaf(c_w[OFF_W2 + n * 144 + k * 9 + tap], av[e], acc[n]);
+                        }
+                    }
+                }
+                float r = 0.f;
+#pragma unroll
+                for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n], 0.f), r);
+                if (ecol < W) rmap[(int64_t)m.out_slot[j] * P.pitch + ecol] = r;
+            }
+        }
+        __syncthreads();  // a1 tile, TMEM accumulators and r writes are complete
+
+        // ---- 5. last band: forecast for this chunk: b3 + (1/H) sum_p r[p]; warp w sums rows
+        //         p = w (mod 8) in increasing p, the 8 partials are added in warp order.
+        if (m.last) {
+            float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c4 < W) {
+#pragma unroll
+                for (int i = 0; i < PREF; ++i) {
+                    const int p = warp + NWARPS * i;
+                    if (p < H) {
+                        const float4 v = recomputed_m(m, p) ? ld4(rmap + (int64_t)slot_m(m, H, sel, p) * P.pitch + c4, vec)
+                                                            : pre[i];
+                        acc4.x += v.x; acc4.y += v.y; acc4.z += v.z; acc4.w += v.w;
+                    }
+                }
+                for (int p = warp + NWARPS * PREF; p < H; p += NWARPS) {
+                    const float4 v = ld4(rmap + (int64_t)slot_m(m, H, sel, p) * P.pitch + c4, vec);
                     acc4.x += v.x; acc4.y += v.y; acc4.z += v.z; acc4.w += v.w;
                 }
             }
-            for (int p = warp + NWARPS * PREF; p < H; p += NWARPS) {
-                const float4 v = ld4(rmap + (int64_t)slot_at(p) * P.pitch + c4, vec);
-                acc4.x += v.x; acc4.y += v.y; acc4.z += v.z; acc4.w += v.w;
-            }
-        }
-        reinterpret_cast<float4*>(psum + warp * TW)[lane] = acc4;
-        __syncthreads();
-        if (tid < TW && w0 + tid < W) {
-            float sum = psum[tid];
+            reinterpret_cast<float4*>(psum + warp * TW)[lane] = acc4;
+            __syncthreads();
+            if (tid < TW && w0 + tid < W) {
+                float sum = psum[tid];
 #pragma unroll
-            for (int w = 1; w < NWARPS; ++w) sum += psum[w * TW + tid];
-            P.scores[(int64_t)map * P.score_stride + w0 + tid] = c_w[OFF_B3] + sum / (float)H;
+                for (int w = 1; w < NWARPS; ++w) sum += psum[w * TW + tid];
+                P.scores[(int64_t)m.map * P.score_stride + w0 + tid] = c_w[OFF_B3] + sum / (float)H;
+            }
+            __syncthreads();
         }
-        __syncthreads();
+        buf ^= 1;
     }
 
     if constexpr (kTC) {
@@ -593,14 +673,17 @@ int ap_set_weights(const float* weights4833, void* stream) {
     return launch_status("ap_set_weights");
 }
 
-int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W, int64_t grid_stride, float* out,
-                       int64_t out_stride, float* rscratch, int precision, int32_t* status, void* stream) {
+int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W, int32_t row_pitch,
+                       int64_t grid_stride, float* out, int64_t out_stride, float* rscratch, int precision,
+                       int32_t* status, void* stream) {
     AP_REQUIRE(H >= 1 && W >= 1 && n_grids >= 0, AP_EPARAM, "bad grid shape");
-    AP_REQUIRE(grid_stride >= (int64_t)H * W, AP_EPARAM, "grid_stride too small");
+    AP_REQUIRE(row_pitch >= W && row_pitch % 4 == 0, AP_EPARAM, "row_pitch must be >= W and a multiple of 4");
+    AP_REQUIRE(grid_stride >= (int64_t)H * row_pitch && grid_stride % 4 == 0, AP_EPARAM, "bad grid_stride");
+    AP_REQUIRE(reinterpret_cast<uintptr_t>(grids) % 16 == 0, AP_EPARAM, "grids must be 16-byte aligned");
     ConvParams P{};
     P.ring = grids;
     P.map_stride = grid_stride;
-    P.pitch = W;
+    P.pitch = row_pitch;
     P.rmap = rscratch;
     P.scores = out;
     P.score_stride = out_stride;
@@ -619,6 +702,7 @@ int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W
 
 int ap_sel_step(const ap_selector* s, int precision, void* stream) {
     AP_REQUIRE(s && s->n_maps > 0, AP_EPARAM, "bad selector descriptor");
+    AP_REQUIRE(s->w_max % 4 == 0, AP_EPARAM, "w_max must be a multiple of 4 (16-byte rows for the bulk copies)");
     AP_REQUIRE(s->update_interval >= 1 && s->calib_period >= 1, AP_ECONFIG, "bad selector config");
     cudaStream_t st = as_stream(stream);
     if (s->k_mid > 0) {

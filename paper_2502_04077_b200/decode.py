@@ -1,0 +1,296 @@
+"""LLaMA-shape decode engine driving the critical-token path end to end.
+
+This is the caller side of the hot path: where the reference's
+evaluation loop feeds recorded attention rows to ``selector.step``
+(evaluation.py:90-115), a real decode step here computes attention over the
+blocks the forecaster predicted at the previous step, appends the step's
+compressed attention row to every (layer, head) history, and — once per
+token, for all layers at once — forecasts + top-k's the blocks for the next
+step ("cross-token": predictions are made one token ahead).
+
+Everything in a step is stream-ordered with device-resident positions, so a
+step is one CUDA graph replay: two graphs (plain step / calibration step,
+selector.py:112-116 cadence) chosen by the host, which knows the counter.
+Non-attention layers are random-init bf16 weights of the named shape run as
+plain library GEMMs; both arms (sparse vs dense attention) share them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import _device as D
+from . import _lib
+from .attention import DecodeAttention
+from .batched import BatchedSelector
+from .errors import ConfigError
+from .predictor import PredictorWeights, init_weights, install_weights
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    name: str
+    n_layers: int
+    hidden: int
+    n_q_heads: int
+    n_kv_heads: int
+    ffn: int
+    vocab: int
+    rope_theta: float
+    head_dim: int = 128
+    eps: float = 1e-5
+
+    @property
+    def qkv_dim(self) -> int:
+        return (self.n_q_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    def weight_bytes(self) -> int:
+        per_layer = self.qkv_dim * self.hidden + self.hidden * self.hidden + 2 * self.ffn * self.hidden \
+            + self.hidden * self.ffn + 2 * self.hidden
+        return 2 * (self.n_layers * per_layer + 2 * self.vocab * self.hidden + self.hidden)
+
+    def kv_bytes_per_token(self) -> int:
+        return 2 * 2 * self.n_layers * self.n_kv_heads * self.head_dim
+
+
+LLAMA31_8B = ModelShape("llama-3.1-8b", 32, 4096, 32, 8, 14336, 128256, 500000.0)
+LONGCHAT_7B_32K = ModelShape("longchat-7b-v1.5-32k", 32, 4096, 32, 32, 11008, 32000, 10000.0)
+SHAPES = {s.name: s for s in (LLAMA31_8B, LONGCHAT_7B_32K)}
+
+
+class DecodeEngine:
+    """Batch decode of ``n_seq`` sequences at context ``ctx_len`` for up to ``max_new`` tokens.
+
+    mode: "sparse" (AttentionPredictor path) or "dense" (full-attention comparator).
+    group: q-heads per selection map — 1 = one history/forecast/top-k per q-head (the
+    reference's per-head semantics), n_q_heads/n_kv_heads = one per KV head (GQA
+    group: compressed rows are max-pooled over the group's heads, and the whole
+    group shares one gathered block set).
+    """
+
+    def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
+                 cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
+                 seed: int = 0):
+        torch = D.torch()
+        if mode not in ("sparse", "dense"):
+            raise ConfigError("mode must be 'sparse' or 'dense'")
+        self.shape, self.n_seq, self.mode, self.group = shape, n_seq, mode, group
+        G = shape.n_q_heads // shape.n_kv_heads
+        if G % group:
+            raise ConfigError("group must divide the GQA group size")
+        self.t_max = -(-(ctx_len + max_new + 1) // 1024) * 1024
+        self.ctx_len = ctx_len
+        dev = D.device()
+        self.dev = dev
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        bf = torch.bfloat16
+        L, Hd, Hq, Hkv, F, V = shape.n_layers, shape.hidden, shape.n_q_heads, shape.n_kv_heads, shape.ffn, shape.vocab
+
+        def rnd(*sz, std=0.02):
+            return (torch.randn(*sz, generator=gen, device=dev, dtype=bf) * std)
+
+        self.embed = rnd(V, Hd)
+        self.wqkv = [rnd(shape.qkv_dim, Hd) for _ in range(L)]
+        self.wo = [rnd(Hd, Hq * 128) for _ in range(L)]
+        self.wgu = [rnd(2 * F, Hd) for _ in range(L)]
+        self.wdown = [rnd(Hd, F) for _ in range(L)]
+        self.ln1 = [torch.ones(Hd, dtype=bf, device=dev) for _ in range(L)]
+        self.ln2 = [torch.ones(Hd, dtype=bf, device=dev) for _ in range(L)]
+        self.lnf = torch.ones(Hd, dtype=bf, device=dev)
+        self.lm_head = rnd(V, Hd)
+        # KV cache [L][S][Hkv][t_max][128]
+        self.k_cache = torch.empty(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
+        self.v_cache = torch.empty(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
+        # activations
+        S = n_seq
+        self.r = torch.zeros(S, Hd, dtype=bf, device=dev)
+        self.y = torch.zeros(S, Hd, dtype=bf, device=dev)
+        self.qkv = torch.zeros(S, shape.qkv_dim, dtype=bf, device=dev)
+        self.q = torch.zeros(S, Hq, 128, dtype=bf, device=dev)
+        self.att_out = torch.zeros(S, Hq, 128, dtype=bf, device=dev)
+        self.o = torch.zeros(S, Hd, dtype=bf, device=dev)
+        self.gu = torch.zeros(S, 2 * F, dtype=bf, device=dev)
+        self.act = torch.zeros(S, F, dtype=bf, device=dev)
+        self.mlp = torch.zeros(S, Hd, dtype=bf, device=dev)
+        self.tok = torch.zeros(S, dtype=torch.int64, device=dev)
+        self.seq_len = torch.full((S,), ctx_len, dtype=torch.int32, device=dev)
+        self.att = DecodeAttention(S, Hq, Hkv, self.t_max, n_splits_dense=min(64, self.t_max // 1024),
+                                   n_splits_sparse=8, device=dev)
+        self.maps_per_layer = Hq // group
+        self.sel = None
+        if mode == "sparse":
+            from .selector import SelectorConfig
+            self.cfg = cfg or SelectorConfig(budget=1024)
+            install_weights(weights or init_weights(0))
+            self.sel = BatchedSelector(self.cfg, S * L * self.maps_per_layer, self.t_max // 16, precision=precision,
+                                       device=dev)
+        self.counter = 0  # selector step counter (host mirror; all maps move in lockstep)
+        self.graphs = {}
+        self._fill_kv(gen)
+
+    # ---------------------------------------------------------------- setup
+    def _fill_kv(self, gen):
+        """Synthetic prefill: N(0,1) bf16 keys/values for positions [0, ctx_len) of every layer."""
+        torch = D.torch()
+        for l in range(self.shape.n_layers):
+            self.k_cache[l, :, :, : self.ctx_len].normal_(generator=gen)
+            self.v_cache[l, :, :, : self.ctx_len].normal_(generator=gen)
+
+    def init_history(self, seed: int = 1):
+        """Prefill-side history initialisation (selector.init_state, selector.py:61-70): the
+        compressed dense attention rows of the last history-1 prompt positions, computed by the
+        calibration kernel over keys [0, pos] with synthetic queries."""
+        if self.sel is None:
+            return
+        torch = D.torch()
+        gen = torch.Generator(device=self.dev)
+        gen.manual_seed(seed)
+        H = self.cfg.history
+        S, L = self.n_seq, self.shape.n_layers
+        q = torch.empty_like(self.q)
+        lens = torch.empty_like(self.seq_len)
+        for i in range(H - 1):
+            pos = self.ctx_len - (H - 1) + i  # prompt position; its attention row covers keys [0, pos]
+            lens.fill_(pos + 1)
+            q.normal_(generator=gen)
+            for l in range(L):
+                self.att.dense(q, self.k_cache[l], self.v_cache[l], lens, None, with_v=False, emit=True,
+                               selector=self.sel, map_base=l * self.maps_per_layer,
+                               maps_per_seq=L * self.maps_per_layer, group=self.group)
+        torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- one step
+    def _layer(self, l: int, variant: str):
+        torch = D.torch()
+        F_ = torch.nn.functional
+        sh = self.shape
+        S = self.n_seq
+        s = _lib.stream_handle()
+        if l == 0:
+            _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.r), None, _lib.ptr(self.ln1[0]), _lib.ptr(self.y), S,
+                                             sh.hidden, sh.eps, s))
+        else:
+            _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.ln1[l]),
+                                             _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
+        torch.matmul(self.y, self.wqkv[l].t(), out=self.qkv)
+        kc, vc = self.k_cache[l], self.v_cache[l]
+        _lib.check(_lib.fn("ap_rope_append")(_lib.ptr(self.qkv), S, sh.n_q_heads, sh.n_kv_heads,
+                                             _lib.ptr(self.seq_len), _lib.ptr(self.q), _lib.ptr(kc), _lib.ptr(vc),
+                                             self.t_max, sh.rope_theta, s))
+        kw = dict(map_base=l * self.maps_per_layer, maps_per_seq=sh.n_layers * self.maps_per_layer,
+                  group=self.group)
+        if variant == "dense":
+            self.att.dense(self.q, kc, vc, self.seq_len, self.att_out, with_v=True)
+        elif variant == "first":
+            self.att.dense(self.q, kc, vc, self.seq_len, self.att_out, with_v=True, emit=True, selector=self.sel,
+                           **kw)
+        elif variant == "calib":
+            self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=False, **kw)
+            self.att.dense(self.q, kc, vc, self.seq_len, None, with_v=False, emit=True, selector=self.sel, **kw)
+        else:
+            self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=True, **kw)
+        torch.matmul(self.att_out.view(S, -1), self.wo[l].t(), out=self.o)
+        _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.o), _lib.ptr(self.r), _lib.ptr(self.ln2[l]), _lib.ptr(self.y),
+                                         S, sh.hidden, sh.eps, s))
+        torch.matmul(self.y, self.wgu[l].t(), out=self.gu)
+        _lib.check(_lib.fn("ap_silu_mul")(_lib.ptr(self.gu), _lib.ptr(self.act), S, sh.ffn, s))
+        torch.matmul(self.act, self.wdown[l].t(), out=self.mlp)
+
+    def _step_body(self, variant: str):
+        torch = D.torch()
+        sh = self.shape
+        S = self.n_seq
+        s = _lib.stream_handle()
+        _lib.check(_lib.fn("ap_advance")(_lib.ptr(self.seq_len), S, 1, s))
+        torch.index_select(self.embed, 0, self.tok, out=self.r)
+        for l in range(sh.n_layers):
+            self._layer(l, variant)
+        _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.lnf), _lib.ptr(self.y),
+                                         S, sh.hidden, sh.eps, s))
+        logits = torch.matmul(self.y, self.lm_head.t())
+        torch.argmax(logits, dim=-1, out=self.tok)
+        if self.sel is not None and variant != "dense":
+            self.sel.step()  # forecast + top-k for the next token, every layer and head at once
+
+    def variant_for_next(self) -> str:
+        if self.mode == "dense":
+            return "dense"
+        if self.counter == 0:
+            return "first"
+        return "calib" if self.counter % self.cfg.calibration_period == 0 else "plain"
+
+    def step(self, use_graph: bool = True):
+        """One decode token for every sequence."""
+        torch = D.torch()
+        v = self.variant_for_next()
+        if use_graph and v != "first":
+            g = self.graphs.get(v)
+            if g is None:
+                g = self._capture(v)
+            g.replay()
+        else:
+            self._step_body(v)
+        if self.sel is not None:
+            self.counter += 1
+        return v
+
+    def _capture(self, variant: str):
+        """Capture one decode step; positions/ring state live on the device so replays advance."""
+        torch = D.torch()
+        # warm the kernels (cuBLAS handles, occupancy caches) outside capture without side effects:
+        # snapshot the mutable state, run once, restore.
+        snap = self._snapshot()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._step_body(variant)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self._restore(snap)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step_body(variant)
+        torch.cuda.synchronize()
+        self._restore(snap)  # capture does not execute, but be explicit about the state contract
+        self.graphs[variant] = g
+        return g
+
+    def _snapshot(self):
+        torch = D.torch()
+        snap = {"seq_len": self.seq_len.clone(), "tok": self.tok.clone()}
+        if self.sel is not None:
+            snap.update(state=self.sel.state.clone(), slot_width=self.sel.slot_width.clone(),
+                        mid_blocks=self.sel.mid_blocks.clone(), mid_mask=self.sel.mid_mask.clone())
+        del torch
+        return snap
+
+    def _restore(self, snap):
+        self.seq_len.copy_(snap["seq_len"])
+        self.tok.copy_(snap["tok"])
+        if self.sel is not None:
+            self.sel.state.copy_(snap["state"])
+            self.sel.slot_width.copy_(snap["slot_width"])
+            self.sel.mid_blocks.copy_(snap["mid_blocks"])
+            self.sel.mid_mask.copy_(snap["mid_mask"])
+
+    def capture_all(self):
+        """Capture every step variant this engine will replay (keeps capture out of timed regions)."""
+        for v in (("dense",) if self.mode == "dense" else ("plain", "calib")):
+            if v not in self.graphs:
+                self._capture(v)
+
+    def set_mode(self, mode: str):
+        """Switch arms on the same weights / KV cache (positions reset to the prompt length)."""
+        if mode == "sparse" and self.sel is None:
+            raise ConfigError("engine was built without a selector")
+        self.mode = mode
+        self.seq_len.fill_(self.ctx_len)
+
+    def kernels_per_step(self, variant: str) -> int:
+        """Launches of libattnpred kernels in one step (the bench's gpu_launches claim)."""
+        L = self.shape.n_layers
+        per_layer = 2 + 1 + 1  # rmsnorm x2, rope_append, silu_mul
+        att = {"dense": 2, "first": 2, "plain": 2, "calib": 4}[variant]
+        sel = 2 if (self.sel is not None and variant != "dense") else 0
+        return 1 + L * (per_layer + att) + 1 + sel  # advance + layers + final norm + selector

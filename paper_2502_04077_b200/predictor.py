@@ -172,13 +172,17 @@ def forward(weights: PredictorWeights, history: AttentionHistory, precision: str
     H, W = grid.shape
     torch = D.torch()
     install_weights(weights)
-    g = D.to_device(grid.astype(np.float32))
+    pitch = -(-W // 4) * 4  # 16-byte rows for the kernel's bulk copies
+    padded = np.zeros((H, pitch), dtype=np.float32)
+    padded[:, :W] = grid
+    g = D.to_device(padded)
     out = torch.empty(W, dtype=torch.float32, device=g.device)
-    scratch = torch.empty(H * W, dtype=torch.float32, device=g.device)
+    scratch = torch.empty(H * pitch, dtype=torch.float32, device=g.device)
     status = D.new_status()
     prec = _lib.PREC[precision or default_precision()]
-    _lib.check(_lib.fn("ap_predict_forward")(_lib.ptr(g), 1, H, W, H * W, _lib.ptr(out), W, _lib.ptr(scratch),
-                                             prec, _lib.ptr(status), _lib.stream_handle()), "forward")
+    _lib.check(_lib.fn("ap_predict_forward")(_lib.ptr(g), 1, H, W, pitch, H * pitch, _lib.ptr(out), W,
+                                             _lib.ptr(scratch), prec, _lib.ptr(status), _lib.stream_handle()),
+               "forward")
     D.sync_and_check(status, "forward")
     return out.cpu().numpy().astype(np.float64)
 
