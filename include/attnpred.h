@@ -174,7 +174,10 @@ int ap_sel_grid_ctas(int precision);
  * 16-token blocks; K/V cache laid out [seq][kv_head][t_max][128].
  * seq_len[s] = number of keys the current query attends (t, incl. itself).
  * Workspaces: partial = n_seq*n_q_heads*n_splits*130 floats;
- * bmax = n_seq*n_q_heads*w_max floats, initialised to -inf once.
+ * bmax = n_seq*n_q_heads*w_max floats, initialised to -inf once;
+ * counters = n_seq*n_q_heads int32, zeroed once.  The split-K partials are
+ * merged by the last CTA of each (sequence, head group) to finish — one
+ * launch per call, no separate combine kernel.
  * ------------------------------------------------------------------------- */
 typedef struct ap_attn_layer {
     int32_t n_seq, n_q_heads, n_kv_heads, head_dim, t_max, n_splits, block, w_max;
@@ -186,6 +189,7 @@ typedef struct ap_attn_layer {
     float* lse;             /* [n_seq][n_q_heads] log2-domain LSE, may be NULL */
     float* partial;
     float* bmax;
+    int32_t* counters;      /* [n_seq][n_q_heads] zeroed once; split-completion counters */
 } ap_attn_layer;
 
 /* Dense decode attention over keys [0, t) (with_v = 1: output + LSE, the

@@ -62,7 +62,7 @@ class AttnLayerDesc(ctypes.Structure):
         ("block", ctypes.c_int32), ("w_max", ctypes.c_int32),
         ("q", ctypes.c_void_p), ("k_cache", ctypes.c_void_p), ("v_cache", ctypes.c_void_p),
         ("seq_len", ctypes.c_void_p), ("out", ctypes.c_void_p), ("lse", ctypes.c_void_p),
-        ("partial", ctypes.c_void_p), ("bmax", ctypes.c_void_p),
+        ("partial", ctypes.c_void_p), ("bmax", ctypes.c_void_p), ("counters", ctypes.c_void_p),
     ]
 
 

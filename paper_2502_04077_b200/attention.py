@@ -46,6 +46,7 @@ class DecodeAttention:
         self.partial = torch.empty(n_seq * n_q_heads * ns * (HEAD_DIM + 2), dtype=torch.float32, device=dev)
         self.bmax = torch.full((n_seq * n_q_heads * self.w_max,), float("-inf"), dtype=torch.float32, device=dev)
         self.lse = torch.empty(n_seq, n_q_heads, dtype=torch.float32, device=dev)
+        self.counters = torch.zeros(n_seq * n_q_heads, dtype=torch.int32, device=dev)
 
     def _desc(self, q, k_cache, v_cache, seq_len, out, n_splits):
         return AttnLayerDesc(
@@ -53,7 +54,7 @@ class DecodeAttention:
             t_max=self.t_max, n_splits=n_splits, block=BLOCK, w_max=self.w_max,
             q=q.data_ptr(), k_cache=k_cache.data_ptr(), v_cache=v_cache.data_ptr(), seq_len=seq_len.data_ptr(),
             out=None if out is None else out.data_ptr(), lse=self.lse.data_ptr(), partial=self.partial.data_ptr(),
-            bmax=self.bmax.data_ptr(),
+            bmax=self.bmax.data_ptr(), counters=self.counters.data_ptr(),
         )
 
     def dense(self, q, k_cache, v_cache, seq_len, out=None, *, with_v=True, emit=False, selector=None,

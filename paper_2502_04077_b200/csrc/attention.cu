@@ -38,7 +38,9 @@ struct AttnParams {
     float* lse;                   // [S][Hq] log2 units (nullable)
     float* partial;               // [S][Hq][n_splits][D+2]
     float* bmax;                  // [S][Hq][w_max] log2-unit block max logits (-inf = untouched)
+    int32_t* counters;            // [S][Hq] split-completion counters (0 between launches)
     int32_t w_max;
+    int32_t with_v, emit;
     // selector binding
     ap_selector sel;
     int32_t map_base, maps_per_seq, group;  // map(s, h) = s*maps_per_seq + map_base + h/group
@@ -188,6 +190,92 @@ __device__ void write_partial(WarpState<NH, WITH_V>& st, float* smem, float* par
     }
 }
 
+// ------------------------------------------------------------------ combine
+// Executed by the LAST CTA to finish among the splits of a unit (flash-decoding
+// reduction fused into the split kernel): merge the splits of heads
+// [h0, h0 + nh) of sequence s; write out (bf16) and lse; when emit, write each
+// map's compressed row max_h exp2(bm_h[j] - lse_h) (0 where untouched) into
+// its ring slot and advance the map's ring state (selector.py:117-120).
+__device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
+    __shared__ float s_w[8][64];
+    __shared__ float s_lse[8], s_L[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = P.seq_len[s];
+    if (warp < nh) {  // warp per head: lanes over splits
+        const float* part = P.partial + ((int64_t)s * P.n_q_heads + h0 + warp) * P.n_splits * (HD + 2);
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+        if (lane < P.n_splits) { m0 = __ldcg(part + lane * (HD + 2)); l0 = __ldcg(part + lane * (HD + 2) + 1); }
+        if (lane + 32 < P.n_splits) { m1 = __ldcg(part + (lane + 32) * (HD + 2)); l1 = __ldcg(part + (lane + 32) * (HD + 2) + 1); }
+        float M = fmaxf(m0, m1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float w0 = (m0 == -INFINITY) ? 0.f : exp2f(m0 - M), w1 = (m1 == -INFINITY) ? 0.f : exp2f(m1 - M);
+        if (lane < P.n_splits) s_w[warp][lane] = w0;
+        if (lane + 32 < P.n_splits) s_w[warp][lane + 32] = w1;
+        float L = l0 * w0 + l1 * w1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        if (lane == 0) {
+            s_L[warp] = L;
+            s_lse[warp] = M + log2f(L);
+            if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + warp] = M + log2f(L);
+        }
+    }
+    __syncthreads();
+    if (P.with_v) {
+        for (int idx = threadIdx.x; idx < nh * HD; idx += ATT_THREADS) {
+            const int hh = idx / HD, d = idx % HD;
+            const float* part = P.partial + ((int64_t)s * P.n_q_heads + h0 + hh) * P.n_splits * (HD + 2) + 2 + d;
+            float o = 0.f;
+            for (int sp = 0; sp < P.n_splits; ++sp) o = fmaf(__ldcg(part + sp * (HD + 2)), s_w[hh][sp], o);
+            P.out[((int64_t)s * P.n_q_heads + h0 + hh) * HD + d] = __float2bfloat16_rn(o / s_L[hh]);
+        }
+    }
+    if (P.emit) {
+        const int64_t W = (t + P.block - 1) / P.block;
+        for (int g0 = 0; g0 < nh; g0 += P.group) {
+            const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;
+            const ap_map_state ms = P.sel.state[map];
+            const int Hh = P.sel.history;
+            const int slot = (int)(ms.n_pushed % Hh);
+            float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
+            float* bm0 = P.bmax + ((int64_t)s * P.n_q_heads + h0 + g0) * P.w_max;
+            for (int64_t j = threadIdx.x; j < W; j += ATT_THREADS) {
+                float v = 0.f;
+                for (int hh = 0; hh < P.group; ++hh) {
+                    const float lg = __ldcg(bm0 + hh * (int64_t)P.w_max + j);
+                    if (lg != -INFINITY) v = fmaxf(v, exp2f(lg - s_lse[g0 + hh]));
+                    bm0[hh * (int64_t)P.w_max + j] = -INFINITY;  // untouched marker for the next step
+                }
+                dst[j] = v;
+            }
+            if (threadIdx.x == 0) {
+                ap_map_state st = ms;
+                P.sel.slot_width[(int64_t)map * Hh + slot] = (int32_t)W;
+                st.n_pushed += 1;
+                st.row_len = t;
+                st.width = (int32_t)W;
+                P.sel.state[map] = st;
+            }
+        }
+    }
+}
+
+// Count this CTA's split as done; the last one (returns true) runs the combine.
+__device__ __forceinline__ bool last_split(int32_t* counter, int n_splits) {
+    __shared__ int s_last;
+    __threadfence();  // partials / block maxima visible device-wide before counting
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(counter, 1);
+        s_last = (prev == n_splits - 1);
+        if (s_last) *counter = 0;  // ready for the next launch (stream-ordered)
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last;
+}
+
 // ------------------------------------------------------------------ dense
 // grid (n_splits, Hkv, S); NH = Hq/Hkv q-heads per CTA share every K/V load.
 template <int NH, bool WITH_V, bool EMIT>
@@ -221,6 +309,7 @@ __global__ void __launch_bounds__(ATT_THREADS) dense_partial_kernel(AttnParams P
     }
     float* part = P.partial + (((int64_t)s * P.n_q_heads + h0) * P.n_splits + split) * (HD + 2);
     write_partial<NH, WITH_V>(st, sm_att, part, (int64_t)P.n_splits * (HD + 2));
+    if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) combine_heads(P, s, h0, NH);
 }
 
 // ------------------------------------------------------------------ sparse
@@ -285,75 +374,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_partial_kernel(AttnParams 
     }
     float* part = P.partial + (((int64_t)s * P.n_q_heads + h0) * P.n_splits + split) * (HD + 2);
     write_partial<NH, true>(st, sm_att, part, (int64_t)P.n_splits * (HD + 2));
-}
-
-// ------------------------------------------------------------------ combine
-// grid (S * Hq / group): merge the splits of every head of one map; write out
-// (bf16) and lse; when EMIT, write the group's compressed row
-// max_h exp2(bm_h[j] - lse_h) (0 where untouched) into the ring slot and
-// advance the map's ring state (selector.py:117-120).
-template <bool WITH_V, bool EMIT>
-__global__ void __launch_bounds__(ATT_THREADS) combine_kernel(AttnParams P) {
-    __shared__ float s_lse[8];
-    __shared__ float s_w[8][64];
-    const int gm = blockIdx.x;
-    const int maps_per_layer = P.n_q_heads / P.group;
-    const int s = gm / maps_per_layer, g = gm % maps_per_layer;
-    const int64_t t = P.seq_len[s];
-    for (int hh = 0; hh < P.group; ++hh) {
-        const int h = g * P.group + hh;
-        const float* part = P.partial + ((int64_t)s * P.n_q_heads + h) * P.n_splits * (HD + 2);
-        // global max and weights per split (n_splits <= 64)
-        float M = -INFINITY;
-        for (int sp = 0; sp < P.n_splits; ++sp) M = fmaxf(M, part[sp * (HD + 2)]);
-        if (threadIdx.x < P.n_splits) {
-            const float m = part[threadIdx.x * (HD + 2)];
-            s_w[hh][threadIdx.x] = (m == -INFINITY) ? 0.f : exp2f(m - M);
-        }
-        __syncthreads();
-        float L = 0.f;
-        for (int sp = 0; sp < P.n_splits; ++sp) L += part[sp * (HD + 2) + 1] * s_w[hh][sp];
-        if (threadIdx.x == 0) {
-            const float lse = M + log2f(L);
-            s_lse[hh] = lse;
-            if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h] = lse;
-        }
-        if constexpr (WITH_V) {
-            for (int d = threadIdx.x; d < HD; d += ATT_THREADS) {
-                float o = 0.f;
-                for (int sp = 0; sp < P.n_splits; ++sp) o += part[sp * (HD + 2) + 2 + d] * s_w[hh][sp];
-                P.out[((int64_t)s * P.n_q_heads + h) * HD + d] = __float2bfloat16_rn(o / L);
-            }
-        }
-        __syncthreads();
-    }
-    if constexpr (EMIT) {
-        const int map = s * P.maps_per_seq + P.map_base + g;
-        const ap_map_state ms = P.sel.state[map];
-        const int H = P.sel.history;
-        const int slot = (int)(ms.n_pushed % H);
-        const int64_t W = (t + P.block - 1) / P.block;
-        float* dst = P.sel.ring + ((int64_t)map * H + slot) * P.sel.w_max;
-        float* bm0 = P.bmax + ((int64_t)s * P.n_q_heads + g * P.group) * P.w_max;
-        for (int64_t j = threadIdx.x; j < W; j += ATT_THREADS) {
-            float v = 0.f;
-            for (int hh = 0; hh < P.group; ++hh) {
-                const float lg = bm0[hh * (int64_t)P.w_max + j];
-                if (lg != -INFINITY) v = fmaxf(v, exp2f(lg - s_lse[hh]));
-                bm0[hh * (int64_t)P.w_max + j] = -INFINITY;  // untouched marker for the next step
-            }
-            dst[j] = v;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            ap_map_state st = ms;
-            P.sel.slot_width[(int64_t)map * H + slot] = (int32_t)W;
-            st.n_pushed += 1;
-            st.row_len = t;
-            st.width = (int32_t)W;
-            P.sel.state[map] = st;
-        }
-    }
+    if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) combine_heads(P, s, h0, NH);
 }
 
 template <int NH>
@@ -384,7 +405,8 @@ static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t m
     P.n_splits = a->n_splits; P.block = a->block;
     P.q = (const __nv_bfloat16*)a->q; P.k = (const __nv_bfloat16*)a->k_cache; P.v = (const __nv_bfloat16*)a->v_cache;
     P.seq_len = a->seq_len; P.out = (__nv_bfloat16*)a->out; P.lse = a->lse; P.partial = a->partial;
-    P.bmax = a->bmax; P.w_max = a->w_max;
+    P.bmax = a->bmax; P.w_max = a->w_max; P.counters = a->counters;
+    AP_REQUIRE(a->counters != nullptr, AP_EPARAM, "counters workspace is required");
     if (sel) P.sel = *sel; else memset(&P.sel, 0, sizeof(P.sel));
     P.map_base = map_base; P.maps_per_seq = maps_per_seq; P.group = group < 1 ? 1 : group;
     const int G = a->n_q_heads / a->n_kv_heads;
@@ -405,6 +427,7 @@ int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, in
     int rc = make_params(a, sel, map_base, maps_per_seq, group, P);
     if (rc != AP_OK) return rc;
     AP_REQUIRE(with_v || emit, AP_EPARAM, "dense pass without V must emit the calibration row");
+    P.with_v = with_v; P.emit = emit;
     AP_REQUIRE(!emit || sel, AP_EPARAM, "emit needs a selector");
     cudaStream_t st = as_stream(stream);
     const int G = a->n_q_heads / a->n_kv_heads;
@@ -414,13 +437,7 @@ int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, in
         case 4: launch_dense<4>(P, with_v, emit, st); break;
         default: launch_dense<8>(P, with_v, emit, st); break;
     }
-    rc = launch_status("dense_partial_kernel");
-    if (rc != AP_OK) return rc;
-    const int n_comb = a->n_seq * a->n_q_heads / P.group;
-    if (with_v && emit) combine_kernel<true, true><<<n_comb, ATT_THREADS, 0, st>>>(P);
-    else if (with_v) combine_kernel<true, false><<<n_comb, ATT_THREADS, 0, st>>>(P);
-    else combine_kernel<false, true><<<n_comb, ATT_THREADS, 0, st>>>(P);
-    return launch_status("combine_kernel");
+    return launch_status("dense_partial_kernel");
 }
 
 int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
@@ -429,6 +446,7 @@ int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_b
     int rc = make_params(a, sel, map_base, maps_per_seq, group, P);
     if (rc != AP_OK) return rc;
     AP_REQUIRE(sel != nullptr, AP_EPARAM, "sparse attention needs a selector");
+    P.with_v = 1; P.emit = emit;
     cudaStream_t st = as_stream(stream);
     switch (P.group) {
         case 1: launch_sparse<1>(P, emit, st); break;
@@ -436,12 +454,7 @@ int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_b
         case 4: launch_sparse<4>(P, emit, st); break;
         default: launch_sparse<8>(P, emit, st); break;
     }
-    rc = launch_status("sparse_partial_kernel");
-    if (rc != AP_OK) return rc;
-    const int n_comb = a->n_seq * a->n_q_heads / P.group;
-    if (emit) combine_kernel<true, true><<<n_comb, ATT_THREADS, 0, st>>>(P);
-    else combine_kernel<true, false><<<n_comb, ATT_THREADS, 0, st>>>(P);
-    return launch_status("combine_kernel");
+    return launch_status("sparse_partial_kernel");
 }
 
 }  // extern "C"

@@ -291,6 +291,6 @@ class DecodeEngine:
         """Launches of libattnpred kernels in one step (the bench's gpu_launches claim)."""
         L = self.shape.n_layers
         per_layer = 2 + 1 + 1  # rmsnorm x2, rope_append, silu_mul
-        att = {"dense": 2, "first": 2, "plain": 2, "calib": 4}[variant]
+        att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
         sel = 2 if (self.sel is not None and variant != "dense") else 0
         return 1 + L * (per_layer + att) + 1 + sel  # advance + layers + final norm + selector
