@@ -52,10 +52,11 @@ def parse():
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--budget", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--group", choices=["head", "kv"], default="head",
+    ap.add_argument("--group", choices=["head", "kv"], default="kv",
                     help="selection map per q-head (reference semantics) or per KV-head group")
     ap.add_argument("--precision", default="fp16x3")
     ap.add_argument("--no-dense", action="store_true", help="skip the full-attention comparator arm")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other selection granularity")
     ap.add_argument("--cpu-sample", type=int, default=48, help="oracle map-steps timed for cpu_baseline")
     return ap.parse_args()
 
@@ -171,9 +172,89 @@ def cpu_oracle_rate(ctx: int, budget: int, n_map_steps: int, seed: int = 0):
 
 
 # ---------------------------------------------------------------- our arm
+def first_token(eng):
+    import torch
+    eng.step(use_graph=False)  # first decode token: dense attention + emission, no prior selection
+    eng.capture_all()
+    torch.cuda.synchronize()
+
+
+def timed_steps(eng, n, world):
+    import torch
+    barrier(world)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    variants = [eng.step() for _ in range(n)]
+    b.record()
+    b.synchronize()
+    return max_over_ranks(a.elapsed_time(b) / 1e3, world), variants
+
+
+def measure_e2e(eng, n, batch, world):
+    """Same metric through the host API: token in (pinned H2D), token out (D2H), every step."""
+    import torch
+    host_in = torch.zeros(batch, dtype=torch.int64).pin_memory()
+    host_out = torch.zeros(batch, dtype=torch.int64).pin_memory()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        eng.tok.copy_(host_in, non_blocking=True)
+        eng.step()
+        host_out.copy_(eng.tok, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        host_in.copy_(host_out)
+    el = max_over_ranks(time.perf_counter() - t0, world)
+    return {"value": round(batch * n * world / el, 2), "unit": "tok/s",
+            "h2d_bytes_per_step": 8 * batch, "d2h_bytes_per_step": 8 * batch}
+
+
+def measure_selector(eng, reps=20):
+    """Median CUDA-event time of the fused forecast + top-k launch (ap_sel_step) in its steady-state
+    form — one new row per map since the last update (incremental), width unchanged.  The decode
+    state is snapshotted and restored around the measurement."""
+    import torch
+    snap = eng._snapshot()
+    ring, rmap = eng.sel.ring.clone(), eng.sel.rmap.clone()
+    st = eng.sel.states()
+    t_now = int(st["row_len"].max())
+    comp = torch.rand(eng.sel.n_maps, eng.sel.w_max, device="cuda") ** 8
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for i in range(reps):
+        eng._restore(snap)
+        eng.sel.ring.copy_(ring)
+        eng.sel.rmap.copy_(rmap)
+        eng.sel.push_compressed(comp, t_now)
+        ev[i][0].record()
+        eng.sel.step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in ev)
+    eng._restore(snap)
+    eng.sel.ring.copy_(ring)
+    eng.sel.rmap.copy_(rmap)
+    W = int(st["width"].max())
+    return us, W
+
+
+def roofline_for(eng, args, us, W, key):
+    cfg = eng.cfg
+    n_maps = eng.sel.n_maps
+    H, K = cfg.history, cfg.middle_blocks
+    b_alg = n_maps * ((H + 1) * W * 4 + 4 * K)  # history window + new row + block ids, per launch
+    peak, peak_kind = measured_peak()
+    achieved = b_alg / (us * 1e-6) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": profiled_traffic().get(key), "peak_kind": peak_kind,
+            "kernel": "ap_sel_step (conv_forecast_kernel + sel_topk_kernel)", "maps": n_maps,
+            "us_per_launch": round(us, 2), "us_per_layer": round(us / eng.shape.n_layers, 3),
+            "algorithmic_bytes_per_launch": b_alg}
+
+
 def run_ours(args, rank, world):
     import torch
-    from paper_2502_04077_b200 import _lib
     from paper_2502_04077_b200.decode import SHAPES, DecodeEngine
     from paper_2502_04077_b200.selector import SelectorConfig
 
@@ -185,81 +266,28 @@ def run_ours(args, rank, world):
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
                        precision=args.precision, seed=rank)
     eng.init_history()
-    eng.step(use_graph=False)  # first decode token: dense attention + emission, no prior selection
-    torch.cuda.synchronize()
-
-    def timed_steps(n):
-        barrier(world)
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        variants = [eng.step() for _ in range(n)]
-        b.record()
-        b.synchronize()
-        return a.elapsed_time(b) / 1e3, variants
-
-    eng.capture_all()
+    first_token(eng)
     for _ in range(args.warmup):
         eng.step()
-    gpu_id = torch.cuda.current_device()
-    with ClockSampler(gpu_id) as clk:
-        elapsed, variants = timed_steps(args.steps)
-    elapsed = max_over_ranks(elapsed, world)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        elapsed, variants = timed_steps(eng, args.steps, world)
     value = args.batch * args.steps * world / elapsed
     launches = sum(eng.kernels_per_step(v) for v in variants)
+    e2e = measure_e2e(eng, args.steps, args.batch, world)
+    us, W = measure_selector(eng)
+    roofline = roofline_for(eng, args, us, W, f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
 
-    # e2e through the host API: token in (pinned H2D), token out (D2H), every step
-    host_in = torch.zeros(args.batch, dtype=torch.int64).pin_memory()
-    host_out = torch.zeros(args.batch, dtype=torch.int64).pin_memory()
-    barrier(world)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        eng.tok.copy_(host_in, non_blocking=True)
-        eng.step()
-        host_out.copy_(eng.tok, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        host_in.copy_(host_out)
-    e2e_elapsed = max_over_ranks(time.perf_counter() - t0, world)
-    e2e = {"value": args.batch * args.steps * world / e2e_elapsed, "unit": "tok/s",
-           "h2d_bytes_per_step": 8 * args.batch, "d2h_bytes_per_step": 8 * args.batch}
-
-    # roofline of the fused forecast + top-k launch, in its steady-state form: one new row per map
-    # since the last update (incremental), width unchanged.  Decode state is snapshotted and restored.
-    snap = eng._snapshot()
-    ring, rmap = eng.sel.ring.clone(), eng.sel.rmap.clone()
-    st = eng.sel.states()
-    t_now = int(st["row_len"].max())
-    comp = torch.rand(eng.sel.n_maps, eng.sel.w_max, device="cuda") ** 8
-    reps = 20
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-    for i in range(reps):
-        eng._restore(snap)
-        eng.sel.ring.copy_(ring)
-        eng.sel.rmap.copy_(rmap)
-        eng.sel.push_compressed(comp, t_now)
-        ev[i][0].record()
-        eng.sel.step()
-        ev[i][1].record()
-    torch.cuda.synchronize()
-    sel_us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in ev)
-    eng._restore(snap)
-    eng.sel.ring.copy_(ring)
-    eng.sel.rmap.copy_(rmap)
-    del ring, rmap
-    n_maps = eng.sel.n_maps
-    W = int(st["width"].max())
-    H, K = cfg.history, cfg.middle_blocks
-    b_alg = n_maps * ((H + 1) * W * 4 + 4 * K)  # history window + new row + block ids, per launch
-    peak, peak_kind = measured_peak()
-    achieved = b_alg / (sel_us * 1e-6) / 1e9
-    traffic = profiled_traffic().get(f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "ap_sel_step (conv_forecast_kernel + sel_topk_kernel)",
-                "us_per_launch": round(sel_us, 2), "us_per_layer": round(sel_us / shape.n_layers, 3),
-                "algorithmic_bytes_per_launch": b_alg}
+    alt = None  # the other selection granularity on the same weights / KV
+    if not args.no_alt and G > 1:
+        other = "head" if args.group == "kv" else "kv"
+        eng.set_selection(1 if other == "head" else G)
+        first_token(eng)
+        for _ in range(args.warmup):
+            eng.step()
+        a_el, _ = timed_steps(eng, args.steps, world)
+        a_us, a_W = measure_selector(eng)
+        alt = {"selection": other, "value": round(args.batch * args.steps * world / a_el, 2), "unit": "tok/s",
+               "roofline": roofline_for(eng, args, a_us, a_W, f"{args.model}:{args.ctx}:{other}:{args.precision}")}
 
     dense = None
     if not args.no_dense:
@@ -267,17 +295,17 @@ def run_ours(args, rank, world):
         eng.capture_all()
         for _ in range(args.warmup):
             eng.step()
-        d_elapsed, _ = timed_steps(args.steps)
-        d_elapsed = max_over_ranks(d_elapsed, world)
+        d_elapsed, _ = timed_steps(eng, args.steps, world)
         dense = args.batch * args.steps * world / d_elapsed
 
     cpu = None
     if rank == 0 and world == 1:
         dt, cores = cpu_oracle_rate(args.ctx, args.budget, args.cpu_sample)
-        per_token = dt * n_maps
+        maps_head = args.batch * shape.n_layers * shape.n_q_heads  # the reference's per-head semantics
+        per_token = dt * maps_head
         cpu = {"value": round(args.batch / per_token, 6), "unit": "tok/s", "cores": cores, "kind": "port",
                "sample": f"{args.cpu_sample} oracle selector.step map-steps (max_pool+forward+mask+topk, "
-                         f"H=64, W={-(-args.ctx // 16)}) x {n_maps} maps per token, extrapolated; "
+                         f"H=64, W={-(-args.ctx // 16)}) timed, x {maps_head} (layer, head) maps per token; "
                          f"OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}",
                "s_per_map_step": round(dt, 4)}
 
@@ -288,11 +316,13 @@ def run_ours(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) KV)",
         "config": {"workload": f"{shape.name} decode, ctx {args.ctx}, budget {args.budget}, batch {args.batch}/GPU",
                    "model_shape": shape.name, "ctx": args.ctx, "budget": args.budget, "block": 16, "history": 64,
-                   "calibration_period": 5, "batch_per_gpu": args.batch, "selection": args.group,
+                   "calibration_period": 5, "batch_per_gpu": args.batch,
+                   "selection": {"kv": f"per KV head ({G} q-heads share a map)", "head": "per q-head"}[args.group],
                    "forecaster_precision": args.precision, "parallelism": f"replicas x{world}",
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+        "alt_selection": alt,
         "dense_tok_s": None if dense is None else round(dense, 2),
         "sparse_over_dense": None if dense is None else round(value / dense, 4),
         "clocks": clk.summary(),
@@ -307,9 +337,7 @@ def run_reference(args, rank, world):
         return
     from paper_2502_04077_b200.decode import SHAPES
     shape = SHAPES[args.model]
-    G = shape.n_q_heads // shape.n_kv_heads
-    maps = args.batch * shape.n_layers * (shape.n_q_heads if args.group == "head" else shape.n_kv_heads)
-    del G
+    maps = args.batch * shape.n_layers * shape.n_q_heads  # the reference's semantics: one selector per (layer, head)
     # warm-up then K steps; each step = one oracle map-step (a bounded sample of one token's 1024 map-steps)
     cpu_oracle_rate(args.ctx, args.budget, max(1, args.warmup))
     dt, cores = cpu_oracle_rate(args.ctx, args.budget, args.steps, seed=1)
@@ -319,7 +347,7 @@ def run_reference(args, rank, world):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic Dirichlet attention rows",
            "impl": "reference",
            "config": {"workload": f"{shape.name} decode, ctx {args.ctx}, budget {args.budget}, batch {args.batch}",
-                      "selection": args.group, "maps_per_token": maps},
+                      "selection": "per (layer, head) map — the reference's semantics", "maps_per_token": maps},
            "cpu_baseline": {"value": round(value, 6), "unit": "tok/s", "cores": cores, "kind": "port",
                             "sample": f"{args.steps} oracle selector.step map-steps per run, x{maps} maps/token"},
            "e2e": {"value": round(value, 6), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -209,6 +209,41 @@ int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_b
                    int32_t group, int emit, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Cross-token prefetch (kernel 5) — the real counterpart of the cross_token
+ * schedule the reference only models (prefetchsim.py:126-151).  K stays
+ * resident (calibration reads all of K); V lives in pinned, mapped host
+ * memory.  Per (layer, sequence, KV head) "vmap" the device keeps V pages
+ * [sink blocks | recent ring | k_cap middle pages]; vmap =
+ * (layer*n_seq + s)*n_kv_heads + h.  Requires KV-group selection
+ * (one selector map per KV head).
+ * ------------------------------------------------------------------------- */
+typedef struct ap_vpages {
+    int32_t k_cap, sink_pages, recent_pages, pad_;
+    int64_t host_t_max;
+    void* pages;            /* bf16 [n_vmaps][sink+recent+k_cap][16][128]            */
+    const void* host_v;     /* bf16 pinned+mapped [n_vmaps][host_t_max][128]         */
+    int32_t* mid_page;      /* [n_vmaps][k_cap] page of each current middle block    */
+    int32_t* old_blocks;    /* [n_vmaps][k_cap] resident middle blocks (sorted)      */
+    int32_t* old_pages;     /* [n_vmaps][k_cap]                                      */
+    int32_t* old_n;         /* [n_vmaps]                                             */
+    int64_t* bytes_copied;  /* [1] running count of host->device bytes (may be NULL) */
+} ap_vpages;
+
+/* After ap_sel_step predicted the next step's middle blocks: for every map of
+ * `layer`, keep the pages of blocks still selected and gather the new ones
+ * from host V (16-byte zero-copy loads).  Launch per layer on a side stream. */
+int ap_prefetch(const ap_selector* sel, const ap_vpages* vp, int32_t layer, int32_t n_seq, int32_t n_kv_heads,
+                int32_t maps_per_seq, void* stream);
+/* Write the step's V row (from qkv) to the paged store and through to host V. */
+int ap_v_append(const void* qkv, int32_t n_q_heads, int32_t n_kv_heads, const int32_t* seq_len, const ap_vpages* vp,
+                int32_t layer, int32_t n_seq, void* stream);
+/* Fill the sink pages and recent ring of every vmap from host V (prompt length t). */
+int ap_v_pages_init(const ap_vpages* vp, int64_t t, int64_t n_vmaps, void* stream);
+/* ap_attn_sparse with V read from the paged store of `layer` (offload mode). */
+int ap_attn_sparse_paged(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                         int32_t group, int emit, const ap_vpages* vp, int32_t layer, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Decode-engine helpers around the path (not reference functions: the
  * reference has no model; these exist so a whole LLaMA-shape decode step runs
  * from one CUDA graph).  bf16 tensors, row-major.

@@ -66,6 +66,18 @@ class AttnLayerDesc(ctypes.Structure):
     ]
 
 
+class VPages(ctypes.Structure):
+    """ap_vpages (include/attnpred.h)."""
+
+    _fields_ = [
+        ("k_cap", ctypes.c_int32), ("sink_pages", ctypes.c_int32), ("recent_pages", ctypes.c_int32),
+        ("pad_", ctypes.c_int32), ("host_t_max", ctypes.c_int64),
+        ("pages", ctypes.c_void_p), ("host_v", ctypes.c_void_p), ("mid_page", ctypes.c_void_p),
+        ("old_blocks", ctypes.c_void_p), ("old_pages", ctypes.c_void_p), ("old_n", ctypes.c_void_p),
+        ("bytes_copied", ctypes.c_void_p),
+    ]
+
+
 MAP_STATE_BYTES = ctypes.sizeof(MapState)  # 56
 
 _P = ctypes.c_void_p
@@ -90,6 +102,11 @@ SIGNATURES = {
                                      _I32, _I32, _I32, ctypes.c_int, _P]),
     "ap_attn_sparse": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.POINTER(Selector), _I32, _I32, _I32,
                                       ctypes.c_int, _P]),
+    "ap_prefetch": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.POINTER(VPages), _I32, _I32, _I32, _I32, _P]),
+    "ap_v_append": (ctypes.c_int, [_P, _I32, _I32, _P, ctypes.POINTER(VPages), _I32, _I32, _P]),
+    "ap_v_pages_init": (ctypes.c_int, [ctypes.POINTER(VPages), _I64, _I64, _P]),
+    "ap_attn_sparse_paged": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.POINTER(Selector), _I32, _I32,
+                                            _I32, ctypes.c_int, ctypes.POINTER(VPages), _I32, _P]),
     "ap_rmsnorm": (ctypes.c_int, [_P, _P, _P, _P, _I32, _I32, ctypes.c_float, _P]),
     "ap_rope_append": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _I32, ctypes.c_float, _P]),
     "ap_silu_mul": (ctypes.c_int, [_P, _P, _I32, _I32, _P]),

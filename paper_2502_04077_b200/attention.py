@@ -66,8 +66,14 @@ class DecodeAttention:
                                             _lib.stream_handle(stream)), "attn_dense")
 
     def sparse(self, q, k_cache, v_cache, seq_len, out, selector, *, emit=True, map_base=0, maps_per_seq=None,
-               group=1, stream=None):
+               group=1, vpages=None, layer=0, stream=None):
+        """v_cache is ignored (may be any tensor) when ``vpages`` (an OffloadedV) supplies paged V."""
         desc = self._desc(q, k_cache, v_cache, seq_len, out, self.n_splits_sparse)
         mps = maps_per_seq if maps_per_seq is not None else self.n_q_heads // group
-        _lib.check(_lib.fn("ap_attn_sparse")(ctypes.byref(desc), ctypes.byref(selector._desc), map_base, mps, group,
-                                             int(emit), _lib.stream_handle(stream)), "attn_sparse")
+        if vpages is None:
+            _lib.check(_lib.fn("ap_attn_sparse")(ctypes.byref(desc), ctypes.byref(selector._desc), map_base, mps,
+                                                 group, int(emit), _lib.stream_handle(stream)), "attn_sparse")
+        else:
+            _lib.check(_lib.fn("ap_attn_sparse_paged")(ctypes.byref(desc), ctypes.byref(selector._desc), map_base,
+                                                       mps, group, int(emit), ctypes.byref(vpages._desc), layer,
+                                                       _lib.stream_handle(stream)), "attn_sparse_paged")

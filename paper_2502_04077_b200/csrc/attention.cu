@@ -44,6 +44,9 @@ struct AttnParams {
     // selector binding
     ap_selector sel;
     int32_t map_base, maps_per_seq, group;  // map(s, h) = s*maps_per_seq + map_base + h/group
+    // paged V (offload mode, kernel 5): V blocks of the selection come from the page pool
+    ap_vpages vp;
+    int32_t paged, layer;
 };
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
@@ -249,6 +252,9 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
                 }
                 dst[j] = v;
             }
+            const int old_w = P.sel.slot_width[(int64_t)map * Hh + slot];
+            for (int64_t j = W + threadIdx.x; j < old_w; j += ATT_THREADS) dst[j] = 0.f;  // zero beyond W
+            __syncthreads();
             if (threadIdx.x == 0) {
                 ap_map_state st = ms;
                 P.sel.slot_width[(int64_t)map * Hh + slot] = (int32_t)W;
@@ -369,7 +375,18 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_partial_kernel(AttnParams 
             if (p < sink_end || p >= local_start) return true;
             return is_mid && p < mid_clip;
         };
-        process_block<NH, true, EMIT>(kh, vh, j, b, qf, st, take,
+        const __nv_bfloat16* vsrc = vh;
+        if (P.paged) {  // page of block j: sink | recent ring | middle page (prefetched, kernel 5)
+            const int64_t vmap = ((int64_t)P.layer * P.n_seq + s) * P.n_kv_heads + kvh;
+            const int npg = P.vp.sink_pages + P.vp.recent_pages + P.vp.k_cap;
+            int page;
+            if (is_mid) page = P.vp.sink_pages + P.vp.recent_pages + P.vp.mid_page[vmap * P.vp.k_cap + (u - sb - n_local)];
+            else if (j < P.vp.sink_pages) page = (int)j;
+            else page = P.vp.sink_pages + (int)(j % P.vp.recent_pages);
+            // rebase so that vsrc + p*HD addresses token p of this block inside its page
+            vsrc = reinterpret_cast<const __nv_bfloat16*>(P.vp.pages) + ((vmap * npg + page) * 16 - j * b) * HD;
+        }
+        process_block<NH, true, EMIT>(kh, vsrc, j, b, qf, st, take,
                                       [&](int h, float v) { if (lane == 0) bm[h * (int64_t)P.w_max + j] = v; });
     }
     float* part = P.partial + (((int64_t)s * P.n_q_heads + h0) * P.n_splits + split) * (HD + 2);
@@ -408,6 +425,9 @@ static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t m
     P.bmax = a->bmax; P.w_max = a->w_max; P.counters = a->counters;
     AP_REQUIRE(a->counters != nullptr, AP_EPARAM, "counters workspace is required");
     if (sel) P.sel = *sel; else memset(&P.sel, 0, sizeof(P.sel));
+    memset(&P.vp, 0, sizeof(P.vp));
+    P.paged = 0;
+    P.layer = 0;
     P.map_base = map_base; P.maps_per_seq = maps_per_seq; P.group = group < 1 ? 1 : group;
     const int G = a->n_q_heads / a->n_kv_heads;
     AP_REQUIRE(G == 1 || G == 2 || G == 4 || G == 8, AP_EPARAM, "q-heads per kv-head must be 1, 2, 4 or 8");
@@ -440,11 +460,26 @@ int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, in
     return launch_status("dense_partial_kernel");
 }
 
+int ap_attn_sparse_paged(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                         int32_t group, int emit, const ap_vpages* vp, int32_t layer, void* stream);
+
 int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
                    int32_t group, int emit, void* stream) {
+    return ap_attn_sparse_paged(a, sel, map_base, maps_per_seq, group, emit, nullptr, 0, stream);
+}
+
+int ap_attn_sparse_paged(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                         int32_t group, int emit, const ap_vpages* vp, int32_t layer, void* stream) {
     AttnParams P;
     int rc = make_params(a, sel, map_base, maps_per_seq, group, P);
     if (rc != AP_OK) return rc;
+    if (vp) {
+        AP_REQUIRE(group == a->n_q_heads / a->n_kv_heads, AP_EPARAM, "paged V needs one selection map per KV head");
+        AP_REQUIRE(vp->pages && vp->mid_page, AP_EPARAM, "bad paged-V descriptor");
+        P.vp = *vp;
+        P.paged = 1;
+        P.layer = layer;
+    }
     AP_REQUIRE(sel != nullptr, AP_EPARAM, "sparse attention needs a selector");
     P.with_v = 1; P.emit = emit;
     cudaStream_t st = as_stream(stream);

@@ -100,7 +100,9 @@ __global__ void sel_reset_kernel(ap_selector s) {
         z.width = 0; z.r_width = 0; z.n_mid = 0; z.pad_ = 0;
         s.state[i] = z;
     }
-    if (i < (int64_t)s.n_maps * s.history) s.slot_width[i] = 0;
+    // slot content unknown after a reset: the first push into a slot zero-fills [W, w_max), so ring rows
+    // are always zero beyond their own width (the forecaster relies on it instead of per-slot masks)
+    if (i < (int64_t)s.n_maps * s.history) s.slot_width[i] = s.w_max;
     const int64_t words = (s.w_max + 31) / 32;
     for (int64_t k = i; k < (int64_t)s.n_maps * words; k += (int64_t)gridDim.x * blockDim.x) s.mid_mask[k] = 0u;
     if (i == 0) *s.status = 0;
@@ -146,6 +148,8 @@ __global__ void sel_push_kernel(ap_selector s, const T* __restrict__ rows, int64
     } else {
         for (int64_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = (float)block_max(row, t, b, j, TakeAll{});
     }
+    const int old_w = s.slot_width[(int64_t)m * H + slot];
+    for (int64_t j = W + threadIdx.x; j < old_w; j += blockDim.x) dst[j] = 0.f;  // keep the row zero beyond W
     __syncthreads();
     if (threadIdx.x == 0) {
         s.slot_width[(int64_t)m * H + slot] = (int32_t)W;
@@ -166,6 +170,8 @@ __global__ void sel_push_f32_b16_kernel(ap_selector s, const float* __restrict__
     float* dst = s.ring + ((int64_t)m * H + slot) * s.w_max;
     const float* row = rows + (int64_t)m * row_stride;
     for (int64_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = block_max16_f32(row, t, j);
+    const int old_w = s.slot_width[(int64_t)m * H + slot];
+    for (int64_t j = W + threadIdx.x; j < old_w; j += blockDim.x) dst[j] = 0.f;  // keep the row zero beyond W
     __syncthreads();
     if (threadIdx.x == 0) {
         s.slot_width[(int64_t)m * H + slot] = (int32_t)W;
@@ -186,6 +192,8 @@ __global__ void sel_push_compressed_kernel(ap_selector s, const float* __restric
     float* dst = s.ring + ((int64_t)m * H + slot) * s.w_max;
     const float* src = comp + (int64_t)m * comp_stride;
     for (int64_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = src[j];
+    const int old_w = s.slot_width[(int64_t)m * H + slot];
+    for (int64_t j = W + threadIdx.x; j < old_w; j += blockDim.x) dst[j] = 0.f;  // keep the row zero beyond W
     __syncthreads();
     if (threadIdx.x == 0) {
         s.slot_width[(int64_t)m * H + slot] = (int32_t)W;

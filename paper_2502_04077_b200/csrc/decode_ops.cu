@@ -84,6 +84,7 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq
     } else if (head < Hq + Hkv) {
         dst = k_cache + (((int64_t)s * Hkv + (head - Hq)) * t_max + pos) * 128;
     } else {
+        if (!v_cache) return;  // offload mode: V goes to the paged store + host (ap_v_append)
         dst = v_cache + (((int64_t)s * Hkv + (head - Hq - Hkv)) * t_max + pos) * 128;
     }
     dst[i] = __float2bfloat16_rn(x1);

@@ -123,7 +123,7 @@ struct Task {
     int lo2;  // start of the bottom range (incremental)
 };
 
-__device__ __forceinline__ Task plan_task(const ConvParams& P, int map, int chunk) {
+__device__ __forceinline__ Task plan_task(const ConvParams& P, const ap_map_state& st, int chunk) {
     Task T;
     T.skip = false; T.full = true; T.merged = false; T.lo2 = 0;
     const int H = P.H;
@@ -133,7 +133,6 @@ __device__ __forceinline__ Task plan_task(const ConvParams& P, int map, int chun
         T.skip = chunk * TW >= T.W;
         return T;
     }
-    const ap_map_state st = P.state[map];
     T.W = st.width;
     T.n_pushed = st.n_pushed;
     if (P.k_mid <= 0 || st.width <= 0 || (st.counter % P.update_interval) != 0 || chunk * TW >= T.W) {
@@ -241,11 +240,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
-// Thread 0's work-list iterator: tasks blockIdx.x, +gridDim.x, ...; bands within a task.
+// Thread 0's work-list iterator: tasks blockIdx.x, +gridDim.x, ...; bands within a task.  The map
+// state of the following task is loaded one task ahead so planning never waits on global memory.
 struct Iter {
     int task, bi;
     Task T;
+    ap_map_state pf;  // state of map (task / n_chunks), loaded when the iterator reached the task before
 };
+
+__device__ __forceinline__ ap_map_state load_state(const ConvParams& P, int task) {
+    ap_map_state st{};
+    if (P.state && task < P.n_maps * P.n_chunks) st = P.state[task / P.n_chunks];
+    return st;
+}
 
 // Advance to the next band, fill its BandMeta and start the TMA bulk copies of its x rows.
 __device__ void next_band(const ConvParams& P, Iter& it, BandMeta& m, float* xdst, uint64_t* bar) {
@@ -259,7 +266,8 @@ __device__ void next_band(const ConvParams& P, Iter& it, BandMeta& m, float* xds
             return;
         }
         if (it.bi == 0) {
-            it.T = plan_task(P, it.task / P.n_chunks, it.task % P.n_chunks);
+            it.T = plan_task(P, it.pf, it.task % P.n_chunks);
+            it.pf = load_state(P, it.task + gridDim.x);  // consumed when the iterator moves on
             if (it.T.skip) {
                 it.task += gridDim.x;
                 continue;
@@ -293,11 +301,9 @@ __device__ void next_band(const ConvParams& P, Iter& it, BandMeta& m, float* xds
     for (int q = 0; q < m.n_out + 4; ++q) {
         const int p = m.o0 - 2 + q;
         int lim = 0;
-        if (p >= 0 && p < H && p >= m.first_real) {
-            const int slot = slot_m(m, H, sel, p);
-            const int width = sel ? P.slot_width[(int64_t)m.map * H + slot] : T.W;
-            lim = min(width, T.W);
-            if (lim > 0 && c_hi > c_lo) bytes += (uint32_t)(c_hi - c_lo) * 4;
+        if (p >= 0 && p < H && p >= m.first_real) {  // ring rows are zero beyond their own width
+            lim = T.W;
+            if (c_hi > c_lo) bytes += (uint32_t)(c_hi - c_lo) * 4;
         }
         lims[q] = lim;
         m.x_lim[q] = lim;
@@ -346,6 +352,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
         *s_xmax = 0;
         it.task = blockIdx.x;
         it.bi = 0;
+        it.pf = load_state(P, it.task);
         next_band(P, it, metas[0], xbuf, &mbar_x[0]);
     }
     tc_fence_before();

@@ -70,7 +70,7 @@ class DecodeEngine:
 
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
-                 seed: int = 0):
+                 seed: int = 0, offload_v: bool = False):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -99,9 +99,11 @@ class DecodeEngine:
         self.ln2 = [torch.ones(Hd, dtype=bf, device=dev) for _ in range(L)]
         self.lnf = torch.ones(Hd, dtype=bf, device=dev)
         self.lm_head = rnd(V, Hd)
-        # KV cache [L][S][Hkv][t_max][128]
+        # KV cache [L][S][Hkv][t_max][128]; with offload_v, V lives in pinned host memory and a small
+        # device page pool fed by the cross-token prefetch (kernel 5), K stays resident
+        self.offload = offload_v
         self.k_cache = torch.empty(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
-        self.v_cache = torch.empty(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
+        self.v_cache = None if offload_v else torch.empty(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
         # activations
         S = n_seq
         self.r = torch.zeros(S, Hd, dtype=bf, device=dev)
@@ -119,12 +121,21 @@ class DecodeEngine:
                                    n_splits_sparse=8, device=dev)
         self.maps_per_layer = Hq // group
         self.sel = None
+        from .selector import SelectorConfig
+        self.cfg = cfg or SelectorConfig(budget=1024)
         if mode == "sparse":
-            from .selector import SelectorConfig
-            self.cfg = cfg or SelectorConfig(budget=1024)
             install_weights(weights or init_weights(0))
             self.sel = BatchedSelector(self.cfg, S * L * self.maps_per_layer, self.t_max // 16, precision=precision,
                                        device=dev)
+        self.voff = None
+        if offload_v:
+            if mode != "sparse" or group != G:
+                raise ConfigError("V offload needs the sparse path with one selection map per KV head")
+            from .prefetch import OffloadedV
+            self.voff = OffloadedV(L, S, Hkv, self.t_max, k_cap=max(1, self.cfg.middle_blocks),
+                                   sink_tokens=self.cfg.sink_tokens, local_tokens=self.cfg.local_tokens, device=dev)
+            self.pf_stream = torch.cuda.Stream(device=dev)
+            self.pf_events = [torch.cuda.Event() for _ in range(L)]
         self.counter = 0  # selector step counter (host mirror; all maps move in lockstep)
         self.graphs = {}
         self._fill_kv(gen)
@@ -135,7 +146,16 @@ class DecodeEngine:
         torch = D.torch()
         for l in range(self.shape.n_layers):
             self.k_cache[l, :, :, : self.ctx_len].normal_(generator=gen)
-            self.v_cache[l, :, :, : self.ctx_len].normal_(generator=gen)
+            if self.voff is None:
+                self.v_cache[l, :, :, : self.ctx_len].normal_(generator=gen)
+            else:  # generate on the device, park in pinned host memory
+                tmp = torch.empty(self.n_seq, self.shape.n_kv_heads, self.ctx_len, 128, dtype=torch.bfloat16,
+                                  device=self.dev).normal_(generator=gen)
+                self.voff.host_v[l, :, :, : self.ctx_len].copy_(tmp)
+                del tmp
+        if self.voff is not None:
+            self.voff.init_pages(self.ctx_len)
+            torch.cuda.synchronize()
 
     def init_history(self, seed: int = 1):
         """Prefill-side history initialisation (selector.init_state, selector.py:61-70): the
@@ -174,10 +194,16 @@ class DecodeEngine:
             _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.ln1[l]),
                                              _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
         torch.matmul(self.y, self.wqkv[l].t(), out=self.qkv)
-        kc, vc = self.k_cache[l], self.v_cache[l]
+        kc = self.k_cache[l]
+        vc = self.v_cache[l] if self.voff is None else self.voff.layer_view(l)
         _lib.check(_lib.fn("ap_rope_append")(_lib.ptr(self.qkv), S, sh.n_q_heads, sh.n_kv_heads,
-                                             _lib.ptr(self.seq_len), _lib.ptr(self.q), _lib.ptr(kc), _lib.ptr(vc),
+                                             _lib.ptr(self.seq_len), _lib.ptr(self.q), _lib.ptr(kc),
+                                             None if self.voff is not None else _lib.ptr(vc),
                                              self.t_max, sh.rope_theta, s))
+        if self.voff is not None:
+            self.voff.append(self.qkv, sh.n_q_heads, self.seq_len, l)
+            if variant in ("plain", "calib"):  # this layer's predicted V blocks must have arrived
+                torch.cuda.current_stream().wait_event(self.pf_events[l])
         kw = dict(map_base=l * self.maps_per_layer, maps_per_seq=sh.n_layers * self.maps_per_layer,
                   group=self.group)
         if variant == "dense":
@@ -186,10 +212,12 @@ class DecodeEngine:
             self.att.dense(self.q, kc, vc, self.seq_len, self.att_out, with_v=True, emit=True, selector=self.sel,
                            **kw)
         elif variant == "calib":
-            self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=False, **kw)
-            self.att.dense(self.q, kc, vc, self.seq_len, None, with_v=False, emit=True, selector=self.sel, **kw)
+            self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=False, vpages=self.voff,
+                            layer=l, **kw)
+            self.att.dense(self.q, kc, kc, self.seq_len, None, with_v=False, emit=True, selector=self.sel, **kw)
         else:
-            self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=True, **kw)
+            self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=True, vpages=self.voff,
+                            layer=l, **kw)
         torch.matmul(self.att_out.view(S, -1), self.wo[l].t(), out=self.o)
         _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.o), _lib.ptr(self.r), _lib.ptr(self.ln2[l]), _lib.ptr(self.y),
                                          S, sh.hidden, sh.eps, s))
@@ -203,9 +231,20 @@ class DecodeEngine:
         S = self.n_seq
         s = _lib.stream_handle()
         _lib.check(_lib.fn("ap_advance")(_lib.ptr(self.seq_len), S, 1, s))
+        main = torch.cuda.current_stream()
+        if self.voff is not None and variant in ("plain", "calib"):
+            # cross-token prefetch: the blocks predicted at the end of the previous token stream in on a
+            # side stream, layer by layer, while this token's earlier layers compute
+            self.pf_stream.wait_stream(main)
+            with torch.cuda.stream(self.pf_stream):
+                for l in range(sh.n_layers):
+                    self.voff.prefetch(self.sel, l, sh.n_layers * self.maps_per_layer, stream=self.pf_stream)
+                    self.pf_events[l].record(self.pf_stream)
         torch.index_select(self.embed, 0, self.tok, out=self.r)
         for l in range(sh.n_layers):
             self._layer(l, variant)
+        if self.voff is not None and variant in ("plain", "calib"):
+            main.wait_stream(self.pf_stream)
         _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.lnf), _lib.ptr(self.y),
                                          S, sh.hidden, sh.eps, s))
         logits = torch.matmul(self.y, self.lm_head.t())
@@ -262,6 +301,10 @@ class DecodeEngine:
         if self.sel is not None:
             snap.update(state=self.sel.state.clone(), slot_width=self.sel.slot_width.clone(),
                         mid_blocks=self.sel.mid_blocks.clone(), mid_mask=self.sel.mid_mask.clone())
+        if self.voff is not None:
+            snap.update(old_n=self.voff.old_n.clone(), old_blocks=self.voff.old_blocks.clone(),
+                        old_pages=self.voff.old_pages.clone(), mid_page=self.voff.mid_page.clone(),
+                        bytes_copied=self.voff.bytes_copied.clone())
         del torch
         return snap
 
@@ -273,6 +316,27 @@ class DecodeEngine:
             self.sel.slot_width.copy_(snap["slot_width"])
             self.sel.mid_blocks.copy_(snap["mid_blocks"])
             self.sel.mid_mask.copy_(snap["mid_mask"])
+        if self.voff is not None and "old_n" in snap:
+            for k in ("old_n", "old_blocks", "old_pages", "mid_page", "bytes_copied"):
+                getattr(self.voff, k).copy_(snap[k])
+
+    def set_selection(self, group: int, precision: str | None = None):
+        """Rebuild the selector for another selection granularity (q-heads per map) on the same
+        weights / KV cache; positions reset to the prompt length, history re-initialised."""
+        G = self.shape.n_q_heads // self.shape.n_kv_heads
+        if G % group:
+            raise ConfigError("group must divide the GQA group size")
+        prec = precision or (self.sel.precision if self.sel is not None else "fp16x3")
+        self.sel = None
+        self.graphs.clear()
+        self.group = group
+        self.maps_per_layer = self.shape.n_q_heads // group
+        self.sel = BatchedSelector(self.cfg, self.n_seq * self.shape.n_layers * self.maps_per_layer,
+                                   self.t_max // 16, precision=prec, device=self.dev)
+        self.mode = "sparse"
+        self.counter = 0
+        self.seq_len.fill_(self.ctx_len)
+        self.init_history()
 
     def capture_all(self):
         """Capture every step variant this engine will replay (keeps capture out of timed regions)."""
@@ -293,4 +357,7 @@ class DecodeEngine:
         per_layer = 2 + 1 + 1  # rmsnorm x2, rope_append, silu_mul
         att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
         sel = 2 if (self.sel is not None and variant != "dense") else 0
-        return 1 + L * (per_layer + att) + 1 + sel  # advance + layers + final norm + selector
+        off = 0
+        if self.voff is not None:
+            off = L * (1 + (1 if variant in ("plain", "calib") else 0))  # v_append (+ prefetch) per layer
+        return 1 + L * (per_layer + att) + 1 + sel + off  # advance + layers + final norm + selector
