@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--precision", default="fp16x3")
     ap.add_argument("--no-dense", action="store_true", help="skip the full-attention comparator arm")
     ap.add_argument("--no-alt", action="store_true", help="skip the other selection granularity")
+    ap.add_argument("--offload", action="store_true",
+                    help="cfg4: V in pinned host memory + cross-token prefetch of the predicted blocks")
     ap.add_argument("--cpu-sample", type=int, default=48, help="oracle map-steps timed for cpu_baseline")
     return ap.parse_args()
 
@@ -192,6 +194,22 @@ def timed_steps(eng, n, world):
     return max_over_ranks(a.elapsed_time(b) / 1e3, world), variants
 
 
+def measure_h2d_peak(nbytes=1 << 29):
+    """Pinned host -> device cudaMemcpy bandwidth on this box (the roofline of the offload path)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(3):
+        d.copy_(h, non_blocking=True)
+    b.record()
+    b.synchronize()
+    return 3 * nbytes / (a.elapsed_time(b) / 1e3) / 1e9
+
+
 def measure_e2e(eng, n, batch, world):
     """Same metric through the host API: token in (pinned H2D), token out (D2H), every step."""
     import torch
@@ -263,15 +281,30 @@ def run_ours(args, rank, world):
     group = 1 if args.group == "head" else G
     cfg = SelectorConfig(budget=args.budget)
     total_steps = args.warmup + args.steps
+    if args.offload:
+        group = G
+        args.no_alt = True
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
-                       precision=args.precision, seed=rank)
+                       precision=args.precision, seed=rank, offload_v=args.offload)
     eng.init_history()
     first_token(eng)
     for _ in range(args.warmup):
         eng.step()
+    if eng.voff is not None:
+        eng.voff.bytes_copied.zero_()
     with ClockSampler(torch.cuda.current_device()) as clk:
         elapsed, variants = timed_steps(eng, args.steps, world)
     value = args.batch * args.steps * world / elapsed
+    prefetch = None
+    if eng.voff is not None:
+        moved = int(eng.voff.bytes_copied.item())
+        h2d = measure_h2d_peak()
+        prefetch = {"bytes_per_step": moved // args.steps, "avg_GBps_over_step": round(moved / elapsed / 1e9, 2),
+                    "h2d_copy_peak_GBps": round(h2d, 1),
+                    "resident_v_bytes_per_seq": eng.voff.pages[0].numel() * 2 * eng.voff.n_vmaps // args.batch,
+                    "host_v_bytes": eng.voff.host_v.numel() * 2,
+                    "note": "K resident (calibration reads all of K); V blocks predicted at step t are gathered "
+                            "from pinned host memory on a side stream during step t+1, per layer"}
     launches = sum(eng.kernels_per_step(v) for v in variants)
     e2e = measure_e2e(eng, args.steps, args.batch, world)
     us, W = measure_selector(eng)
@@ -293,10 +326,11 @@ def run_ours(args, rank, world):
     if not args.no_dense:
         eng.set_mode("dense")
         eng.capture_all()
-        for _ in range(args.warmup):
+        d_steps = args.steps if not args.offload else max(3, args.steps // 8)  # offload: V over PCIe each step
+        for _ in range(min(args.warmup, d_steps)):
             eng.step()
-        d_elapsed, _ = timed_steps(eng, args.steps, world)
-        dense = args.batch * args.steps * world / d_elapsed
+        d_elapsed, _ = timed_steps(eng, d_steps, world)
+        dense = args.batch * d_steps * world / d_elapsed
 
     cpu = None
     if rank == 0 and world == 1:
@@ -322,7 +356,7 @@ def run_ours(args, rank, world):
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
-        "alt_selection": alt,
+        "alt_selection": alt, "prefetch": prefetch,
         "dense_tok_s": None if dense is None else round(dense, 2),
         "sparse_over_dense": None if dense is None else round(value / dense, 4),
         "clocks": clk.summary(),

@@ -175,7 +175,7 @@ class DecodeEngine:
             lens.fill_(pos + 1)
             q.normal_(generator=gen)
             for l in range(L):
-                self.att.dense(q, self.k_cache[l], self.v_cache[l], lens, None, with_v=False, emit=True,
+                self.att.dense(q, self.k_cache[l], self.k_cache[l], lens, None, with_v=False, emit=True,
                                selector=self.sel, map_base=l * self.maps_per_layer,
                                maps_per_seq=L * self.maps_per_layer, group=self.group)
         torch.cuda.synchronize()
