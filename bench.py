@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--precision", default="fp16x3")
     ap.add_argument("--no-dense", action="store_true", help="skip the full-attention comparator arm")
     ap.add_argument("--no-alt", action="store_true", help="skip the other selection granularity")
+    ap.add_argument("--parallel", choices=["replicas", "heads"], default="replicas",
+                    help="N>1: independent sequences per GPU (weak) or one sequence with KV heads split (strong)")
     ap.add_argument("--offload", action="store_true",
                     help="cfg4: V in pinned host memory + cross-token prefetch of the predicted blocks")
     ap.add_argument("--cpu-sample", type=int, default=48, help="oracle map-steps timed for cpu_baseline")
@@ -284,8 +286,15 @@ def run_ours(args, rank, world):
     if args.offload:
         group = G
         args.no_alt = True
+    split = None
+    if args.parallel == "heads" and world > 1:
+        from paper_2502_04077_b200.distributed import HeadSplit
+        split = HeadSplit(rank, world, shape.n_q_heads, shape.n_kv_heads)
+        args.no_alt = True
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
-                       precision=args.precision, seed=rank, offload_v=args.offload)
+                       precision=args.precision, seed=rank if split is None else 0, offload_v=args.offload,
+                       head_split=split)
+    units = world if split is None else 1  # replicas: every rank decodes its own sequences
     eng.init_history()
     first_token(eng)
     for _ in range(args.warmup):
@@ -294,7 +303,7 @@ def run_ours(args, rank, world):
         eng.voff.bytes_copied.zero_()
     with ClockSampler(torch.cuda.current_device()) as clk:
         elapsed, variants = timed_steps(eng, args.steps, world)
-    value = args.batch * args.steps * world / elapsed
+    value = args.batch * args.steps * units / elapsed
     prefetch = None
     if eng.voff is not None:
         moved = int(eng.voff.bytes_copied.item())
@@ -347,12 +356,14 @@ def run_ours(args, rank, world):
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, N(0,1) KV)",
+        "scaling": "weak" if split is None else "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, N(0,1) KV)",
         "config": {"workload": f"{shape.name} decode, ctx {args.ctx}, budget {args.budget}, batch {args.batch}/GPU",
                    "model_shape": shape.name, "ctx": args.ctx, "budget": args.budget, "block": 16, "history": 64,
                    "calibration_period": 5, "batch_per_gpu": args.batch,
                    "selection": {"kv": f"per KV head ({G} q-heads share a map)", "head": "per q-head"}[args.group],
-                   "forecaster_precision": args.precision, "parallelism": f"replicas x{world}",
+                   "forecaster_precision": args.precision,
+                   "parallelism": f"replicas x{world}" if split is None else f"kv-head split x{world} + all-gather",
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,

@@ -70,10 +70,17 @@ class DecodeEngine:
 
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
-                 seed: int = 0, offload_v: bool = False):
+                 seed: int = 0, offload_v: bool = False, head_split=None):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
+        self.full_shape = shape
+        # KV-head split (distributed.HeadSplit): this rank owns kv_per_rank KV heads and their q-heads;
+        # per-layer attention outputs are all-gathered before the (replicated) o_proj
+        self.split = head_split if (head_split is not None and head_split.world > 1) else None
+        if self.split is not None:
+            from dataclasses import replace
+            shape = replace(shape, n_q_heads=self.split.q_per_rank, n_kv_heads=self.split.kv_per_rank)
         self.shape, self.n_seq, self.mode, self.group = shape, n_seq, mode, group
         G = shape.n_q_heads // shape.n_kv_heads
         if G % group:
@@ -91,8 +98,12 @@ class DecodeEngine:
             return (torch.randn(*sz, generator=gen, device=dev, dtype=bf) * std)
 
         self.embed = rnd(V, Hd)
-        self.wqkv = [rnd(shape.qkv_dim, Hd) for _ in range(L)]
-        self.wo = [rnd(Hd, Hq * 128) for _ in range(L)]
+        self.wqkv = [rnd(self.full_shape.qkv_dim, Hd) for _ in range(L)]
+        if self.split is not None:  # same random model on every rank; keep this rank's q/k/v rows
+            rows = torch.tensor(self.split.qkv_rows(128), device=dev)
+            self.wqkv = [w.index_select(0, rows).contiguous() for w in self.wqkv]
+        Hq_full = self.full_shape.n_q_heads
+        self.wo = [rnd(Hd, Hq_full * 128) for _ in range(L)]
         self.wgu = [rnd(2 * F, Hd) for _ in range(L)]
         self.wdown = [rnd(Hd, F) for _ in range(L)]
         self.ln1 = [torch.ones(Hd, dtype=bf, device=dev) for _ in range(L)]
@@ -111,6 +122,7 @@ class DecodeEngine:
         self.qkv = torch.zeros(S, shape.qkv_dim, dtype=bf, device=dev)
         self.q = torch.zeros(S, Hq, 128, dtype=bf, device=dev)
         self.att_out = torch.zeros(S, Hq, 128, dtype=bf, device=dev)
+        self.att_full = self.att_out if self.split is None else torch.zeros(S, Hq_full, 128, dtype=bf, device=dev)
         self.o = torch.zeros(S, Hd, dtype=bf, device=dev)
         self.gu = torch.zeros(S, 2 * F, dtype=bf, device=dev)
         self.act = torch.zeros(S, F, dtype=bf, device=dev)
@@ -218,7 +230,13 @@ class DecodeEngine:
         else:
             self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=True, vpages=self.voff,
                             layer=l, **kw)
-        torch.matmul(self.att_out.view(S, -1), self.wo[l].t(), out=self.o)
+        if self.split is not None:  # one collective per layer: the heads' outputs over NVLink
+            import torch.distributed as dist
+            parts = torch.empty(self.split.world, S, sh.n_q_heads, 128, dtype=self.att_out.dtype,
+                                device=self.att_out.device)
+            dist.all_gather_into_tensor(parts, self.att_out.contiguous())
+            self.att_full.copy_(parts.permute(1, 0, 2, 3).reshape(S, -1, 128))
+        torch.matmul(self.att_full.view(S, -1), self.wo[l].t(), out=self.o)
         _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.o), _lib.ptr(self.r), _lib.ptr(self.ln2[l]), _lib.ptr(self.y),
                                          S, sh.hidden, sh.eps, s))
         torch.matmul(self.y, self.wgu[l].t(), out=self.gu)
