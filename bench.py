@@ -212,7 +212,7 @@ def measure_h2d_peak(nbytes=1 << 29):
     return 3 * nbytes / (a.elapsed_time(b) / 1e3) / 1e9
 
 
-def measure_e2e(eng, n, batch, world):
+def measure_e2e(eng, n, batch, world, units=None):
     """Same metric through the host API: token in (pinned H2D), token out (D2H), every step."""
     import torch
     host_in = torch.zeros(batch, dtype=torch.int64).pin_memory()
@@ -227,7 +227,7 @@ def measure_e2e(eng, n, batch, world):
         torch.cuda.current_stream().synchronize()
         host_in.copy_(host_out)
     el = max_over_ranks(time.perf_counter() - t0, world)
-    return {"value": round(batch * n * world / el, 2), "unit": "tok/s",
+    return {"value": round(batch * n * (world if units is None else units) / el, 2), "unit": "tok/s",
             "h2d_bytes_per_step": 8 * batch, "d2h_bytes_per_step": 8 * batch}
 
 
@@ -315,7 +315,7 @@ def run_ours(args, rank, world):
                     "note": "K resident (calibration reads all of K); V blocks predicted at step t are gathered "
                             "from pinned host memory on a side stream during step t+1, per layer"}
     launches = sum(eng.kernels_per_step(v) for v in variants)
-    e2e = measure_e2e(eng, args.steps, args.batch, world)
+    e2e = measure_e2e(eng, args.steps, args.batch, world, units)
     us, W = measure_selector(eng)
     roofline = roofline_for(eng, args, us, W, f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
 
@@ -328,7 +328,7 @@ def run_ours(args, rank, world):
             eng.step()
         a_el, _ = timed_steps(eng, args.steps, world)
         a_us, a_W = measure_selector(eng)
-        alt = {"selection": other, "value": round(args.batch * args.steps * world / a_el, 2), "unit": "tok/s",
+        alt = {"selection": other, "value": round(args.batch * args.steps * units / a_el, 2), "unit": "tok/s",
                "roofline": roofline_for(eng, args, a_us, a_W, f"{args.model}:{args.ctx}:{other}:{args.precision}")}
 
     dense = None
@@ -339,7 +339,7 @@ def run_ours(args, rank, world):
         for _ in range(min(args.warmup, d_steps)):
             eng.step()
         d_elapsed, _ = timed_steps(eng, d_steps, world)
-        dense = args.batch * d_steps * world / d_elapsed
+        dense = args.batch * d_steps * units / d_elapsed
 
     cpu = None
     if rank == 0 and world == 1:
