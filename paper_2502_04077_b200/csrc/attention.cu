@@ -47,6 +47,7 @@ struct AttnParams {
     // paged V (offload mode, kernel 5): V blocks of the selection come from the page pool
     ap_vpages vp;
     int32_t paged, layer;
+    int32_t sparse_units;  // emission from the selection's units only (sparse path)
 };
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
@@ -77,19 +78,21 @@ struct WarpState {
 
 // Process one 16-token block j for NH heads.  take(p) decides token membership.
 // Writes the block max (log2 logits) of each head through bm_out(h, value) when EMIT.
-template <int NH, bool WITH_V, bool EMIT, typename Take, typename BmOut>
-__device__ __forceinline__ void process_block(const __nv_bfloat16* kh, const __nv_bfloat16* vh, int64_t j, int b,
-                                              const float (&qf)[NH][8], WarpState<NH, WITH_V>& st, Take take,
-                                              BmOut bm_out) {
+//
+// Lane layout: half = token parity, sub = 8-dim slice.  Each lane first forms
+// partial dots for its 8 tokens x 8 dims, then a transpose-reduce across the
+// 16 lanes of its half (xor 8, 4, 2: halving the live values each step, then
+// xor 1) leaves lane `sub` holding the full dot of token (sub >> 1) — 8
+// shuffles per head instead of 32, and one exp2 per lane instead of eight.
+template <bool WITH_V>
+__device__ __forceinline__ void load_block(const __nv_bfloat16* kh, const __nv_bfloat16* vh, int64_t j, int b,
+                                           uint4 (&kv)[8], uint4 (&vv)[8]) {
     const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
-    float s[NH][8];
-    uint4 kv[8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
         const int64_t p = j * b + jj * 2 + half;
         kv[jj] = __ldg(reinterpret_cast<const uint4*>(kh + p * HD + sub * 8));
     }
-    uint4 vv[8];
     if constexpr (WITH_V) {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
@@ -97,57 +100,106 @@ __device__ __forceinline__ void process_block(const __nv_bfloat16* kh, const __n
             vv[jj] = __ldg(reinterpret_cast<const uint4*>(vh + p * HD + sub * 8));
         }
     }
+}
+
+template <int NH, bool WITH_V, bool EMIT, typename Take, typename BmOut>
+__device__ __forceinline__ void compute_block(const uint4 (&kv)[8], const uint4 (&vv)[8], int64_t j, int b,
+                                              const float (&qf)[NH][8], WarpState<NH, WITH_V>& st, Take take,
+                                              BmOut bm_out) {
+    const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
+    float d[NH][8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
         float kf[8];
         bf16x8_to_f32(kv[jj], kf);
-        const int64_t p = j * b + jj * 2 + half;
-        const bool sel = take(p);
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
-            float d = 0.f;
+            float a = 0.f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) d = fmaf(qf[h][i], kf[i], d);
-            d += __shfl_xor_sync(0xffffffffu, d, 8);
-            d += __shfl_xor_sync(0xffffffffu, d, 4);
-            d += __shfl_xor_sync(0xffffffffu, d, 2);
-            d += __shfl_xor_sync(0xffffffffu, d, 1);
-            s[h][jj] = sel ? d : -INFINITY;
+            for (int i = 0; i < 8; ++i) a = fmaf(qf[h][i], kf[i], a);
+            d[h][jj] = a;
         }
     }
+    const bool b3 = (sub >> 3) & 1, b2 = (sub >> 2) & 1, b1 = (sub >> 1) & 1;
+    const int my_jj = (sub >> 1) & 7;
+    const bool my_sel = take(j * b + my_jj * 2 + half);
+    float pm[NH];
+    bool any = false;
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
-        float mx = s[h][0];
+        float e4[4];
 #pragma unroll
-        for (int jj = 1; jj < 8; ++jj) mx = fmaxf(mx, s[h][jj]);
+        for (int k = 0; k < 4; ++k) {
+            const float send = b3 ? d[h][k] : d[h][k + 4];
+            const float keep = b3 ? d[h][k + 4] : d[h][k];
+            e4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        float e2[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float send = b2 ? e4[k] : e4[k + 2];
+            const float keep = b2 ? e4[k + 2] : e4[k];
+            e2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        const float send = b1 ? e2[0] : e2[1];
+        float e1 = (b1 ? e2[1] : e2[0]) + __shfl_xor_sync(0xffffffffu, send, 2);
+        e1 += __shfl_xor_sync(0xffffffffu, e1, 1);
+        const float sc = my_sel ? e1 : -INFINITY;
+        float mx = sc;
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         if constexpr (EMIT) bm_out(h, mx);
-        if (mx == -INFINITY) continue;  // nothing selected in this block (uniform across the warp)
+        pm[h] = 0.f;
+        if (mx == -INFINITY) continue;  // nothing selected in this block for this head (warp-uniform)
+        any = true;
         const float m_new = fmaxf(st.m[h], mx);
         const float corr = exp2f(st.m[h] - m_new);
-        float psum = 0.f;
-        float pj[8];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-            pj[jj] = exp2f(s[h][jj] - m_new);
-            psum += pj[jj];
-        }
+        pm[h] = exp2f(sc - m_new);  // 0 for unselected tokens
+        // each token sits in two lanes (sub, sub^1): reduce over xor 16, 8, 4, 2 only
+        float psum = pm[h];
         psum += __shfl_xor_sync(0xffffffffu, psum, 16);
+        psum += __shfl_xor_sync(0xffffffffu, psum, 8);
+        psum += __shfl_xor_sync(0xffffffffu, psum, 4);
+        psum += __shfl_xor_sync(0xffffffffu, psum, 2);
         st.l[h] = st.l[h] * corr + psum;
         st.m[h] = m_new;
         if constexpr (WITH_V) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) st.acc[h][i] *= corr;
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                if (s[h][jj] == -INFINITY) continue;  // unselected / beyond t: never touch its V (may be garbage)
-                float vf[8];
-                bf16x8_to_f32(vv[jj], vf);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) st.acc[h][i] = fmaf(pj[jj], vf[i], st.acc[h][i]);
-            }
         }
     }
+    if constexpr (WITH_V) {
+        if (!any) return;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int src = half * 16 + jj * 2;  // lane holding token jj of this half
+            float pj[NH];
+            bool nz = false;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                pj[h] = __shfl_sync(0xffffffffu, pm[h], src);
+                nz |= pj[h] != 0.f;
+            }
+            if (!nz) continue;  // unselected / beyond t: never touch its V (may be garbage)
+            float vf[8];
+            bf16x8_to_f32(vv[jj], vf);  // once per token, shared by every head
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) st.acc[h][i] = fmaf(pj[h], vf[i], st.acc[h][i]);
+        }
+    }
+}
+
+template <int NH, bool WITH_V, bool EMIT, typename Take, typename BmOut>
+__device__ __forceinline__ void process_block(const __nv_bfloat16* kh, const __nv_bfloat16* vh, int64_t j, int b,
+                                              const float (&qf)[NH][8], WarpState<NH, WITH_V>& st, Take take,
+                                              BmOut bm_out) {
+    uint4 kv[8], vv[8];
+    load_block<WITH_V>(kh, vh, j, b, kv, vv);
+    compute_block<NH, WITH_V, EMIT>(kv, vv, j, b, qf, st, take, bm_out);
 }
 
 // Merge the 8 warps' states of a CTA and write the split partial (m, l, acc[128]).
@@ -243,7 +295,7 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
             const int slot = (int)(ms.n_pushed % Hh);
             float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
             float* bm0 = P.bmax + ((int64_t)s * P.n_q_heads + h0 + g0) * P.w_max;
-            for (int64_t j = threadIdx.x; j < W; j += ATT_THREADS) {
+            auto emit_block = [&](int64_t j) {
                 float v = 0.f;
                 for (int hh = 0; hh < P.group; ++hh) {
                     const float lg = __ldcg(bm0 + hh * (int64_t)P.w_max + j);
@@ -251,6 +303,24 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
                     bm0[hh * (int64_t)P.w_max + j] = -INFINITY;  // untouched marker for the next step
                 }
                 dst[j] = v;
+            };
+            if (P.sparse_units) {
+                // only the selected blocks carry mass (sink, local, middle): zero the row, then write them
+                for (int64_t j = threadIdx.x; j < W; j += ATT_THREADS) dst[j] = 0.f;
+                __syncthreads();
+                const int64_t sink_end = P.sel.sink < t ? P.sel.sink : t;
+                const int64_t sb = (sink_end + P.block - 1) / P.block;
+                int64_t lb = (t - P.sel.local > 0 ? t - P.sel.local : 0) / P.block;
+                if (lb < sb) lb = sb;
+                const int n_local = (int)(W - lb);
+                const int n_mid = ms.n_mid;
+                const int32_t* mid = P.sel.mid_blocks + (int64_t)map * (P.sel.k_mid > 0 ? P.sel.k_mid : 1);
+                for (int u = threadIdx.x; u < (int)sb + n_local + n_mid; u += ATT_THREADS) {
+                    const int64_t j = u < sb ? u : (u < sb + n_local ? lb + (u - sb) : mid[u - sb - n_local]);
+                    emit_block(j);
+                }
+            } else {
+                for (int64_t j = threadIdx.x; j < W; j += ATT_THREADS) emit_block(j);
             }
             const int old_w = P.sel.slot_width[(int64_t)map * Hh + slot];
             for (int64_t j = W + threadIdx.x; j < old_w; j += ATT_THREADS) dst[j] = 0.f;  // zero beyond W
@@ -309,9 +379,20 @@ __global__ void __launch_bounds__(ATT_THREADS) dense_partial_kernel(AttnParams P
     WarpState<NH, WITH_V> st;
     st.init();
     float* bm = P.bmax + ((int64_t)s * P.n_q_heads + h0) * P.w_max;
-    for (int64_t j = j0 + warp; j < j1; j += ATT_WARPS) {
-        process_block<NH, WITH_V, EMIT>(kh, vh, j, b, qf, st, [&](int64_t p) { return p < t; },
+    // one block ahead: the next block's K/V loads are in flight while this one is computed
+    uint4 kv[8], vv[8], kn[8], vn[8];
+    int64_t j = j0 + warp;
+    if (j < j1) load_block<WITH_V>(kh, vh, j, b, kv, vv);
+    for (; j < j1; j += ATT_WARPS) {
+        const int64_t jn = j + ATT_WARPS;
+        if (jn < j1) load_block<WITH_V>(kh, vh, jn, b, kn, vn);
+        compute_block<NH, WITH_V, EMIT>(kv, vv, j, b, qf, st, [&](int64_t p) { return p < t; },
                                         [&](int h, float v) { if (lane == 0) bm[h * (int64_t)P.w_max + j] = v; });
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            kv[q] = kn[q];
+            if constexpr (WITH_V) vv[q] = vn[q];
+        }
     }
     float* part = P.partial + (((int64_t)s * P.n_q_heads + h0) * P.n_splits + split) * (HD + 2);
     write_partial<NH, WITH_V>(st, sm_att, part, (int64_t)P.n_splits * (HD + 2));
@@ -426,6 +507,7 @@ static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t m
     AP_REQUIRE(a->counters != nullptr, AP_EPARAM, "counters workspace is required");
     if (sel) P.sel = *sel; else memset(&P.sel, 0, sizeof(P.sel));
     memset(&P.vp, 0, sizeof(P.vp));
+    P.sparse_units = 0;
     P.paged = 0;
     P.layer = 0;
     P.map_base = map_base; P.maps_per_seq = maps_per_seq; P.group = group < 1 ? 1 : group;
@@ -481,7 +563,7 @@ int ap_attn_sparse_paged(const ap_attn_layer* a, const ap_selector* sel, int32_t
         P.layer = layer;
     }
     AP_REQUIRE(sel != nullptr, AP_EPARAM, "sparse attention needs a selector");
-    P.with_v = 1; P.emit = emit;
+    P.with_v = 1; P.emit = emit; P.sparse_units = 1;
     cudaStream_t st = as_stream(stream);
     switch (P.group) {
         case 1: launch_sparse<1>(P, emit, st); break;
