@@ -237,7 +237,7 @@ def measure_selector(eng, reps=20):
     state is snapshotted and restored around the measurement."""
     import torch
     snap = eng._snapshot()
-    ring, rmap = eng.sel.ring.clone(), eng.sel.rmap.clone()
+    ring, rmap, rsum = eng.sel.ring.clone(), eng.sel.rmap.clone(), eng.sel.rsum.clone()
     st = eng.sel.states()
     t_now = int(st["row_len"].max())
     comp = torch.rand(eng.sel.n_maps, eng.sel.w_max, device="cuda") ** 8
@@ -246,6 +246,7 @@ def measure_selector(eng, reps=20):
         eng._restore(snap)
         eng.sel.ring.copy_(ring)
         eng.sel.rmap.copy_(rmap)
+        eng.sel.rsum.copy_(rsum)
         eng.sel.push_compressed(comp, t_now)
         ev[i][0].record()
         eng.sel.step()
@@ -255,6 +256,7 @@ def measure_selector(eng, reps=20):
     eng._restore(snap)
     eng.sel.ring.copy_(ring)
     eng.sel.rmap.copy_(rmap)
+    eng.sel.rsum.copy_(rsum)
     W = int(st["width"].max())
     return us, W
 

@@ -126,6 +126,7 @@ typedef struct ap_selector {
     int32_t pad_;
     float* ring;              /* [n_maps][H][w_max] compressed history rows        */
     float* rmap;              /* [n_maps][H][w_max] per-row predictor contributions */
+    double* rsum;             /* [n_maps][w_max] running sum of rmap over the H slots */
     int32_t* slot_width;      /* [n_maps][H] width of the row stored in each slot   */
     ap_map_state* state;      /* [n_maps]                                           */
     float* scores;            /* [n_maps][w_max] last forecast (selector.py:133)    */

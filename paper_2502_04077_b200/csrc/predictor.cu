@@ -10,7 +10,10 @@
 // recomputes the history rows whose 3x3∘3x3 receptive field changed:
 // rows {0,1} (new zero padding at the top) and rows [H-s-2, H) (the s new
 // rows at the bottom), plus every row of the column chunks touched by a
-// width change.  See DESIGN.md §Predictor.
+// width change.  The sum over i is a per-column fp64 running sum kept equal
+// to sum_slot rmap[slot] (S += r_new - r_old for every rewritten slot; a full
+// task rebuilds it), so an incremental step reads and writes only the
+// recomputed rows.  See DESIGN.md §Predictor.
 //
 // conv2 (92% of the FLOPs) is an implicit GEMM on the 5th-gen tensor cores:
 // M = 128 consecutive output pixels of one history row, N = 32 out channels,
@@ -19,6 +22,9 @@
 // SWIZZLE_NONE K-major a1 tile in shared memory; accumulators live in TMEM
 // and the epilogue (bias, ReLU, dot w3) reads them with tcgen05.ld.
 // conv1 (K = 9, 3% of FLOPs) runs on the FMA pipe straight into that tile.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 
 namespace ap {
@@ -33,6 +39,11 @@ __constant__ float c_w[AP_PARAM_COUNT];
 // 11+11 significant bits without overflow; the epilogue undoes the scale.
 constexpr int BTILE_BYTES = 1024;
 __device__ __align__(16) uint4 g_bpack[2 * 9 * BTILE_BYTES / 16];
+// Sliding-window B operands of the warp-specialised kernel: per [hi/lo][dj] an N=96 x K=16 tile
+// whose rows stack w2[:, :, di, dj] for di = 2, 1, 0 (the three output rows an a1 row feeds);
+// element (n, k) at byte (k/8)*1536 + n*16 + (k%8)*2  (LBO 1536, SBO 128).
+constexpr int B96_BYTES = 96 * 16 * 2;
+__device__ __align__(16) uint4 g_bpack96[2 * 3 * B96_BYTES / 16];
 __device__ int g_wexp;            // power-of-2 exponent applied to w2
 __device__ float g_w1abs[16];     // sum_t |w1[c][t]|  (a1 magnitude bound)
 __device__ float g_b1abs[16];     // |b1[c]|
@@ -64,7 +75,6 @@ constexpr int RING_COLS = 3 * 3 * 2 * 8;   // 144
 constexpr int ACC_BASE = RING_COLS;        // accumulators at [144, 144 + 96)
 static_assert(ACC_BASE + MAXO * 32 <= TMEM_COLS, "TMEM budget");
 constexpr int NWARPS = NTHREADS / 32;
-constexpr int PREF = 8;             // r rows per warp prefetched in registers (H <= 64)
 
 // One CTA: w2 scale, then the [hi/lo][tap] fp16 tiles and the a1 magnitude bounds.
 __global__ void pack_weights_kernel() {
@@ -97,6 +107,12 @@ __global__ void pack_weights_kernel() {
         const int off = (k / 8) * 256 + n * 8 + (k % 8);  // in fp16 elements
         base[(0 * 9 + tap) * 512 + off] = hi;
         base[(1 * 9 + tap) * 512 + off] = lo;
+        // N=96 window tile: row n96 = (2 - di) * 32 + n
+        const int di = tap / 3, dj = tap % 3, n96 = (2 - di) * 32 + n;
+        __half* b96 = reinterpret_cast<__half*>(g_bpack96);
+        const int off96 = (k / 8) * 768 + n96 * 8 + (k % 8);
+        b96[(0 * 3 + dj) * (B96_BYTES / 2) + off96] = hi;
+        b96[(1 * 3 + dj) * (B96_BYTES / 2) + off96] = lo;
     }
 }
 
@@ -107,10 +123,13 @@ struct ConvParams {
     float* rmap;            // r rows: rmap + map*map_stride + slot*pitch + col (same geometry)
     float* scores;          // scores + map*score_stride + col
     int64_t score_stride;
+    double* rsum;           // rsum + map*pitch + col: running sum over the H ring slots of r (selector
+                            // mode; invariant rsum == sum_slot rmap[slot]); null => explicit grids
     const int32_t* slot_width;  // [map][H] (selector mode)
     const ap_map_state* state;  // [map]    (selector mode); null => explicit grids
     int32_t n_maps, H, W_explicit, n_chunks, update_interval, k_mid;
     int32_t* status;
+    int32_t debug;  // ATTNPRED_FORECAST_DEBUG bit mask (profiling only): 1 no conv1, 2 no MMA, 4 no epilogue
 };
 
 // Which history rows a task recomputes: full = [0, H); incremental (s new rows
@@ -204,9 +223,9 @@ struct BandMeta {
     int o0, n_out;                    // output rows [o0, o0 + n_out)
     int out_slot[MAXO];
     int x_lim[MAXX];                  // x tile row q (position o0-2+q): valid columns are [0, x_lim)
+    int aexp;                         // fp16 operand scale exponent (warp-specialised kernel)
 };
 
-__device__ __forceinline__ bool recomputed_m(const BandMeta& m, int p) { return m.full || p < 2 || p >= m.lo2; }
 __device__ __forceinline__ int slot_m(const BandMeta& m, int H, bool sel, int p) {
     if (!sel) return p;
     const int s2 = m.base_slot + p;
@@ -221,16 +240,11 @@ struct SmemLayout {
     static constexpr int off_bpack = 0;
     static constexpr int off_a1 = off_bpack + kBpack;
     static constexpr int off_x = off_a1 + kA1;                   // [2 buffers][MAXX][XC4] fp32
-    static constexpr int off_sum = off_x + kX;                   // [NWARPS][128] partial sums
-    static constexpr int off_meta = off_sum + NWARPS * TW * 4;   // [2] BandMeta
+    static constexpr int off_sum = off_x + kX;                   // double [2][128] partial sums
+    static constexpr int off_meta = off_sum + 2 * TW * 8;        // [2] BandMeta
     static constexpr int off_bar = (off_meta + 2 * (int)sizeof(BandMeta) + 15) / 16 * 16;
     static constexpr int total = off_bar + 48;  // mbar(mma), mbar_x[2], tmem slot, xmax
 };
-
-__device__ __forceinline__ float4 ld4(const float* p, bool vec) {
-    if (vec) return __ldg(reinterpret_cast<const float4*>(p));
-    return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), __ldg(p + 3));
-}
 
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -324,7 +338,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
     using L = SmemLayout<PREC>;
     extern __shared__ __align__(1024) uint8_t smem[];
     float* xbuf = reinterpret_cast<float*>(smem + L::off_x);
-    float* psum = reinterpret_cast<float*>(smem + L::off_sum);
+    double* psum = reinterpret_cast<double*>(smem + L::off_sum);
     BandMeta* metas = reinterpret_cast<BandMeta*>(smem + L::off_meta);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + L::off_bar);
     uint64_t* mbar_x = reinterpret_cast<uint64_t*>(smem + L::off_bar + 8);   // [2]
@@ -335,7 +349,6 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
     uint32_t tmem_base = 0, phase = 0;
     const int H = P.H;
     const bool sel = P.state != nullptr;
-    const bool vec = (P.pitch % 4) == 0;
 
     if constexpr (kTC) {  // B operands once per persistent CTA
         const uint4* src = g_bpack;
@@ -362,26 +375,18 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
     const int wexp = kTC ? g_wexp : 0;
     const float b1max = kTC ? g_b1abs[0] : 0.f, w1max = kTC ? g_w1abs[0] : 0.f;  // packed maxima (see pack)
     uint32_t xphase[2] = {0u, 0u};
-    float4 pre[PREF];
+    // Each thread owns one pixel column and the output rows j = half, half + 2, ... of every band;
+    // dS accumulates its (r_new - r_old) over the task's bands, the two halves meet at the last band.
+    const int half = kTC ? (warp >> 2) : tid / TW;
+    double dS = 0.0;
     int buf = 0;
 
     for (;;) {
         const BandMeta& m = metas[buf];
         if (!m.valid) break;
         const int W = m.W, w0 = m.chunk * TW;
-        const int c4 = w0 + 4 * lane;
         float* rmap = P.rmap + (int64_t)m.map * P.map_stride;
-        // ---- 0. first band of a task: prefetch the r rows it does not recompute
-        //         (warp w: rows p = w + 8i, lane: 4 columns) — overlaps everything below
-        if (m.first) {
-#pragma unroll
-            for (int i = 0; i < PREF; ++i) {
-                const int p = warp + NWARPS * i;
-                pre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (p < H && c4 < W && !recomputed_m(m, p))
-                    pre[i] = ld4(rmap + (int64_t)slot_m(m, H, sel, p) * P.pitch + c4, vec);
-            }
-        }
+        if (m.first) dS = 0.0;
         // ---- 1. thread 0 starts the next band's x-row copies into the other buffer
         if (tid == 0) next_band(P, it, metas[buf ^ 1], xbuf + (buf ^ 1) * MAXX * XC4, &mbar_x[buf ^ 1]);
         mbar_wait(&mbar_x[buf], xphase[buf]);
@@ -537,7 +542,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
                     const float s2 = fmaf(acc[n] * u2, u, c_w[OFF_B2 + n]);
                     r = fmaf(c_w[OFF_W3 + n], fmaxf(s2, 0.f), r);
                 }
-                if (ecol < W) rmap[(int64_t)m.out_slot[j] * P.pitch + ecol] = r;
+                if (ecol < W) {
+                    float* dst = rmap + (int64_t)m.out_slot[j] * P.pitch + ecol;
+                    dS += (double)r - (m.full ? 0.0 : (double)*dst);
+                    *dst = r;
+                }
             }
             tc_fence_before();
         } else {
@@ -565,37 +574,27 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
                 float r = 0.f;
 #pragma unroll
                 for (int n = 0; n < 32; ++n) r = fmaf(c_w[OFF_W3 + n], fmaxf(acc[n], 0.f), r);
-                if (ecol < W) rmap[(int64_t)m.out_slot[j] * P.pitch + ecol] = r;
+                if (ecol < W) {
+                    float* dst = rmap + (int64_t)m.out_slot[j] * P.pitch + ecol;
+                    dS += (double)r - (m.full ? 0.0 : (double)*dst);
+                    *dst = r;
+                }
             }
         }
         __syncthreads();  // a1 tile, TMEM accumulators and r writes are complete
 
-        // ---- 5. last band: forecast for this chunk: b3 + (1/H) sum_p r[p]; warp w sums rows
-        //         p = w (mod 8) in increasing p, the 8 partials are added in warp order.
+        // ---- 5. last band: forecast for this chunk, b3 + (1/H) S with S the updated running sum
         if (m.last) {
-            float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (c4 < W) {
-#pragma unroll
-                for (int i = 0; i < PREF; ++i) {
-                    const int p = warp + NWARPS * i;
-                    if (p < H) {
-                        const float4 v = recomputed_m(m, p) ? ld4(rmap + (int64_t)slot_m(m, H, sel, p) * P.pitch + c4, vec)
-                                                            : pre[i];
-                        acc4.x += v.x; acc4.y += v.y; acc4.z += v.z; acc4.w += v.w;
-                    }
-                }
-                for (int p = warp + NWARPS * PREF; p < H; p += NWARPS) {
-                    const float4 v = ld4(rmap + (int64_t)slot_m(m, H, sel, p) * P.pitch + c4, vec);
-                    acc4.x += v.x; acc4.y += v.y; acc4.z += v.z; acc4.w += v.w;
-                }
-            }
-            reinterpret_cast<float4*>(psum + warp * TW)[lane] = acc4;
+            const int pix = kTC ? ((warp & 3) * 32 + lane) : (tid & (TW - 1));
+            psum[half * TW + pix] = dS;
             __syncthreads();
             if (tid < TW && w0 + tid < W) {
-                float sum = psum[tid];
-#pragma unroll
-                for (int w = 1; w < NWARPS; ++w) sum += psum[w * TW + tid];
-                P.scores[(int64_t)m.map * P.score_stride + w0 + tid] = c_w[OFF_B3] + sum / (float)H;
+                const int64_t at = (int64_t)m.map * P.pitch + w0 + tid;
+                double S = (m.full || !P.rsum) ? 0.0 : P.rsum[at];
+                S += psum[tid];
+                S += psum[TW + tid];
+                if (P.rsum) P.rsum[at] = S;
+                P.scores[(int64_t)m.map * P.score_stride + w0 + tid] = c_w[OFF_B3] + (float)S / (float)H;
             }
             __syncthreads();
         }
@@ -607,6 +606,21 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
         __syncthreads();
         if (warp == 0) tmem_dealloc(tmem_base, TMEM_COLS);
     }
+}
+
+}  // namespace ap
+#include "forecast_ws.cuh"
+namespace ap {
+
+template <int PREC>
+static int grid_ctas_ws() {
+    static int cached = 0;
+    if (!cached) {
+        cudaFuncSetAttribute(ws::conv_forecast_ws_kernel<PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ws::Smem<PREC>::total);
+        cached = ap_device_sm_count();  // one 16-warp CTA (and all 512 TMEM columns) per SM
+    }
+    return cached;
 }
 
 template <int PREC>
@@ -634,7 +648,26 @@ static int grid_ctas() {
     return cached;
 }
 
-static int launch_conv(const ConvParams& P, int precision, cudaStream_t st) {
+// ATTNPRED_FORECAST_KERNEL=bands selects the non-specialised kernel (A/B comparisons)
+static bool ws_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ATTNPRED_FORECAST_KERNEL");
+        v = !(e && strcmp(e, "bands") == 0);
+    }
+    return v == 1;
+}
+
+static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
+    ConvParams P = Pin;
+    {
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char* e = getenv("ATTNPRED_FORECAST_DEBUG");
+            dbg = e ? atoi(e) : 0;
+        }
+        P.debug = dbg;
+    }
     const int n_tasks = P.n_maps * P.n_chunks;
     if (n_tasks == 0) return AP_OK;
     switch (precision) {
@@ -644,13 +677,23 @@ static int launch_conv(const ConvParams& P, int precision, cudaStream_t st) {
             break;
         }
         case AP_PREC_F16X3: {
-            int g = grid_ctas<AP_PREC_F16X3>();
-            conv_forecast_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_F16X3>::total, st>>>(P);
+            if (P.pitch % 4 == 0 && ws_enabled()) {
+                int g = grid_ctas_ws<AP_PREC_F16X3>();
+                ws::conv_forecast_ws_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, ws::NT, ws::Smem<AP_PREC_F16X3>::total, st>>>(P);
+            } else {
+                int g = grid_ctas<AP_PREC_F16X3>();
+                conv_forecast_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_F16X3>::total, st>>>(P);
+            }
             break;
         }
         case AP_PREC_F16: {
-            int g = grid_ctas<AP_PREC_F16>();
-            conv_forecast_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_F16>::total, st>>>(P);
+            if (P.pitch % 4 == 0 && ws_enabled()) {
+                int g = grid_ctas_ws<AP_PREC_F16>();
+                ws::conv_forecast_ws_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, ws::NT, ws::Smem<AP_PREC_F16>::total, st>>>(P);
+            } else {
+                int g = grid_ctas<AP_PREC_F16>();
+                conv_forecast_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, NTHREADS, SmemLayout<AP_PREC_F16>::total, st>>>(P);
+            }
             break;
         }
         default:
@@ -718,6 +761,7 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream) {
         P.map_stride = (int64_t)s->history * s->w_max;
         P.pitch = s->w_max;
         P.rmap = s->rmap;
+        P.rsum = s->rsum;
         P.scores = s->scores;
         P.score_stride = s->w_max;
         P.slot_width = s->slot_width;
@@ -734,6 +778,12 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream) {
     }
     launch_sel_topk(*s, st);
     return launch_status("sel_topk_kernel");
+}
+
+// debug: copy the warp-specialised kernel's per-CTA role counters (ATTNPRED_FORECAST_DEBUG & 8)
+int ap_debug_prof(unsigned long long* host_out, int n) {
+    return cudaMemcpyFromSymbol(host_out, ws::g_prof, sizeof(unsigned long long) * (n < 16 * 160 ? n : 16 * 160)) ==
+                   cudaSuccess ? AP_OK : AP_ECUDA;
 }
 
 int ap_sel_grid_ctas(int precision) {
