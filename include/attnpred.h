@@ -128,6 +128,7 @@ typedef struct ap_selector {
     float* rmap;              /* [n_maps][H][w_max] per-row predictor contributions */
     double* rsum;             /* [n_maps][w_max] running sum of rmap over the H slots */
     int32_t* slot_width;      /* [n_maps][H] width of the row stored in each slot   */
+    float* slot_xmax;         /* [n_maps][H] max |x| of the row stored in each slot */
     ap_map_state* state;      /* [n_maps]                                           */
     float* scores;            /* [n_maps][w_max] last forecast (selector.py:133)    */
     int32_t* mid_blocks;      /* [n_maps][k_mid] middle block ids, ascending        */

@@ -48,7 +48,7 @@ class Selector(ctypes.Structure):
         ("local", ctypes.c_int32), ("calib_period", ctypes.c_int32), ("update_interval", ctypes.c_int32),
         ("pad_", ctypes.c_int32),
         ("ring", ctypes.c_void_p), ("rmap", ctypes.c_void_p), ("rsum", ctypes.c_void_p),
-        ("slot_width", ctypes.c_void_p),
+        ("slot_width", ctypes.c_void_p), ("slot_xmax", ctypes.c_void_p),
         ("state", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("mid_blocks", ctypes.c_void_p),
         ("mid_mask", ctypes.c_void_p), ("status", ctypes.c_void_p),
     ]

@@ -60,6 +60,7 @@ class BatchedSelector:
         self.rmap = torch.zeros(n_maps, H, w_max, dtype=f32, device=dev)
         self.rsum = torch.zeros(n_maps, w_max, dtype=torch.float64, device=dev)
         self.slot_width = torch.zeros(n_maps, H, dtype=i32, device=dev)
+        self.slot_xmax = torch.zeros(n_maps, H, dtype=f32, device=dev)
         self.state = torch.zeros(n_maps * _STATE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         self.scores = torch.zeros(n_maps, w_max, dtype=f32, device=dev)
         self.mid_blocks = torch.zeros(n_maps, max(self.k_mid, 1), dtype=i32, device=dev)
@@ -70,7 +71,7 @@ class BatchedSelector:
             sink=cfg.sink_tokens, local=cfg.local_tokens, calib_period=cfg.calibration_period,
             update_interval=cfg.update_interval, pad_=0,
             ring=self.ring.data_ptr(), rmap=self.rmap.data_ptr(), rsum=self.rsum.data_ptr(),
-            slot_width=self.slot_width.data_ptr(),
+            slot_width=self.slot_width.data_ptr(), slot_xmax=self.slot_xmax.data_ptr(),
             state=self.state.data_ptr(), scores=self.scores.data_ptr(), mid_blocks=self.mid_blocks.data_ptr(),
             mid_mask=self.mid_mask.data_ptr(), status=self.status.data_ptr(),
         )

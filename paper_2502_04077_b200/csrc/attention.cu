@@ -295,6 +295,7 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
             const int slot = (int)(ms.n_pushed % Hh);
             float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
             float* bm0 = P.bmax + ((int64_t)s * P.n_q_heads + h0 + g0) * P.w_max;
+            float mx = 0.f;  // max of the emitted row (forecaster operand scale)
             auto emit_block = [&](int64_t j) {
                 float v = 0.f;
                 for (int hh = 0; hh < P.group; ++hh) {
@@ -303,6 +304,7 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
                     bm0[hh * (int64_t)P.w_max + j] = -INFINITY;  // untouched marker for the next step
                 }
                 dst[j] = v;
+                mx = track_row_max(mx, v, P.sel.status);
             };
             if (P.sparse_units) {
                 // only the selected blocks carry mass (sink, local, middle): zero the row, then write them
@@ -324,8 +326,9 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
             }
             const int old_w = P.sel.slot_width[(int64_t)map * Hh + slot];
             for (int64_t j = W + threadIdx.x; j < old_w; j += ATT_THREADS) dst[j] = 0.f;  // zero beyond W
-            __syncthreads();
+            mx = cta_max_nonneg(mx);
             if (threadIdx.x == 0) {
+                P.sel.slot_xmax[(int64_t)map * Hh + slot] = mx;
                 ap_map_state st = ms;
                 P.sel.slot_width[(int64_t)map * Hh + slot] = (int32_t)W;
                 st.n_pushed += 1;

@@ -34,6 +34,67 @@ __device__ __forceinline__ void raise_status(int32_t* status, int code) {
     if (status) atomicCAS(status, 0, code);  // first error wins
 }
 
+// Max over the CTA of non-negative per-thread values; every thread must call it (contains
+// __syncthreads); the result is valid in thread 0.
+__device__ __forceinline__ float cta_max_nonneg(float v) {
+    __shared__ float red[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int w = 1; w < (int)((blockDim.x + 31) / 32); ++w) v = fmaxf(v, red[w]);
+    __syncthreads();
+    return v;
+}
+
+// Packed fp32 FMA (sm_100 FFMA2): {d0, d1} = {a0, a1} * w + {d0, d1}; each lane rounds exactly
+// like fmaf.
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float w) {
+    unsigned long long d, a, b;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(w));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(d0), "f"(d1));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+
+// Packed fp32 FMA with per-lane b: {d0, d1} = {a0, a1} * {b0, b1} + {d0, d1}.
+__device__ __forceinline__ void ffma2v(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    unsigned long long d, a, b;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(b0), "f"(b1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(d0), "f"(d1));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+
+// {v0, v1} -> f16x2 (round to nearest), v0 in the low half
+__device__ __forceinline__ uint32_t pack_f16x2(float v0, float v1) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(v1), "f"(v0));
+    return r;
+}
+
+// fp16 hi/lo split of two non-negative fp32 values below 2^15: hi = v truncated to fp16's 11
+// significant bits (exact in fp16 for v >= 2^-14), lo = v - hi (exact in fp32; rounded once to
+// fp16).  Returns the pairs packed as f16x2 with v0 in the low half.
+__device__ __forceinline__ void split_f16x2(float v0, float v1, uint32_t& hi2, uint32_t& lo2) {
+    const float h0 = __uint_as_float(__float_as_uint(v0) & 0xffffe000u);
+    const float h1 = __uint_as_float(__float_as_uint(v1) & 0xffffe000u);
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hi2) : "f"(h1), "f"(h0));
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(lo2) : "f"(v1 - h1), "f"(v0 - h0));
+}
+
+// Running max |v| of values written to a ring row; non-finite values raise AP_ENUMERIC (the
+// forecaster's input check, done where the row is produced).
+__device__ __forceinline__ float track_row_max(float mx, float v, int32_t* status) {
+    const float a = fabsf(v);
+    if (!(a <= 3.402823466e38f)) raise_status(status, AP_ENUMERIC);
+    return fmaxf(mx, a);
+}
+
 // -------------------------------------------------------------- typed access
 template <typename T> __device__ __forceinline__ double to_f64(T v);
 template <> __device__ __forceinline__ double to_f64<float>(float v) { return (double)v; }
@@ -171,9 +232,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred done;\n\t"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
         "@!done bra WAIT_%=;\n\t}"
-        :: "r"(addr), "r"(parity) : "memory");
+        :: "r"(addr), "r"(parity), "r"(1000000u) : "memory");  // suspend (<= 1 ms) instead of spinning
 }
 
 // 32 lanes x 32 columns of zeros -> TMEM (used to clear accumulators).
@@ -200,6 +261,38 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Split form for software pipelining: start a load, do other work, then wait.  The wait names the
+// destination registers so the compiler cannot read them before it.
+__device__ __forceinline__ void tmem_ld32_start(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16_start(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :: "memory");
 }
 
 }  // namespace ap

@@ -136,6 +136,7 @@ __global__ void sel_push_kernel(ap_selector s, const T* __restrict__ rows, int64
     const T* row = rows + (int64_t)m * row_stride;
     const bool calibrate = (st.counter % s.calib_period) == 0;
     const bool masked = (mode == 1) && !calibrate && st.n_pushed > 0 && st.row_len > 0;
+    float mx = 0.f;  // max |x| of the row (forecaster operand scale)
     if (masked) {
         PrevSelection sel;
         sel.nl = st.row_len + 1;
@@ -144,14 +145,23 @@ __global__ void sel_push_kernel(ap_selector s, const T* __restrict__ rows, int64
         sel.mid_clip = st.mid_clip;
         sel.b = b;
         sel.mask = s.mid_mask + (int64_t)m * ((s.w_max + 31) / 32);
-        for (int64_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = (float)block_max(row, t, b, j, sel);
+        for (int64_t j = threadIdx.x; j < W; j += blockDim.x) {
+            const float v = (float)block_max(row, t, b, j, sel);
+            dst[j] = v;
+            mx = track_row_max(mx, v, s.status);
+        }
     } else {
-        for (int64_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = (float)block_max(row, t, b, j, TakeAll{});
+        for (int64_t j = threadIdx.x; j < W; j += blockDim.x) {
+            const float v = (float)block_max(row, t, b, j, TakeAll{});
+            dst[j] = v;
+            mx = track_row_max(mx, v, s.status);
+        }
     }
     const int old_w = s.slot_width[(int64_t)m * H + slot];
     for (int64_t j = W + threadIdx.x; j < old_w; j += blockDim.x) dst[j] = 0.f;  // keep the row zero beyond W
-    __syncthreads();
+    mx = cta_max_nonneg(mx);
     if (threadIdx.x == 0) {
+        s.slot_xmax[(int64_t)m * H + slot] = mx;
         s.slot_width[(int64_t)m * H + slot] = (int32_t)W;
         st.n_pushed += 1;
         st.row_len = t;
@@ -169,11 +179,17 @@ __global__ void sel_push_f32_b16_kernel(ap_selector s, const float* __restrict__
     const int slot = (int)(st.n_pushed % H);
     float* dst = s.ring + ((int64_t)m * H + slot) * s.w_max;
     const float* row = rows + (int64_t)m * row_stride;
-    for (int64_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = block_max16_f32(row, t, j);
+    float mx = 0.f;
+    for (int64_t j = threadIdx.x; j < W; j += blockDim.x) {
+        const float v = block_max16_f32(row, t, j);
+        dst[j] = v;
+        mx = track_row_max(mx, v, s.status);
+    }
     const int old_w = s.slot_width[(int64_t)m * H + slot];
     for (int64_t j = W + threadIdx.x; j < old_w; j += blockDim.x) dst[j] = 0.f;  // keep the row zero beyond W
-    __syncthreads();
+    mx = cta_max_nonneg(mx);
     if (threadIdx.x == 0) {
+        s.slot_xmax[(int64_t)m * H + slot] = mx;
         s.slot_width[(int64_t)m * H + slot] = (int32_t)W;
         st.n_pushed += 1;
         st.row_len = t;
@@ -191,11 +207,17 @@ __global__ void sel_push_compressed_kernel(ap_selector s, const float* __restric
     const int slot = (int)(st.n_pushed % H);
     float* dst = s.ring + ((int64_t)m * H + slot) * s.w_max;
     const float* src = comp + (int64_t)m * comp_stride;
-    for (int64_t j = threadIdx.x; j < W; j += blockDim.x) dst[j] = src[j];
+    float mx = 0.f;
+    for (int64_t j = threadIdx.x; j < W; j += blockDim.x) {
+        const float v = src[j];
+        dst[j] = v;
+        mx = track_row_max(mx, v, s.status);
+    }
     const int old_w = s.slot_width[(int64_t)m * H + slot];
     for (int64_t j = W + threadIdx.x; j < old_w; j += blockDim.x) dst[j] = 0.f;  // keep the row zero beyond W
-    __syncthreads();
+    mx = cta_max_nonneg(mx);
     if (threadIdx.x == 0) {
+        s.slot_xmax[(int64_t)m * H + slot] = mx;
         s.slot_width[(int64_t)m * H + slot] = (int32_t)W;
         st.n_pushed += 1;
         st.row_len = t;

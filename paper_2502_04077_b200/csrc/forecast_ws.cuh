@@ -5,9 +5,12 @@
 // One CTA (16 warps) per SM, persistent over (map, 128-column chunk) tasks; each
 // task is processed as bands of <= MAXO history rows.  Roles, connected by
 // mbarrier handshakes so no role ever waits on a CTA-wide barrier:
-//   warp 0      producer: plans the next bands (map state loaded one task ahead),
-//               fills the band metadata and starts cp.async.bulk copies of the
-//               band's history rows into a 3-stage x ring;
+//   warp 0      producer (whole warp): plans 32 tasks at a time (map state loads in
+//               parallel), publishes band metadata and starts lane-parallel
+//               cp.async.bulk copies of the band's history rows into an x ring; the
+//               fp16 operand scale comes from the per-slot row maxima the ring
+//               writers recorded (selector mode) or from a scan of the landed tile
+//               two bands behind (explicit grids);
 //   warp 1      MMA: per band, tcgen05.cp the dj-shifted a1 windows into the TMEM
 //               ring and issues the conv2 MMAs (A from TMEM) into one of two TMEM
 //               accumulator buffers; commits release the a1 tile and publish the
@@ -156,6 +159,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             __syncwarp();
             t_scan += clock64() - f0;
         };
+        const bool pre_xm = sel && P.slot_xmax && H <= 64;
         int b = 0;
         for (int task0 = blockIdx.x;; task0 += 32 * G) {
             long long tp0 = clock64();
@@ -169,10 +173,24 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             const int base_slot = sel ? slot_of(row_index(T.n_pushed, H, 0), H) : 0;
             const int first_real = (!sel || T.n_pushed >= H) ? 0 : (int)(H - T.n_pushed);
             unsigned todo = __ballot_sync(0xffffffffu, live);
+            // Row maxima of a task's map (H <= 64: lane l holds slots l and l + 32), loaded one task
+            // ahead so no band waits on global memory for its operand scale.
+            auto load_xm = [&](int mp, float& va, float& vb) {
+                const float* src = P.slot_xmax + (int64_t)mp * H;
+                va = lane < H ? src[lane] : 0.f;
+                vb = lane + 32 < H ? src[lane + 32] : 0.f;
+            };
+            float ca = 0.f, cb = 0.f;
+            if (pre_xm && todo) load_xm(__shfl_sync(0xffffffffu, map, __ffs(todo) - 1), ca, cb);
             t_plan += clock64() - tp0;
             while (todo) {
                 const int l = __ffs(todo) - 1;
                 todo &= todo - 1;
+                float na = 0.f, nb_ = 0.f;
+                {
+                    const int nmap = __shfl_sync(0xffffffffu, map, todo ? __ffs(todo) - 1 : 0);
+                    if (pre_xm && todo) load_xm(nmap, na, nb_);
+                }
                 const int q_map = __shfl_sync(0xffffffffu, map, l), q_chunk = __shfl_sync(0xffffffffu, chunk, l);
                 const int q_W = __shfl_sync(0xffffffffu, T.W, l), q_full = __shfl_sync(0xffffffffu, (int)T.full, l);
                 const int q_lo2 = __shfl_sync(0xffffffffu, T.lo2, l);
@@ -184,6 +202,9 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
                 const int w0 = q_chunk * TW;
                 const int c_lo = max(0, w0 - 4), c_hi = min(P.pitch, w0 + TW + 4);
                 const float* ring = P.ring + (int64_t)q_map * P.map_stride;
+                int pa = lane - q_base, pb = lane + 32 - q_base;  // history positions of slots lane, lane + 32
+                pa += pa < 0 ? H : 0;
+                pb += pb < 0 ? H : 0;
                 for (int bi = 0; bi < nb; ++bi, ++b) {
                     const int s = b % NX;
                     long long t0 = clock64();
@@ -203,6 +224,19 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
                                                                                        : q_base + o0 + lane)
                                                             : o0 + lane;
                     const unsigned nrows = __popc(__ballot_sync(0xffffffffu, xrow));
+                    if (P.slot_xmax) {  // operand scale from the rows' maxima recorded when they were written
+                        float xm;
+                        if (pre_xm) {
+                            const int plo = max(max(o0 - 2, q_fr), 0), phi = min(o0 + n_out + 2, H);
+                            xm = (lane < H && pa >= plo && pa < phi) ? ca : 0.f;
+                            if (lane + 32 < H && pb >= plo && pb < phi) xm = fmaxf(xm, cb);
+                        } else {
+                            xm = xrow ? P.slot_xmax[(int64_t)q_map * H + slot] : 0.f;
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) xm = fmaxf(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+                        if (lane == 0) m.aexp = f16_scale_exp(fmaf(w1max, xm, b1max));
+                    }
                     if (lane == 0) {
                         m.valid = 1; m.map = q_map; m.chunk = q_chunk; m.W = q_W;
                         m.first = bi == 0; m.last = bi == nb - 1;
@@ -216,18 +250,21 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
                                  ring + (int64_t)slot * P.pitch + c_lo, (uint32_t)(c_hi - c_lo) * 4, &x_full[s]);
                     t_wait += t1 - t0;
                     t_plan += clock64() - t1;
-                    if (b >= SCAN_LAG) finalize(b - SCAN_LAG);
+                    if (!P.slot_xmax && b >= SCAN_LAG) finalize(b - SCAN_LAG);
                 }
+                ca = na;
+                cb = nb_;
             }
             if (task0 + 32 * G >= n_tasks) break;
         }
-        for (int j = max(0, b - SCAN_LAG); j < b; ++j) finalize(j);
+        if (!P.slot_xmax)
+            for (int j = max(0, b - SCAN_LAG); j < b; ++j) finalize(j);
         {  // end of work: an invalid band tells the consumers to stop
             const int s = b % NX;
             if (b >= NX) mbar_wait(&x_empty[s], ((b / NX) & 1) ^ 1);
             if (lane == 0) {
                 meta[s].valid = 0;
-                mbar_arrive(&x_ready[s]);
+                mbar_arrive(P.slot_xmax ? &x_full[s] : &x_ready[s]);
             }
         }
         if ((dbg & 8) && lane == 0) {
@@ -312,7 +349,12 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
         __syncwarp();
         if (lane == 0)
             for (int a = 0; a < NA; ++a) mbar_arrive(&acc_empty[a]);
-        double S = 0.0;  // running sum of this column: the map's stored value, or rebuilt by a full task
+        // Running sum of this column: the stored value (incremental task) or 0 (full task), plus the
+        // new r of every recomputed slot, minus the values those slots held.  The old values are
+        // loaded at the task's first band (before any of its stores) and subtracted at its last.
+        constexpr int NOLD = 8;
+        double S = 0.0, Snew = 0.0;
+        float oldv[NOLD];
         unsigned long long e_wait = 0, e_work = 0, e_math = 0;
         long long e_t = clock64();
         for (int b = 0;; ++b) {
@@ -336,39 +378,71 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             const bool live = col < W;
             float* rmap = P.rmap + (int64_t)I.map * P.map_stride + col;
             const int64_t at = (int64_t)I.map * P.pitch + col;
-            if (I.first) S = (I.full || !P.rsum || !live) ? 0.0 : P.rsum[at];
-            // values the rewritten slots held (incremental tasks): loads land during the TMEM reads
-            float old[MAXO];
+            if (I.first) {
+                S = (I.full || !P.rsum || !live) ? 0.0 : P.rsum[at];  // first used at the last band
+                Snew = 0.0;
+                const int n_old = (I.full || !live) ? 0 : 2 + H - I.lo2;  // positions {0, 1} ∪ [lo2, H)
+                auto slot_at = [&](int k) {
+                    const int p = k < 2 ? k : I.lo2 + k - 2;
+                    const int sl = sel ? I.base_slot + p : p;
+                    return sl >= H ? sl - H : sl;
+                };
 #pragma unroll
-            for (int j = 0; j < MAXO; ++j)
-                old[j] = (!I.full && live && j < I.n_out) ? rmap[(int64_t)I.out_slot[j] * P.pitch] : 0.f;
+                for (int k = 0; k < NOLD; ++k) oldv[k] = k < n_old ? rmap[(int64_t)slot_at(k) * P.pitch] : 0.f;
+                for (int k = NOLD; k < n_old; ++k) Snew -= (double)rmap[(int64_t)slot_at(k) * P.pitch];  // > NOLD - 4 new rows
+            }
             long long q0 = clock64();
             if (!(dbg & 4)) {
                 const int e = I.aexp + wexp;
                 const bool one_mul = e >= -126 && e <= 126;
                 const float u = one_mul ? pow2f(-e) : pow2f(-I.aexp), u2 = one_mul ? 1.f : pow2f(-wexp);
+                // 16-column pieces (row j = c / 2, channels 16 (c % 2) ..) ping-pong between two register
+                // sets: piece c+1's TMEM load overlaps piece c's math
+                const int n_pc = 2 * I.n_out;
+                const uint32_t t0 = lane_base + a * ACC_COLS + 2 * 32;
+                uint32_t ra[16], rb[16];
+                tmem_ld16_start(t0, ra);
+                tmem_ld_wait(ra);
+                float r0 = 0.f, r1 = 0.f, bsum = 0.f;  // bsum: this band's new r (one fp64 add per band)
 #pragma unroll
-                for (int j = 0; j < MAXO; ++j) {
-                    if (j >= I.n_out) break;
-                    float acc[32];
-                    tmem_ld32(lane_base + a * ACC_COLS + (j + 2) * 32, acc);
-                    float r = 0.f;
+                for (int c = 0; c < 2 * MAXO; ++c) {
+                    if (c >= n_pc) break;
+                    uint32_t (&cur)[16] = (c & 1) ? rb : ra;
+                    uint32_t (&nxt)[16] = (c & 1) ? ra : rb;
+                    if (c + 1 < n_pc) tmem_ld16_start(t0 + (c + 1) * 16, nxt);
+                    if (!one_mul) {  // scale too extreme for one multiply (never for attention rows)
 #pragma unroll
-                    for (int n = 0; n < 32; ++n) {
-                        const float s2 = fmaf(acc[n] * u2, u, c_w[OFF_B2 + n]);
-                        r = fmaf(c_w[OFF_W3 + n], fmaxf(s2, 0.f), r);
+                        for (int n = 0; n < 16; ++n) cur[n] = __float_as_uint(__uint_as_float(cur[n]) * u2);
                     }
-                    if (live) {
-                        rmap[(int64_t)I.out_slot[j] * P.pitch] = r;
-                        S += (double)r - (double)old[j];
+                    // r += sum_c w3[c] relu(acc[c] * u + b2[c]), channel pairs on the packed FMA pipe
+                    const int ch0 = (c & 1) * 16;
+#pragma unroll
+                    for (int n = 0; n < 16; n += 2) {
+                        float s0 = c_w[OFF_B2 + ch0 + n], s1 = c_w[OFF_B2 + ch0 + n + 1];
+                        ffma2(s0, s1, __uint_as_float(cur[n]), __uint_as_float(cur[n + 1]), u);
+                        ffma2v(r0, r1, fmaxf(s0, 0.f), fmaxf(s1, 0.f), c_w[OFF_W3 + ch0 + n], c_w[OFF_W3 + ch0 + n + 1]);
                     }
+                    if (c & 1) {  // row complete
+                        const float r = r0 + r1;
+                        if (live) {
+                            rmap[(int64_t)I.out_slot[c >> 1] * P.pitch] = r;
+                            bsum += r;
+                        }
+                        r0 = r1 = 0.f;
+                    }
+                    if (c + 1 < n_pc) tmem_ld_wait(nxt);
                 }
+                Snew += (double)bsum;
             }
             e_math += clock64() - q0;
             tc_fence_before();  // our tcgen05.ld reads of buffer a are complete before it is reused
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[a]);
             if (I.last && live) {
+                float osum = 0.f;
+#pragma unroll
+                for (int k = 0; k < NOLD; ++k) osum += oldv[k];
+                S += Snew - (double)osum;
                 if (P.rsum) P.rsum[at] = S;
                 P.scores[(int64_t)I.map * P.score_stride + col] = c_w[OFF_B3] + (float)S / (float)H;
             }
@@ -382,7 +456,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             const int s = b % NX;
             long long c0 = clock64();
             c_work += c0 - c_t;
-            mbar_wait(&x_ready[s], (b / NX) & 1);
+            mbar_wait(P.slot_xmax ? &x_full[s] : &x_ready[s], (b / NX) & 1);  // tile landed / scanned
             c_t = clock64();
             c_wx += c_t - c0;
             const BandMeta& m = meta[s];
@@ -409,44 +483,56 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             c_wa += cb - ca;
             c_work -= cb - ca;
             uint8_t* a1t = smem + L::off_a1 + a * L::kA1;
-            for (int i = ct; i < ((dbg & 1) ? 0 : n_a1 * A1C); i += NCONV_T) {
-                const int ar = i / A1C, ac = i - ar * A1C;
-                const int p = m.o0 - 1 + ar, c = w0 - 1 + ac;
-                if (!(p >= 0 && p < H && c >= 0 && c < W)) {  // zero padding of the conv2 input
-                    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-                    *reinterpret_cast<uint4*>(a1t + 0 * PLANE + i * 16) = z;
-                    *reinterpret_cast<uint4*>(a1t + 1 * PLANE + i * 16) = z;
-                    if constexpr (PREC == AP_PREC_F16X3) {
-                        *reinterpret_cast<uint4*>(a1t + 2 * PLANE + i * 16) = z;
-                        *reinterpret_cast<uint4*>(a1t + 3 * PLANE + i * 16) = z;
-                    }
-                    continue;
-                }
-                float x9[9];
+            // Two adjacent a1 pixels per thread (packed FFMA2, shared x window).  Only rows inside the
+            // history are computed: conv2's zero-padding rows (position < 0 or >= H) are never read.
+            const int ar_lo = max(0, 1 - m.o0), ar_hi = min(n_a1, H + 1 - m.o0);
+            constexpr int PAIRS = A1C / 2;
+            for (int i = ct; i < ((dbg & 1) ? 0 : (ar_hi - ar_lo) * PAIRS); i += NCONV_T) {
+                const int rr = i / PAIRS, ar = ar_lo + rr, ac = 2 * (i - rr * PAIRS);
+                const int c = w0 - 1 + ac;  // pixel columns c, c + 1
+                float xw[3][4];
 #pragma unroll
                 for (int di = 0; di < 3; ++di) {
                     const int lim = m.x_lim[ar + di];
                     const float* xr = xs + (ar + di) * XC4 + ac + 2;
 #pragma unroll
-                    for (int dj = 0; dj < 3; ++dj)
-                        x9[di * 3 + dj] = ((unsigned)(c - 1 + dj) < (unsigned)lim) ? xr[dj] : 0.f;
+                    for (int e = 0; e < 4; ++e) xw[di][e] = ((unsigned)(c - 1 + e) < (unsigned)lim) ? xr[e] : 0.f;
                 }
+                // pixels outside [0, W) are conv2's zero padding: a zero scale clears them
+                const float sc0 = (unsigned)c < (unsigned)W ? ascale : 0.f;
+                const float sc1 = (unsigned)(c + 1) < (unsigned)W ? ascale : 0.f;
+                const int px = ar * A1C + ac;
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
-                    __align__(16) __half hi[8], lo[8];
+                    float v0[8], v1[8];  // scaled relu(a1) of pixels c, c+1, channels 8g ..
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const int ch = g * 8 + q;
-                        float acc = c_w[OFF_B1 + ch];
+                        float s0 = c_w[OFF_B1 + ch], s1 = s0;
 #pragma unroll
-                        for (int k = 0; k < 9; ++k) acc = fmaf(c_w[OFF_W1 + ch * 9 + k], x9[k], acc);
-                        const float as = fmaxf(acc, 0.f) * ascale;
-                        hi[q] = __float2half_rn(as);
-                        lo[q] = __float2half_rn(as - __half2float(hi[q]));
+                        for (int k = 0; k < 9; ++k)
+                            ffma2(s0, s1, xw[k / 3][k % 3], xw[k / 3][k % 3 + 1], c_w[OFF_W1 + ch * 9 + k]);
+                        v0[q] = fmaxf(s0 * sc0, 0.f);  // relu(s) * 2^aexp (scale > 0, exact)
+                        v1[q] = fmaxf(s1 * sc1, 0.f);
                     }
-                    *reinterpret_cast<uint4*>(a1t + g * PLANE + i * 16) = *reinterpret_cast<uint4*>(hi);
-                    if constexpr (PREC == AP_PREC_F16X3)
-                        *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE + i * 16) = *reinterpret_cast<uint4*>(lo);
+                    uint4 h0, l0, h1, l1;
+                    if constexpr (PREC == AP_PREC_F16X3) {
+                        split_f16x2(v0[0], v0[1], h0.x, l0.x); split_f16x2(v0[2], v0[3], h0.y, l0.y);
+                        split_f16x2(v0[4], v0[5], h0.z, l0.z); split_f16x2(v0[6], v0[7], h0.w, l0.w);
+                        split_f16x2(v1[0], v1[1], h1.x, l1.x); split_f16x2(v1[2], v1[3], h1.y, l1.y);
+                        split_f16x2(v1[4], v1[5], h1.z, l1.z); split_f16x2(v1[6], v1[7], h1.w, l1.w);
+                    } else {  // single fp16 operand: round to nearest
+                        h0 = make_uint4(pack_f16x2(v0[0], v0[1]), pack_f16x2(v0[2], v0[3]), pack_f16x2(v0[4], v0[5]),
+                                        pack_f16x2(v0[6], v0[7]));
+                        h1 = make_uint4(pack_f16x2(v1[0], v1[1]), pack_f16x2(v1[2], v1[3]), pack_f16x2(v1[4], v1[5]),
+                                        pack_f16x2(v1[6], v1[7]));
+                    }
+                    *reinterpret_cast<uint4*>(a1t + g * PLANE + px * 16) = h0;
+                    *reinterpret_cast<uint4*>(a1t + g * PLANE + px * 16 + 16) = h1;
+                    if constexpr (PREC == AP_PREC_F16X3) {
+                        *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE + px * 16) = l0;
+                        *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE + px * 16 + 16) = l1;
+                    }
                 }
             }
             if (ct == 0) {

@@ -126,6 +126,7 @@ struct ConvParams {
     double* rsum;           // rsum + map*pitch + col: running sum over the H ring slots of r (selector
                             // mode; invariant rsum == sum_slot rmap[slot]); null => explicit grids
     const int32_t* slot_width;  // [map][H] (selector mode)
+    const float* slot_xmax;     // [map][H] max |x| per ring row (selector mode; null => scan the tiles)
     const ap_map_state* state;  // [map]    (selector mode); null => explicit grids
     int32_t n_maps, H, W_explicit, n_chunks, update_interval, k_mid;
     int32_t* status;
@@ -765,6 +766,7 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream) {
         P.scores = s->scores;
         P.score_stride = s->w_max;
         P.slot_width = s->slot_width;
+        P.slot_xmax = s->slot_xmax;
         P.state = s->state;
         P.n_maps = s->n_maps;
         P.H = s->history;
