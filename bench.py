@@ -147,6 +147,14 @@ def measured_peak():
         return HBM_FALLBACK, "fallback"
 
 
+def measured_tensor_peak():
+    """Sustained dense bf16 TFLOP/s (the selector runs inside a long decode step)."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops_sustained"])
+    except Exception:
+        return 1590.0  # B200_PROFILING.md fallback
+
+
 def profiled_traffic():
     p = ROOT / "profiles" / "roofline_traffic.json"
     try:
@@ -268,11 +276,20 @@ def roofline_for(eng, args, us, W, key):
     b_alg = n_maps * ((H + 1) * W * 4 + 4 * K)  # history window + new row + block ids, per launch
     peak, peak_kind = measured_peak()
     achieved = b_alg / (us * 1e-6) / 1e9
+    # tensor work of the executed incremental form, F_inc = maps * W * (5*9216 + 7*288)
+    # (one new history row per step: rows {0,1} and [H-3, H) of conv2, 7 rows of conv1), against the
+    # measured dense bf16 peak; the fp16x3 split issues each conv2 product three times.
+    f_inc = n_maps * W * (5 * 9216 + 7 * 288)
+    tf_peak = measured_tensor_peak()
+    tflops = f_inc / (us * 1e-6) / 1e12
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": profiled_traffic().get(key), "peak_kind": peak_kind,
-            "kernel": "ap_sel_step (conv_forecast_kernel + sel_topk_kernel)", "maps": n_maps,
+            "kernel": "ap_sel_step (conv_forecast_ws_kernel + sel_topk_kernel)", "maps": n_maps,
             "us_per_launch": round(us, 2), "us_per_layer": round(us / eng.shape.n_layers, 3),
-            "algorithmic_bytes_per_launch": b_alg}
+            "algorithmic_bytes_per_launch": b_alg,
+            "tensor": {"algorithmic_flops_per_launch": f_inc, "achieved": round(tflops, 1), "peak": tf_peak,
+                       "unit": "TFLOP/s", "frac": round(tflops / tf_peak, 4),
+                       "issued_frac_fp16x3": round(3 * tflops / tf_peak, 4) if args.precision == "fp16x3" else None}}
 
 
 def run_ours(args, rank, world):
