@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--offload", action="store_true",
                     help="cfg4: V in pinned host memory + cross-token prefetch of the predicted blocks")
     ap.add_argument("--cpu-sample", type=int, default=48, help="oracle map-steps timed for cpu_baseline")
+    ap.add_argument("--dense-layers", type=int, default=0,
+                    help="layer-skip policy: the first N layers always run full attention (the paper uses 2)")
     return ap.parse_args()
 
 
@@ -312,7 +314,7 @@ def run_ours(args, rank, world):
         args.no_alt = True
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
                        precision=args.precision, seed=rank if split is None else 0, offload_v=args.offload,
-                       head_split=split)
+                       head_split=split, dense_layers=args.dense_layers)
     units = world if split is None else 1  # replicas: every rank decodes its own sequences
     eng.init_history()
     first_token(eng)
@@ -381,7 +383,7 @@ def run_ours(args, rank, world):
                    "model_shape": shape.name, "ctx": args.ctx, "budget": args.budget, "block": 16, "history": 64,
                    "calibration_period": 5, "batch_per_gpu": args.batch,
                    "selection": {"kv": f"per KV head ({G} q-heads share a map)", "head": "per q-head"}[args.group],
-                   "forecaster_precision": args.precision,
+                   "forecaster_precision": args.precision, "dense_layers": args.dense_layers,
                    "parallelism": f"replicas x{world}" if split is None else f"kv-head split x{world} + all-gather",
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},

@@ -66,11 +66,14 @@ class DecodeEngine:
     reference's per-head semantics), n_q_heads/n_kv_heads = one per KV head (GQA
     group: compressed rows are max-pooled over the group's heads, and the whole
     group shares one gathered block set).
+    dense_layers: layer-skip policy (the paper keeps the first 2 layers
+    dense) — layers [0, dense_layers) always run full attention and own no
+    selector maps.
     """
 
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
-                 seed: int = 0, offload_v: bool = False, head_split=None):
+                 seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -85,6 +88,12 @@ class DecodeEngine:
         G = shape.n_q_heads // shape.n_kv_heads
         if G % group:
             raise ConfigError("group must divide the GQA group size")
+        if not 0 <= dense_layers < shape.n_layers:
+            raise ConfigError("dense_layers must be in [0, n_layers)")
+        if dense_layers and offload_v:
+            raise ConfigError("dense layers need their V resident: not combinable with V offload")
+        self.dense_layers = dense_layers
+        self.sel_layers = shape.n_layers - dense_layers  # layers that own selector maps
         self.t_max = -(-(ctx_len + max_new + 1) // 1024) * 1024
         self.ctx_len = ctx_len
         dev = D.device()
@@ -128,6 +137,7 @@ class DecodeEngine:
         self.act = torch.zeros(S, F, dtype=bf, device=dev)
         self.mlp = torch.zeros(S, Hd, dtype=bf, device=dev)
         self.tok = torch.zeros(S, dtype=torch.int64, device=dev)
+        self.logits = torch.zeros(S, V, dtype=bf, device=dev)
         self.seq_len = torch.full((S,), ctx_len, dtype=torch.int32, device=dev)
         self.att = DecodeAttention(S, Hq, Hkv, self.t_max, n_splits_dense=min(64, self.t_max // 1024),
                                    n_splits_sparse=8, device=dev)
@@ -137,8 +147,8 @@ class DecodeEngine:
         self.cfg = cfg or SelectorConfig(budget=1024)
         if mode == "sparse":
             install_weights(weights or init_weights(0))
-            self.sel = BatchedSelector(self.cfg, S * L * self.maps_per_layer, self.t_max // 16, precision=precision,
-                                       device=dev)
+            self.sel = BatchedSelector(self.cfg, S * self.sel_layers * self.maps_per_layer, self.t_max // 16,
+                                       precision=precision, device=dev)
         self.voff = None
         if offload_v:
             if mode != "sparse" or group != G:
@@ -186,11 +196,15 @@ class DecodeEngine:
             pos = self.ctx_len - (H - 1) + i  # prompt position; its attention row covers keys [0, pos]
             lens.fill_(pos + 1)
             q.normal_(generator=gen)
-            for l in range(L):
+            for l in range(self.dense_layers, L):
                 self.att.dense(q, self.k_cache[l], self.k_cache[l], lens, None, with_v=False, emit=True,
-                               selector=self.sel, map_base=l * self.maps_per_layer,
-                               maps_per_seq=L * self.maps_per_layer, group=self.group)
+                               selector=self.sel, **self._map_kw(l))
         torch.cuda.synchronize()
+
+    def _map_kw(self, l: int) -> dict:
+        """Selector map range of layer l (layers below dense_layers own none)."""
+        return dict(map_base=(l - self.dense_layers) * self.maps_per_layer,
+                    maps_per_seq=self.sel_layers * self.maps_per_layer, group=self.group)
 
     # ---------------------------------------------------------------- one step
     def _layer(self, l: int, variant: str):
@@ -216,8 +230,9 @@ class DecodeEngine:
             self.voff.append(self.qkv, sh.n_q_heads, self.seq_len, l)
             if variant in ("plain", "calib"):  # this layer's predicted V blocks must have arrived
                 torch.cuda.current_stream().wait_event(self.pf_events[l])
-        kw = dict(map_base=l * self.maps_per_layer, maps_per_seq=sh.n_layers * self.maps_per_layer,
-                  group=self.group)
+        if l < self.dense_layers:
+            variant = "dense"  # layer-skip policy
+        kw = self._map_kw(l) if variant != "dense" else {}
         if variant == "dense":
             self.att.dense(self.q, kc, vc, self.seq_len, self.att_out, with_v=True)
         elif variant == "first":
@@ -256,7 +271,7 @@ class DecodeEngine:
             self.pf_stream.wait_stream(main)
             with torch.cuda.stream(self.pf_stream):
                 for l in range(sh.n_layers):
-                    self.voff.prefetch(self.sel, l, sh.n_layers * self.maps_per_layer, stream=self.pf_stream)
+                    self.voff.prefetch(self.sel, l, self.sel_layers * self.maps_per_layer, stream=self.pf_stream)
                     self.pf_events[l].record(self.pf_stream)
         torch.index_select(self.embed, 0, self.tok, out=self.r)
         for l in range(sh.n_layers):
@@ -265,8 +280,8 @@ class DecodeEngine:
             main.wait_stream(self.pf_stream)
         _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.lnf), _lib.ptr(self.y),
                                          S, sh.hidden, sh.eps, s))
-        logits = torch.matmul(self.y, self.lm_head.t())
-        torch.argmax(logits, dim=-1, out=self.tok)
+        torch.matmul(self.y, self.lm_head.t(), out=self.logits)
+        torch.argmax(self.logits, dim=-1, out=self.tok)
         if self.sel is not None and variant != "dense":
             self.sel.step()  # forecast + top-k for the next token, every layer and head at once
 
@@ -349,7 +364,7 @@ class DecodeEngine:
         self.graphs.clear()
         self.group = group
         self.maps_per_layer = self.shape.n_q_heads // group
-        self.sel = BatchedSelector(self.cfg, self.n_seq * self.shape.n_layers * self.maps_per_layer,
+        self.sel = BatchedSelector(self.cfg, self.n_seq * self.sel_layers * self.maps_per_layer,
                                    self.t_max // 16, precision=prec, device=self.dev)
         self.mode = "sparse"
         self.counter = 0
@@ -374,8 +389,9 @@ class DecodeEngine:
         L = self.shape.n_layers
         per_layer = 2 + 1 + 1  # rmsnorm x2, rope_append, silu_mul
         att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
+        att_total = self.dense_layers + (L - self.dense_layers) * att
         sel = 2 if (self.sel is not None and variant != "dense") else 0
         off = 0
         if self.voff is not None:
             off = L * (1 + (1 if variant in ("plain", "calib") else 0))  # v_append (+ prefetch) per layer
-        return 1 + L * (per_layer + att) + 1 + sel + off  # advance + layers + final norm + selector
+        return 1 + L * per_layer + att_total + 1 + sel + off  # advance + layers + final norm + selector
