@@ -37,6 +37,10 @@ extern "C" {
 #define AP_ESTATE    3  /* StateError     */
 #define AP_ENUMERIC  4  /* NumericError   */
 #define AP_ECUDA     5  /* DeviceError    */
+#define AP_EFORMAT   6  /* FormatError     (trace container: magic / version / short header) */
+#define AP_ECORRUPT  7  /* CorruptionError (trace container: truncation, length prefix, trailing bytes) */
+#define AP_EVALID    8  /* ValidationError (trace header fields, row invariants) */
+#define AP_EIO       9  /* OSError         (open / read / write failures) */
 
 /* element types */
 #define AP_F32   0
@@ -244,6 +248,60 @@ int ap_v_pages_init(const ap_vpages* vp, int64_t t, int64_t n_vmaps, void* strea
 /* ap_attn_sparse with V read from the paged store of `layer` (offload mode). */
 int ap_attn_sparse_paged(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
                          int32_t group, int emit, const ap_vpages* vp, int32_t layer, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * .att1 attention-trace container (reference: trace.py:9-25 layout,
+ * TraceHeader.validate 55-72, AttentionTrace.validate 112-168, write_trace
+ * 182-212, read_trace 215-291).  Host code: the reader memory-maps a file (or
+ * borrows a caller buffer) and addresses any (layer, head, step) row by offset,
+ * so golden traces stream straight into device staging buffers for replay; the
+ * writer streams rows in file order and produces byte-identical output.
+ * Error messages name the location the way the reference does.
+ * ------------------------------------------------------------------------- */
+typedef struct ap_trace_header {
+    int32_t num_layers, num_heads, prefill_len, num_decode_steps;
+    int32_t has_qk, head_dim, first_step_offset, pad_;
+} ap_trace_header;
+typedef struct ap_trace ap_trace;                /* opaque reader */
+typedef struct ap_trace_writer ap_trace_writer;  /* opaque writer */
+
+/* TraceHeader.validate (trace.py:55-72): AP_EVALID on a field violation. */
+int ap_trace_check_header(const ap_trace_header* h);
+/* Row invariants of AttentionTrace.validate (trace.py:138-150): finite, >= 0, float64 sum within
+ * 1e-4 of 1; AP_EVALID naming (layer, head, step). */
+int ap_trace_check_row(const float* row, int64_t len, int32_t layer, int32_t head, int32_t step);
+/* Total container bytes the header declares (header + rows + q/k blocks). */
+int64_t ap_trace_nbytes(const ap_trace_header* h);
+/* Open a reader over a file (memory-mapped) or over caller bytes (borrowed; keep them alive).
+ * Parses the header (AP_EFORMAT: short header, bad magic, bad version; AP_EVALID: fields). */
+int ap_trace_open(const char* path, ap_trace** out);
+int ap_trace_open_memory(const void* data, int64_t nbytes, ap_trace** out);
+void ap_trace_close(ap_trace* t);
+int ap_trace_get_header(const ap_trace* t, ap_trace_header* out);
+/* Everything read_trace + validate check: every length prefix, truncation (AP_ECORRUPT naming
+ * the row), trailing bytes, and per-row invariants (finite, >= 0, sums to 1 within 1e-4:
+ * AP_EVALID).  Rows are addressed by offset, so the other readers do not need this first. */
+int ap_trace_validate(const ap_trace* t);
+/* Rows of (layer, head) for steps [step_lo, step_hi): step s -> dst + (s - step_lo) * dst_stride
+ * floats, zero-filled up to pad_to floats (pad_to <= dst_stride; 0 = no padding). */
+int ap_trace_read_rows(const ap_trace* t, int32_t layer, int32_t head, int32_t step_lo, int32_t step_hi,
+                       float* dst, int64_t dst_stride, int64_t pad_to);
+/* Row of `step` for every (layer, head): map m = layer * num_heads + head -> dst + m * dst_stride,
+ * zero-filled up to pad_to floats (the staging layout of ap_sel_push_rows). */
+int ap_trace_gather_step(const ap_trace* t, int32_t step, float* dst, int64_t dst_stride, int64_t pad_to);
+/* q/k blocks of (layer, head) (has_qk): queries [rows_per_head][head_dim], keys [total_len][head_dim]. */
+int ap_trace_read_qk(const ap_trace* t, int32_t layer, int32_t head, float* queries, float* keys);
+
+/* Streaming writer: rows in file order (layer-major, head, step oldest first), then (has_qk) one
+ * q/k pair per (layer, head) in the same order.  path NULL = in-memory (ap_trace_writer_bytes).
+ * append_row validates the row (length AP_EVALID, invariants AP_EVALID naming the location). */
+int ap_trace_writer_open(const char* path, const ap_trace_header* h, ap_trace_writer** out);
+int ap_trace_writer_append_row(ap_trace_writer* w, const float* row, int64_t len);
+int ap_trace_writer_append_qk(ap_trace_writer* w, const float* queries, const float* keys);
+/* AP_EVALID if rows / q-k blocks are missing; *nbytes = bytes written. */
+int ap_trace_writer_finish(ap_trace_writer* w, int64_t* nbytes);
+int ap_trace_writer_bytes(const ap_trace_writer* w, const void** data, int64_t* nbytes);
+void ap_trace_writer_free(ap_trace_writer* w);
 
 /* ---------------------------------------------------------------------------
  * Decode-engine helpers around the path (not reference functions: the

@@ -16,7 +16,7 @@ from . import errors as E
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libattnpred.so"
 
-AP_OK, AP_EPARAM, AP_ECONFIG, AP_ESTATE, AP_ENUMERIC, AP_ECUDA = range(6)
+AP_OK, AP_EPARAM, AP_ECONFIG, AP_ESTATE, AP_ENUMERIC, AP_ECUDA, AP_EFORMAT, AP_ECORRUPT, AP_EVALID, AP_EIO = range(10)
 AP_F32, AP_F64, AP_BF16 = 0, 1, 2
 PREC = {"fp32": 0, "fp16x3": 1, "fp16": 2}
 
@@ -26,6 +26,10 @@ _ERR = {
     AP_ESTATE: E.StateError,
     AP_ENUMERIC: E.NumericError,
     AP_ECUDA: E.DeviceError,
+    AP_EFORMAT: E.FormatError,
+    AP_ECORRUPT: E.CorruptionError,
+    AP_EVALID: E.ValidationError,
+    AP_EIO: OSError,
 }
 
 
@@ -81,6 +85,13 @@ class VPages(ctypes.Structure):
 
 MAP_STATE_BYTES = ctypes.sizeof(MapState)  # 56
 
+
+class TraceHeaderC(ctypes.Structure):
+    """ap_trace_header (include/attnpred.h)."""
+
+    _fields_ = [(n, ctypes.c_int32) for n in ("num_layers", "num_heads", "prefill_len", "num_decode_steps",
+                                               "has_qk", "head_dim", "first_step_offset", "pad_")]
+
 _P = ctypes.c_void_p
 _I32, _I64 = ctypes.c_int32, ctypes.c_int64
 
@@ -112,6 +123,24 @@ SIGNATURES = {
     "ap_rope_append": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _I32, ctypes.c_float, _P]),
     "ap_silu_mul": (ctypes.c_int, [_P, _P, _I32, _I32, _P]),
     "ap_advance": (ctypes.c_int, [_P, _I32, _I32, _P]),
+    # .att1 trace container (host code)
+    "ap_trace_check_header": (ctypes.c_int, [ctypes.POINTER(TraceHeaderC)]),
+    "ap_trace_check_row": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32]),
+    "ap_trace_nbytes": (_I64, [ctypes.POINTER(TraceHeaderC)]),
+    "ap_trace_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(_P)]),
+    "ap_trace_open_memory": (ctypes.c_int, [_P, _I64, ctypes.POINTER(_P)]),
+    "ap_trace_close": (None, [_P]),
+    "ap_trace_get_header": (ctypes.c_int, [_P, ctypes.POINTER(TraceHeaderC)]),
+    "ap_trace_validate": (ctypes.c_int, [_P]),
+    "ap_trace_read_rows": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I64, _I64]),
+    "ap_trace_gather_step": (ctypes.c_int, [_P, _I32, _P, _I64, _I64]),
+    "ap_trace_read_qk": (ctypes.c_int, [_P, _I32, _I32, _P, _P]),
+    "ap_trace_writer_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(TraceHeaderC), ctypes.POINTER(_P)]),
+    "ap_trace_writer_append_row": (ctypes.c_int, [_P, _P, _I64]),
+    "ap_trace_writer_append_qk": (ctypes.c_int, [_P, _P, _P]),
+    "ap_trace_writer_finish": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
+    "ap_trace_writer_bytes": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
+    "ap_trace_writer_free": (None, [_P]),
 }
 
 _lib = None

@@ -35,7 +35,7 @@ def nvcc() -> str:
 
 
 def sources() -> list[Path]:
-    return sorted(CSRC.glob("*.cu"))
+    return sorted([*CSRC.glob("*.cu"), *CSRC.glob("*.cpp")])  # .cpp: host-only translation units
 
 
 def up_to_date() -> bool:

@@ -215,6 +215,47 @@ def gen_loops():
         np.savez_compressed(OUT / f"loop_{name}.npz", **store)
 
 
+def gen_trace_fixture():
+    """trace_tiny.att1: the reference's tiny_trace fixture shape (pkg/tests/conftest.py:72-87, q/k
+    included) written by attncast.trace.write_trace (trace.py:182-212); trace_tiny.npz: the rows and
+    q/k blocks as attncast.trace.read_trace decodes them, plus the predictor branch's middle blocks
+    (evaluation.py:90-115) per (layer, head, step) for a device replay through the C++ reader."""
+    from attncast import trace as T
+    tr = gen_trace(SynthConfig(head_dim=16, prefill_len=96, decode_steps=30, query_drift=0.2, key_drift=0.2,
+                               seasonal_period=5, reaccess_positions=frozenset({7, 40}), rng_seed=5, num_layers=2,
+                               num_heads=2), keep_prefill_rows=8)
+    path = OUT / "trace_tiny.att1"
+    with open(path, "wb") as fh:
+        T.write_trace(tr, fh)
+    with open(path, "rb") as fh:
+        back = T.read_trace(fh)
+    assert back == tr
+    h = back.header
+    store = {"header": np.array([h.num_layers, h.num_heads, h.prefill_len, h.num_decode_steps, int(h.has_qk),
+                                 h.head_dim, h.first_step_offset])}
+    cfg = selector.SelectorConfig(budget=96, block_size=16, history=8, calibration_period=5, sink_tokens=16,
+                                  local_tokens=16)
+    wt = predictor.init_weights(7)
+    store["weights"] = wt.flat()
+    store["cfg"] = np.array([cfg.budget, cfg.block_size, cfg.history, cfg.calibration_period, cfg.sink_tokens,
+                             cfg.local_tokens, cfg.update_interval])
+    for layer in range(h.num_layers):
+        for head in range(h.num_heads):
+            store[f"rows_{layer}_{head}"], store[f"rows_{layer}_{head}_off"] = ragged(
+                [back.row(layer, head, s) for s in h.steps], np.float32)
+            store[f"q_{layer}_{head}"] = back.queries[layer][head]
+            store[f"k_{layer}_{head}"] = back.head_keys(layer, head)
+            sels, _ = run_loop(back, cfg, wt, layer, head)
+            mids = []
+            for t, sel in enumerate(sels):
+                nl = h.prefill_len + t + 1  # selection for the row of length prefill + t + 1
+                sink = set(range(min(cfg.sink_tokens, nl)))
+                local = set(range(max(0, nl - cfg.local_tokens), nl))
+                mids.append(sorted({i // cfg.block_size for i in set(sel) - sink - local}))
+            store[f"mid_{layer}_{head}"], store[f"mid_{layer}_{head}_off"] = ragged(mids, np.int64)
+    np.savez_compressed(OUT / "trace_tiny.npz", **store)
+
+
 def main():
     import tempfile
     rng = np.random.default_rng(20250204)
@@ -225,6 +266,7 @@ def main():
     with tempfile.TemporaryDirectory() as d:
         gen_weights(Path(d))
     gen_loops()
+    gen_trace_fixture()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
 
