@@ -53,6 +53,8 @@ class ModelShape:
         return 2 * 2 * self.n_layers * self.n_kv_heads * self.head_dim
 
 
+GEMV_RMS, GEMV_SILU, GEMV_ARGMAX = 1, 1 << 1, 2 << 1  # ap_gemv flags (include/attnpred.h)
+
 LLAMA31_8B = ModelShape("llama-3.1-8b", 32, 4096, 32, 8, 14336, 128256, 500000.0)
 LONGCHAT_7B_32K = ModelShape("longchat-7b-v1.5-32k", 32, 4096, 32, 32, 11008, 32000, 10000.0)
 SHAPES = {s.name: s for s in (LLAMA31_8B, LONGCHAT_7B_32K)}
@@ -69,11 +71,15 @@ class DecodeEngine:
     dense_layers: layer-skip policy (the paper keeps the first 2 layers
     dense) — layers [0, dense_layers) always run full attention and own no
     selector maps.
+    fused: batch <= 4 runs the projections through ap_gemv with the neighbouring elementwise ops
+    fused (RMSNorm prologues, SiLU-gate epilogue, LM head + greedy argmax); the down projection
+    stays a cuBLAS GEMM.  fused=False keeps one library GEMM + one elementwise kernel per op.
     """
 
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
-                 seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0):
+                 seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0,
+                 fused: bool = True):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -127,6 +133,9 @@ class DecodeEngine:
         # activations
         S = n_seq
         self.r = torch.zeros(S, Hd, dtype=bf, device=dev)
+        self.r2 = torch.zeros(S, Hd, dtype=bf, device=dev)  # fused path: residual stream ping-pong
+        self.fused = fused and S <= 4
+        self.argws = torch.zeros(48, dtype=torch.uint8, device=dev)  # ap_gemv ARGMAX workspace
         self.y = torch.zeros(S, Hd, dtype=bf, device=dev)
         self.qkv = torch.zeros(S, shape.qkv_dim, dtype=bf, device=dev)
         self.q = torch.zeros(S, Hq, 128, dtype=bf, device=dev)
@@ -213,13 +222,20 @@ class DecodeEngine:
         sh = self.shape
         S = self.n_seq
         s = _lib.stream_handle()
-        if l == 0:
-            _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.r), None, _lib.ptr(self.ln1[0]), _lib.ptr(self.y), S,
-                                             sh.hidden, sh.eps, s))
+        if self.fused:  # residual stream ping-pong: qkv reads r2 and writes r, gate/up the reverse
+            if l == 0:
+                self._gemv(self.wqkv[l], self.r, self.qkv, GEMV_RMS, ln=self.ln1[0])
+            else:
+                self._gemv(self.wqkv[l], self.mlp, self.qkv, GEMV_RMS, residual=self.r2, residual_out=self.r,
+                           ln=self.ln1[l])
         else:
-            _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.ln1[l]),
-                                             _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
-        torch.matmul(self.y, self.wqkv[l].t(), out=self.qkv)
+            if l == 0:
+                _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.r), None, _lib.ptr(self.ln1[0]), _lib.ptr(self.y), S,
+                                                 sh.hidden, sh.eps, s))
+            else:
+                _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.ln1[l]),
+                                                 _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
+            torch.matmul(self.y, self.wqkv[l].t(), out=self.qkv)
         kc = self.k_cache[l]
         vc = self.v_cache[l] if self.voff is None else self.voff.layer_view(l)
         _lib.check(_lib.fn("ap_rope_append")(_lib.ptr(self.qkv), S, sh.n_q_heads, sh.n_kv_heads,
@@ -251,12 +267,25 @@ class DecodeEngine:
                                 device=self.att_out.device)
             dist.all_gather_into_tensor(parts, self.att_out.contiguous())
             self.att_full.copy_(parts.permute(1, 0, 2, 3).reshape(S, -1, 128))
-        torch.matmul(self.att_full.view(S, -1), self.wo[l].t(), out=self.o)
-        _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.o), _lib.ptr(self.r), _lib.ptr(self.ln2[l]), _lib.ptr(self.y),
-                                         S, sh.hidden, sh.eps, s))
-        torch.matmul(self.y, self.wgu[l].t(), out=self.gu)
-        _lib.check(_lib.fn("ap_silu_mul")(_lib.ptr(self.gu), _lib.ptr(self.act), S, sh.ffn, s))
+        if self.fused:
+            self._gemv(self.wo[l], self.att_full.view(S, -1), self.o, 0)
+            self._gemv(self.wgu[l], self.o, self.act, GEMV_RMS | GEMV_SILU, residual=self.r, residual_out=self.r2,
+                       ln=self.ln2[l])
+        else:
+            torch.matmul(self.att_full.view(S, -1), self.wo[l].t(), out=self.o)
+            _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.o), _lib.ptr(self.r), _lib.ptr(self.ln2[l]),
+                                             _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
+            torch.matmul(self.y, self.wgu[l].t(), out=self.gu)
+            _lib.check(_lib.fn("ap_silu_mul")(_lib.ptr(self.gu), _lib.ptr(self.act), S, sh.ffn, s))
         torch.matmul(self.act, self.wdown[l].t(), out=self.mlp)
+
+    def _gemv(self, W, x, y, flags, residual=None, residual_out=None, ln=None, tokens=None):
+        """ap_gemv: y = W x for this step's sequences with the fused prologue / epilogue in flags."""
+        N, K = W.shape
+        _lib.check(_lib.fn("ap_gemv")(_lib.ptr(W), _lib.ptr(x), _lib.ptr(y), N, K, self.n_seq, 2, flags,
+                                      _lib.ptr(residual), _lib.ptr(residual_out), _lib.ptr(ln), self.shape.eps,
+                                      _lib.ptr(self.argws) if tokens is not None else None, _lib.ptr(tokens),
+                                      _lib.stream_handle()), "ap_gemv")
 
     def _step_body(self, variant: str):
         torch = D.torch()
@@ -278,10 +307,14 @@ class DecodeEngine:
             self._layer(l, variant)
         if self.voff is not None and variant in ("plain", "calib"):
             main.wait_stream(self.pf_stream)
-        _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.lnf), _lib.ptr(self.y),
-                                         S, sh.hidden, sh.eps, s))
-        torch.matmul(self.y, self.lm_head.t(), out=self.logits)
-        torch.argmax(self.logits, dim=-1, out=self.tok)
+        if self.fused:  # final norm + LM head + greedy argmax in one pass over the LM head
+            self._gemv(self.lm_head, self.mlp, self.logits, GEMV_RMS | GEMV_ARGMAX, residual=self.r2, ln=self.lnf,
+                       tokens=self.tok)
+        else:
+            _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.lnf),
+                                             _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
+            torch.matmul(self.y, self.lm_head.t(), out=self.logits)
+            torch.argmax(self.logits, dim=-1, out=self.tok)
         if self.sel is not None and variant != "dense":
             self.sel.step()  # forecast + top-k for the next token, every layer and head at once
 
@@ -387,11 +420,11 @@ class DecodeEngine:
     def kernels_per_step(self, variant: str) -> int:
         """Launches of libattnpred kernels in one step (the bench's gpu_launches claim)."""
         L = self.shape.n_layers
-        per_layer = 2 + 1 + 1  # rmsnorm x2, rope_append, silu_mul
+        per_layer = 3 + 1 if self.fused else 2 + 1 + 1  # gemv x3 + rope | rmsnorm x2, rope_append, silu_mul
         att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
         att_total = self.dense_layers + (L - self.dense_layers) * att
         sel = 2 if (self.sel is not None and variant != "dense") else 0
         off = 0
         if self.voff is not None:
             off = L * (1 + (1 if variant in ("plain", "calib") else 0))  # v_append (+ prefetch) per layer
-        return 1 + L * per_layer + att_total + 1 + sel + off  # advance + layers + final norm + selector
+        return 1 + L * per_layer + att_total + 1 + sel + off  # advance + layers + final norm/LM head + selector
