@@ -17,6 +17,7 @@
 // block of one head is 4 KiB contiguous.  A warp processes one block: lane =
 // (token parity, 8-dim slice), 16-byte loads, half-warp shuffle reductions.
 // Flash-decoding split over blocks; a combine kernel merges the splits.
+#include <cooperative_groups.h>
 #include <cstring>
 
 #include "common.cuh"
@@ -478,6 +479,196 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_partial_kernel(AttnParams 
     if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) combine_heads(P, s, h0, NH);
 }
 
+// ------------------------------------------------------------------ sparse, one cluster per map
+// The CL split CTAs of a map form a thread-block cluster: partials meet in distributed shared
+// memory behind cluster barriers instead of a global workspace + completion counter, the CTA of
+// rank h finalises q-head h, and every CTA emits the compressed-row values of its own blocks once
+// the LSEs are known (the rest of the row was zeroed by the CTAs at the start, off the critical
+// path).  Same arithmetic as sparse_partial_kernel + combine_heads.
+template <int NH>
+__device__ void merge_warps_to_smem(WarpState<NH, true>& st, float* scratch, float (*cpart)[HD + 2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = lane >> 4, sub = lane & 15;
+#pragma unroll
+    for (int h = 0; h < NH; ++h)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st.acc[h][i] += __shfl_xor_sync(0xffffffffu, st.acc[h][i], 16);
+    float* w = scratch + warp * NH * (HD + 2);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        if (lane == 0) {
+            w[h * (HD + 2) + 0] = st.m[h];
+            w[h * (HD + 2) + 1] = st.l[h];
+        }
+        if (half == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[h * (HD + 2) + 2 + sub * 8 + i] = st.acc[h][i];
+        }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < NH * (HD + 2); idx += ATT_THREADS) {
+        const int h = idx / (HD + 2), e = idx % (HD + 2);
+        float M = -INFINITY;
+        for (int ww = 0; ww < ATT_WARPS; ++ww) M = fmaxf(M, scratch[(ww * NH + h) * (HD + 2)]);
+        float val = 0.f;
+        if (e == 0) {
+            val = M;
+        } else if (M != -INFINITY) {
+            for (int ww = 0; ww < ATT_WARPS; ++ww) {
+                const float mw = scratch[(ww * NH + h) * (HD + 2)];
+                if (mw == -INFINITY) continue;
+                val += scratch[(ww * NH + h) * (HD + 2) + e] * exp2f(mw - M);
+            }
+        }
+        cpart[h][e] = val;
+    }
+}
+
+// CL = cluster size = splits per map (8 portable, 16 with the non-portable opt-in); launched with
+// the cluster dimension as a launch attribute.
+template <int NH, bool EMIT, int CL>
+__global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams P) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ float cpart[NH][HD + 2];  // this split's (m, l, acc) per head
+    __shared__ float s_lse[NH];          // LSE of head h, valid in the CTA of rank h
+    extern __shared__ float sm_att[];    // [warps][NH][HD+2] merge scratch, then [units][NH] block maxima
+    const int split = (int)cluster.block_rank(), g = blockIdx.y, s = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane & 15;
+    const int64_t t = P.seq_len[s];
+    const int b = P.block;
+    const int map = s * P.maps_per_seq + P.map_base + g;
+    const ap_map_state ms = P.sel.state[map];
+    const int64_t sink_end = P.sel.sink < t ? P.sel.sink : t;
+    const int64_t local_start = t - P.sel.local > 0 ? t - P.sel.local : 0;
+    const int64_t sb = (sink_end + b - 1) / b;
+    const int64_t eb = (t + b - 1) / b;
+    int64_t lb = local_start / b;
+    if (lb < sb) lb = sb;
+    const int n_local = (int)(eb - lb);
+    const int n_units = (int)sb + n_local + ms.n_mid;
+    const int per = (n_units + CL - 1) / CL;
+    const int u0 = split * per, u1 = min(n_units, u0 + per);
+    const int32_t* mid = P.sel.mid_blocks + (int64_t)map * (P.sel.k_mid > 0 ? P.sel.k_mid : 1);
+    const int h0 = g * NH;
+    const int kvh = h0 / (P.n_q_heads / P.n_kv_heads);
+    const __nv_bfloat16* kh = P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
+    const __nv_bfloat16* vh = P.v + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
+    float* s_bm = sm_att + ATT_WARPS * NH * (HD + 2);  // [per][NH]
+    const int Hh = P.sel.history;
+    const int slot = (int)(ms.n_pushed % Hh);
+    float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
+    const int64_t W = eb;
+    if constexpr (EMIT) {  // zero this CTA's share of the new row (and of [W, old width)), refilled after barrier 2
+        const int old_w = P.sel.slot_width[(int64_t)map * Hh + slot];
+        const int64_t Z = old_w > W ? old_w : W;
+        const int64_t z0 = Z * split / CL, z1 = Z * (split + 1) / CL;
+        for (int64_t j = z0 + threadIdx.x; j < z1; j += ATT_THREADS) dst[j] = 0.f;
+        if (split == 0 && threadIdx.x == 0) P.sel.slot_xmax[(int64_t)map * Hh + slot] = 0.f;  // atomicMax'd later
+    }
+    const float qscale = LOG2E * rsqrtf((float)HD);
+    float qf[NH][8];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(P.q + ((int64_t)s * P.n_q_heads + h0 + h) * HD + sub * 8));
+        bf16x8_to_f32(u, qf[h]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qf[h][i] *= qscale;
+    }
+    WarpState<NH, true> st;
+    st.init();
+    const int64_t mid_clip = ms.mid_clip;
+    auto block_of = [&](int u, bool& is_mid) -> int64_t {
+        is_mid = false;
+        if (u < sb) return u;
+        if (u < sb + n_local) return lb + (u - sb);
+        is_mid = true;
+        return mid[u - sb - n_local];
+    };
+    auto v_of = [&](int u, int64_t j, bool is_mid) -> const __nv_bfloat16* {
+        if (!P.paged) return vh;
+        // page of block j: sink | recent ring | middle page (prefetched, kernel 5); rebased so that
+        // vsrc + p*HD addresses token p of this block inside its page
+        const int64_t vmap = ((int64_t)P.layer * P.n_seq + s) * P.n_kv_heads + kvh;
+        const int npg = P.vp.sink_pages + P.vp.recent_pages + P.vp.k_cap;
+        int page;
+        if (is_mid) page = P.vp.sink_pages + P.vp.recent_pages + P.vp.mid_page[vmap * P.vp.k_cap + (u - sb - n_local)];
+        else if (j < P.vp.sink_pages) page = (int)j;
+        else page = P.vp.sink_pages + (int)(j % P.vp.recent_pages);
+        return reinterpret_cast<const __nv_bfloat16*>(P.vp.pages) + ((vmap * npg + page) * 16 - j * b) * HD;
+    };
+    for (int u = u0 + warp; u < u1; u += ATT_WARPS) {
+        bool is_mid;
+        const int64_t j = block_of(u, is_mid);
+        auto take = [&](int64_t p) {
+            if (p >= t) return false;
+            if (p < sink_end || p >= local_start) return true;
+            return is_mid && p < mid_clip;
+        };
+        process_block<NH, true, EMIT>(kh, v_of(u, j, is_mid), j, b, qf, st, take,
+                                      [&](int h, float v) { if (lane == 0) s_bm[(u - u0) * NH + h] = v; });
+    }
+    merge_warps_to_smem<NH>(st, sm_att, cpart);
+    cluster.sync();  // (1) every split's partial is visible in its shared memory
+    if (split < NH) {  // rank h finalises q-head h over the CL partials
+        const int h = split;
+        float mr[CL], wr[CL];
+        float M = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+            mr[r] = cluster.map_shared_rank(&cpart[h][0], r)[0];
+            M = fmaxf(M, mr[r]);
+        }
+        float L = 0.f;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+            wr[r] = (mr[r] == -INFINITY) ? 0.f : exp2f(mr[r] - M);
+            L += cluster.map_shared_rank(&cpart[h][1], r)[0] * wr[r];
+        }
+        if (threadIdx.x < HD) {
+            float o = 0.f;
+#pragma unroll
+            for (int r = 0; r < CL; ++r) o = fmaf(cluster.map_shared_rank(&cpart[h][2 + threadIdx.x], r)[0], wr[r], o);
+            P.out[((int64_t)s * P.n_q_heads + h0 + h) * HD + threadIdx.x] = __float2bfloat16_rn(o / L);
+        }
+        if (threadIdx.x == 0) {
+            s_lse[h] = M + log2f(L);
+            if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = M + log2f(L);
+        }
+    }
+    if constexpr (EMIT) {
+        cluster.sync();  // (2) the LSEs are visible
+        float lse[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) lse[h] = cluster.map_shared_rank(&s_lse[h], h)[0];
+        float mx = 0.f;
+        for (int u = u0 + threadIdx.x; u < u1; u += ATT_THREADS) {
+            bool is_mid;
+            const int64_t j = block_of(u, is_mid);
+            float v = 0.f;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                const float lg = s_bm[(u - u0) * NH + h];
+                if (lg != -INFINITY) v = fmaxf(v, exp2f(lg - lse[h]));
+            }
+            dst[j] = v;
+            mx = track_row_max(mx, v, P.sel.status);
+        }
+        mx = cta_max_nonneg(mx);
+        if (threadIdx.x == 0) {
+            atomicMax(reinterpret_cast<int*>(P.sel.slot_xmax + (int64_t)map * Hh + slot), __float_as_int(mx));
+            if (split == 0) {
+                ap_map_state st2 = ms;
+                P.sel.slot_width[(int64_t)map * Hh + slot] = (int32_t)W;
+                st2.n_pushed += 1;
+                st2.row_len = t;
+                st2.width = (int32_t)W;
+                P.sel.state[map] = st2;
+            }
+        }
+    }
+    cluster.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
 template <int NH>
 static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream_t st) {
     dim3 grid(P.n_splits, P.n_kv_heads, P.n_seq);
@@ -487,8 +678,40 @@ static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream
     else dense_partial_kernel<NH, false, true><<<grid, ATT_THREADS, sm, st>>>(P);
 }
 
+template <int NH, bool EMIT, int CL>
+static void launch_cluster(const AttnParams& P, cudaStream_t st) {
+    const int units_max = (P.sel.sink + P.block - 1) / P.block + P.sel.local / P.block + 2 + P.sel.k_mid;
+    const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * NH) * sizeof(float);
+    auto k = sparse_cluster_kernel<NH, EMIT, CL>;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (CL > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, P.n_q_heads / NH, P.n_seq);
+    cfg.blockDim = dim3(ATT_THREADS);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, P);
+}
+
 template <int NH>
 static void launch_sparse(const AttnParams& P, bool emit, cudaStream_t st) {
+    if (P.n_splits == 8 || P.n_splits == 16) {  // cluster form
+        if (P.n_splits == 8) {
+            if (emit) launch_cluster<NH, true, 8>(P, st);
+            else launch_cluster<NH, false, 8>(P, st);
+        } else {
+            if (emit) launch_cluster<NH, true, 16>(P, st);
+            else launch_cluster<NH, false, 16>(P, st);
+        }
+        return;
+    }
     dim3 grid(P.n_splits, P.n_q_heads / NH, P.n_seq);
     const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
     if (emit) sparse_partial_kernel<NH, true><<<grid, ATT_THREADS, sm, st>>>(P);

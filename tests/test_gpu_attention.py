@@ -100,19 +100,21 @@ def _set_selection(sel, rng, lens, maps, k_mid, b=16):
     return blocks_per_map
 
 
+@pytest.mark.parametrize("splits", [4, 8])  # 8 = the thread-block-cluster form
 @pytest.mark.parametrize("group", [1, 4])
-def test_sparse_attention_and_observed_row(group):
+def test_sparse_attention_and_observed_row(group, splits):
     import torch
     from paper_2502_04077_b200.attention import DecodeAttention
     S, Hq, Hkv, t_max = 2, 8, 2, 2048
     q, k, v = _setup(S, Hq, Hkv, t_max, seed=3)
     lens = [1500, 2001]
     seq_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
-    att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_sparse=4)
+    att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_sparse=splits)
     qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
     out = torch.empty(S, Hq, 128, dtype=torch.bfloat16, device="cuda")
     maps = Hq // group
     sel = _selector(S * maps, t_max // 16)
+    sel.ring.fill_(7.0)  # stale slot content: everything outside the selection must be re-zeroed
     blocks = _set_selection(sel, np.random.default_rng(1), lens, maps, 56)
     att.sparse(qd, kd, vd, seq_len, out, sel, emit=True, map_base=0, maps_per_seq=maps, group=group)
     torch.cuda.synchronize()
@@ -137,9 +139,15 @@ def test_sparse_attention_and_observed_row(group):
             got = ring[m, 0, : want.size]
             assert np.allclose(got, want, rtol=1e-3, atol=1e-7 * want.max()), (s, g)
             assert np.count_nonzero(got) == np.count_nonzero(want)
+            assert not ring[m, 0, want.size:].any()  # zero beyond the row's width
+            assert np.isclose(float(sel.slot_xmax[m, 0]), float(got.max()), rtol=1e-6)
+    st = sel.states()
+    assert (st["n_pushed"] == 1).all()
+    assert list(st["width"][::maps]) == [-(-t // 16) for t in lens]
 
 
-def test_sparse_with_full_selection_equals_dense():
+@pytest.mark.parametrize("splits", [3, 8])
+def test_sparse_with_full_selection_equals_dense(splits):
     """With a budget that covers every block, sparse attention reproduces dense attention."""
     import torch
     from paper_2502_04077_b200.attention import DecodeAttention
@@ -147,7 +155,7 @@ def test_sparse_with_full_selection_equals_dense():
     q, k, v = _setup(S, Hq, Hkv, t_max, seed=5)
     t = 500
     seq_len = torch.tensor([t], dtype=torch.int32, device="cuda")
-    att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_dense=2, n_splits_sparse=3)
+    att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_dense=2, n_splits_sparse=splits)
     qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
     o1 = torch.empty(S, Hq, 128, dtype=torch.bfloat16, device="cuda")
     o2 = torch.empty_like(o1)
