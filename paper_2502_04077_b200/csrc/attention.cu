@@ -371,6 +371,12 @@ __global__ void __launch_bounds__(ATT_THREADS) dense_partial_kernel(AttnParams P
     const __nv_bfloat16* kh = P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
     const __nv_bfloat16* vh = P.v + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
     const int h0 = kvh * NH;
+    pdl_trigger();
+    for (int64_t jp = j0 + warp; jp < j1 && jp < j0 + 2 * ATT_WARPS; jp += ATT_WARPS) {  // first blocks into L2
+        prefetch_l2(reinterpret_cast<const char*>(kh + jp * b * HD) + lane * 128);
+        if constexpr (WITH_V) prefetch_l2(reinterpret_cast<const char*>(vh + jp * b * HD) + lane * 128);
+    }
+    pdl_wait();  // q and the newest K/V token come from the kernel just before
     const float qscale = LOG2E * rsqrtf((float)HD);
     float qf[NH][8];
 #pragma unroll
@@ -534,6 +540,9 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     extern __shared__ float sm_att[];    // [warps][NH][HD+2] merge scratch, then [units][NH] block maxima
     const int split = (int)cluster.block_rank(), g = blockIdx.y, s = blockIdx.z;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane & 15;
+    pdl_trigger();
+    // Until pdl_wait: only data older than the previous kernel (positions, map state and selection,
+    // the ring slot being replaced) — q and the newest K/V token come from the kernel just before.
     const int64_t t = P.seq_len[s];
     const int b = P.block;
     const int map = s * P.maps_per_seq + P.map_base + g;
@@ -565,6 +574,22 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
         for (int64_t j = z0 + threadIdx.x; j < z1; j += ATT_THREADS) dst[j] = 0.f;
         if (split == 0 && threadIdx.x == 0) P.sel.slot_xmax[(int64_t)map * Hh + slot] = 0.f;  // atomicMax'd later
     }
+    auto block_of = [&](int u, bool& is_mid) -> int64_t {
+        is_mid = false;
+        if (u < sb) return u;
+        if (u < sb + n_local) return lb + (u - sb);
+        is_mid = true;
+        return mid[u - sb - n_local];
+    };
+    for (int u = u0 + warp; u < u1; u += ATT_WARPS) {  // K/V of this CTA's blocks into L2 (8 KB each)
+        bool is_mid;
+        const int64_t j = block_of(u, is_mid);
+        const char* kb = reinterpret_cast<const char*>(kh + j * b * HD);
+        const char* vb = reinterpret_cast<const char*>(vh + j * b * HD);
+        prefetch_l2(kb + lane * 128);
+        if (!P.paged) prefetch_l2(vb + lane * 128);
+    }
+    pdl_wait();
     const float qscale = LOG2E * rsqrtf((float)HD);
     float qf[NH][8];
 #pragma unroll
@@ -577,13 +602,6 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     WarpState<NH, true> st;
     st.init();
     const int64_t mid_clip = ms.mid_clip;
-    auto block_of = [&](int u, bool& is_mid) -> int64_t {
-        is_mid = false;
-        if (u < sb) return u;
-        if (u < sb + n_local) return lb + (u - sb);
-        is_mid = true;
-        return mid[u - sb - n_local];
-    };
     auto v_of = [&](int u, int64_t j, bool is_mid) -> const __nv_bfloat16* {
         if (!P.paged) return vh;
         // page of block j: sink | recent ring | middle page (prefetched, kernel 5); rebased so that
@@ -673,9 +691,9 @@ template <int NH>
 static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream_t st) {
     dim3 grid(P.n_splits, P.n_kv_heads, P.n_seq);
     const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
-    if (with_v && emit) dense_partial_kernel<NH, true, true><<<grid, ATT_THREADS, sm, st>>>(P);
-    else if (with_v) dense_partial_kernel<NH, true, false><<<grid, ATT_THREADS, sm, st>>>(P);
-    else dense_partial_kernel<NH, false, true><<<grid, ATT_THREADS, sm, st>>>(P);
+    if (with_v && emit) launch_ex(dense_partial_kernel<NH, true, true>, grid, dim3(ATT_THREADS), sm, st, 1, P);
+    else if (with_v) launch_ex(dense_partial_kernel<NH, true, false>, grid, dim3(ATT_THREADS), sm, st, 1, P);
+    else launch_ex(dense_partial_kernel<NH, false, true>, grid, dim3(ATT_THREADS), sm, st, 1, P);
 }
 
 template <int NH, bool EMIT, int CL>
@@ -685,19 +703,7 @@ static void launch_cluster(const AttnParams& P, cudaStream_t st) {
     auto k = sparse_cluster_kernel<NH, EMIT, CL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (CL > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL, P.n_q_heads / NH, P.n_seq);
-    cfg.blockDim = dim3(ATT_THREADS);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k, P);
+    launch_ex(k, dim3(CL, P.n_q_heads / NH, P.n_seq), dim3(ATT_THREADS), sm, st, CL, P);
 }
 
 template <int NH>

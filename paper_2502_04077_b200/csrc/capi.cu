@@ -1,6 +1,7 @@
 // Library-wide host helpers: version, last-error text, SM count.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -13,6 +14,15 @@ void set_last_error(const char* fmt, ...) {
     va_start(ap_, fmt);
     vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap_);
     va_end(ap_);
+}
+
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ATTNPRED_PDL");
+        v = !(e && e[0] == '0');
+    }
+    return v == 1;
 }
 
 int launch_status(const char* what) {

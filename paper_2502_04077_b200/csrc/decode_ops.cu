@@ -67,6 +67,8 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq
     const int s = blockIdx.y;
     const int head = blockIdx.x;  // [0, Hq + 2*Hkv)
     const int i = threadIdx.x;    // 0..63
+    pdl_trigger();
+    pdl_wait();  // qkv comes from the projection just before
     const int pos = seq_len[s] - 1;
     const __nv_bfloat16* src = qkv + ((int64_t)s * (Hq + 2 * Hkv) + head) * 128;
     float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + 64]);
@@ -123,9 +125,9 @@ int ap_rmsnorm(const void* x, void* residual, const void* weight, void* y, int32
 int ap_rope_append(const void* qkv, int32_t n_seq, int32_t n_q_heads, int32_t n_kv_heads, const int32_t* seq_len,
                    void* q_out, void* k_cache, void* v_cache, int32_t t_max, float theta, void* stream) {
     dim3 grid(n_q_heads + 2 * n_kv_heads, n_seq);
-    rope_append_kernel<<<grid, 64, 0, as_stream(stream)>>>((const __nv_bfloat16*)qkv, n_q_heads, n_kv_heads, seq_len,
-                                                           (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
-                                                           (__nv_bfloat16*)v_cache, t_max, theta);
+    launch_ex(rope_append_kernel, grid, dim3(64), 0, as_stream(stream), 1, (const __nv_bfloat16*)qkv, (int)n_q_heads,
+              (int)n_kv_heads, seq_len, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache,
+              (int)t_max, theta);
     return launch_status("ap_rope_append");
 }
 

@@ -58,6 +58,22 @@ __global__ void __launch_bounds__(THREADS) gemv_kernel(Params P) {
     extern __shared__ __align__(16) float xs[];  // [NS][K] fp32 activations
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int K = P.K;
+    pdl_trigger();
+    {  // before the producer of x has finished: pull this warp's first weight rows into L2
+        const int g = blockIdx.x * WARPS + warp;
+        const int per_group = (EPI == EPI_SILU) ? ROWS / 2 : ROWS;
+        const int n_groups = (((EPI == EPI_SILU) ? P.N / 2 : P.N) + per_group - 1) / per_group;
+        if (g < n_groups)
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                int n;
+                if constexpr (EPI == EPI_SILU) n = g * per_group + (r >> 1) + ((r & 1) ? P.N / 2 : 0);
+                else n = g * ROWS + r;
+                const char* row = reinterpret_cast<const char*>(P.W + (int64_t)min(n, P.N - 1) * K);
+                for (int off = lane * 128; off < K * 2; off += 32 * 128) prefetch_l2(row + off);
+            }
+    }
+    pdl_wait();
     // ---- activations -> shared memory (fp32), optionally normalised
     if constexpr (PRO == PRO_RMSNORM) {
         __shared__ float red[NS][WARPS];
@@ -222,14 +238,16 @@ int launch(const Params& P, cudaStream_t st) {
     const int per_cta = WARPS * ((EPI == EPI_SILU) ? ROWS / 2 : ROWS);
     const size_t smem = (size_t)NS * P.K * 4;
     auto k = gemv_kernel<ROWS, NS, PRO, EPI>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static bool attr_set = false;
+    if (!attr_set) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
     // persistent: at most one wave of resident CTAs, so the activation prologue runs once per CTA
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, THREADS, smem);
     const int cap = ap_device_sm_count() * (occ > 0 ? occ : 1);
     int grid = (outs + per_cta - 1) / per_cta;
     grid = grid < cap ? grid : cap;
-    k<<<grid, THREADS, smem, st>>>(P);
+    launch_ex(k, dim3(grid), dim3(THREADS), smem, st, 1, P);
     return launch_status("gemv_kernel");
 }
 
