@@ -320,8 +320,8 @@ int ap_silu_mul(const void* gate_up, void* out, int32_t rows, int32_t ffn, void*
 /* seq_len[i] += by */
 int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream);
 
-/* Batch-1..4 bf16 GEMV y[s] = W x[s] (W [N][K] row-major, fp32 accumulate), HBM-streaming.
- * rows_per_warp 1/2/4.  flags: bit 0 = RMSNORM prologue (h = x [+ residual], written to residual_out
+/* Batch-1..4 bf16 GEMV y[s] = W x[s] (W [N][K] row-major, K % 8 == 0, fp32 accumulate), HBM-streaming.
+ * rows_per_warp: ignored (ABI slot of an earlier kernel).  flags: bit 0 = RMSNORM prologue (h = x [+ residual], written to residual_out
  * when non-NULL (must not alias); x = rmsnorm(h) * ln_w, the arithmetic of ap_rmsnorm);
  * bits 1-2 = epilogue: 0 store y [s][N],
  * 1 SILU (W = [gate; up], y [s][N/2] = silu(gate) * up, as ap_silu_mul), 2 ARGMAX (greedy token of

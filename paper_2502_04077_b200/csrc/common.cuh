@@ -275,6 +275,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
         :: "r"(addr), "r"(parity), "r"(1000000u) : "memory");  // suspend (<= 1 ms) instead of spinning
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
+}
+// Barrier among `n` threads (a multiple of 32) on hardware barrier `id` (1..15; 0 = __syncthreads).
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory");
+}
+// mbarrier arrive that also expects `bytes` of async-proxy transactions (bulk copies) this phase.
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// Linear global -> shared bulk copy (TMA engine, no tensor map); completion counted on `bar`.
+// bytes and both addresses must be multiples of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// Polling wait (no suspend-time hint): for waits expected to be short and latency-critical.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* mbar, uint32_t parity) {
+    uint32_t addr = smem_u32(mbar);
+    asm volatile(
+        "{\n\t.reg .pred done;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}"
+        :: "r"(addr), "r"(parity) : "memory");
+}
+
 // 32 lanes x 32 columns of zeros -> TMEM (used to clear accumulators).
 __device__ __forceinline__ void tmem_zero32(uint32_t taddr) {
     const uint32_t z = 0u;

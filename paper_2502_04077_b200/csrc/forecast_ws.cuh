@@ -62,12 +62,6 @@ struct Smem {
     static constexpr int total = off_bar + 8 * (3 * NX + 4 * NA) + 16;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory");
-}
 
 template <int PREC>
 __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {

@@ -247,14 +247,6 @@ struct SmemLayout {
     static constexpr int total = off_bar + 48;  // mbar(mma), mbar_x[2], tmem slot, xmax
 };
 
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-
 // Thread 0's work-list iterator: tasks blockIdx.x, +gridDim.x, ...; bands within a task.  The map
 // state of the following task is loaded one task ahead so planning never waits on global memory.
 struct Iter {

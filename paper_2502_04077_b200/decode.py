@@ -72,8 +72,8 @@ class DecodeEngine:
     dense) — layers [0, dense_layers) always run full attention and own no
     selector maps.
     fused: batch <= 4 runs the projections through ap_gemv with the neighbouring elementwise ops
-    fused (RMSNorm prologues, SiLU-gate epilogue, LM head + greedy argmax); the down projection
-    stays a cuBLAS GEMM.  fused=False keeps one library GEMM + one elementwise kernel per op.
+    fused (RMSNorm prologues, SiLU-gate epilogue, LM head + greedy argmax) and the down projection
+    as a plain ap_gemv.  fused=False keeps one library GEMM + one elementwise kernel per op.
     """
 
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
@@ -277,7 +277,10 @@ class DecodeEngine:
                                              _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
             torch.matmul(self.y, self.wgu[l].t(), out=self.gu)
             _lib.check(_lib.fn("ap_silu_mul")(_lib.ptr(self.gu), _lib.ptr(self.act), S, sh.ffn, s))
-        torch.matmul(self.act, self.wdown[l].t(), out=self.mlp)
+        if self.fused:
+            self._gemv(self.wdown[l], self.act, self.mlp, 0)
+        else:
+            torch.matmul(self.act, self.wdown[l].t(), out=self.mlp)
 
     def _gemv(self, W, x, y, flags, residual=None, residual_out=None, ln=None, tokens=None):
         """ap_gemv: y = W x for this step's sequences with the fused prologue / epilogue in flags."""
@@ -420,7 +423,7 @@ class DecodeEngine:
     def kernels_per_step(self, variant: str) -> int:
         """Launches of libattnpred kernels in one step (the bench's gpu_launches claim)."""
         L = self.shape.n_layers
-        per_layer = 3 + 1 if self.fused else 2 + 1 + 1  # gemv x3 + rope | rmsnorm x2, rope_append, silu_mul
+        per_layer = 4 + 1 if self.fused else 2 + 1 + 1  # gemv x4 + rope | rmsnorm x2, rope_append, silu_mul
         att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
         att_total = self.dense_layers + (L - self.dense_layers) * att
         sel = 2 if (self.sel is not None and variant != "dense") else 0

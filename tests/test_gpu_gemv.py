@@ -93,8 +93,8 @@ def test_argument_errors():
     x = torch.zeros(5, 16, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(ParameterError):
         _call(W, x, torch.empty(5, 8, device="cuda", dtype=torch.bfloat16), 5, 0)  # > 4 rows
-    with pytest.raises(ParameterError):
-        _call(W, x[:1], torch.empty(1, 4, device="cuda", dtype=torch.bfloat16), 1, SILU, rows=1)
+    with pytest.raises(ParameterError):  # SILU needs [gate; up] row pairs
+        _call(W[:7], x[:1], torch.empty(1, 4, device="cuda", dtype=torch.bfloat16), 1, SILU)
 
 
 def test_fused_engine_matches_unfused():
