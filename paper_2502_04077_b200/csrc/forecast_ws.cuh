@@ -26,6 +26,8 @@ namespace ap {
 namespace ws {
 
 __device__ unsigned long long g_prof[16 * 160];  // debug bit 8: per-CTA cycle counters per role phase
+__device__ long long g_trace[64 * 8];             // debug bit 16: CTA 0 timeline of its first 64 bands
+#define WS_TRACE(b, e) if ((dbg & 16) && blockIdx.x == 0 && (b) < 64) g_trace[(b) * 8 + (e)] = clock64();
 
 constexpr int NT = 512;
 constexpr int NX = 6;                       // x tile stages
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
                     if (xrow)
                         bulk_g2s(reinterpret_cast<float*>(smem + L::off_x + s * L::kX) + lane * XC4 + (c_lo - (w0 - 4)),
                                  ring + (int64_t)slot * P.pitch + c_lo, (uint32_t)(c_hi - c_lo) * 4, &x_full[s]);
+                    if (lane == 0) WS_TRACE(b, 0);
                     t_wait += t1 - t0;
                     t_plan += clock64() - t1;
                     if (!P.slot_xmax && b >= SCAN_LAG) finalize(b - SCAN_LAG);
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
                     break;
                 }
                 tc_fence_after();
+                WS_TRACE(b, 4);
                 ainfo[a] = I;
                 const uint32_t a1_addr = smem_u32(smem + L::off_a1 + a * L::kA1);
                 // Slot q's first writer initialises it (accumulate = 0): the first real a1 row
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
                     }
                     first_row = false;
                 }
+                WS_TRACE(b, 5);
                 mma_commit(&a1_empty[a]);   // a1 tile consumed -> conv1 may refill it
                 mma_commit(&acc_full[a]);   // accumulators ready
                 mbar_arrive(&acc_full[a]);  // releases ainfo[a]
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             e_t = clock64();
             e_wait += e_t - e0;
             const BandInfo I = ainfo[a];
+            if (warp == EPI0 && lane == 0) WS_TRACE(b, 6);
             if (!I.valid) {
                 if ((dbg & 8) && warp == EPI0 && lane == 0) {
                     g_prof[blockIdx.x * 16 + 2] = e_wait;
@@ -431,6 +437,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             e_math += clock64() - q0;
             tc_fence_before();  // our tcgen05.ld reads of buffer a are complete before it is reused
             __syncwarp();
+            if (warp == EPI0 && lane == 0) WS_TRACE(b, 7);
             if (lane == 0) mbar_arrive(&acc_empty[a]);
             if (I.last && live) {
                 float osum = 0.f;
@@ -474,6 +481,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             long long ca = clock64();
             if (b >= NA) mbar_wait(&a1_empty[a], ((b / NA) & 1) ^ 1);
             long long cb = clock64();
+            if (ct == 0) WS_TRACE(b, 2);
             c_wa += cb - ca;
             c_work -= cb - ca;
             uint8_t* a1t = smem + L::off_a1 + a * L::kA1;
@@ -538,6 +546,8 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             }
             fence_async_smem();  // a1 tile -> visible to the tensor core's async proxy
             __syncwarp();
+            if (ct == 0) WS_TRACE(b, 3);
+            if (ct == NCONV_T - 32) WS_TRACE(b, 1);
             if (lane == 0) {
                 mbar_arrive(&a1_full[a]);
                 mbar_arrive(&x_empty[s]);

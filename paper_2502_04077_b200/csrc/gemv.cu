@@ -296,14 +296,27 @@ int launch(Params P, cudaStream_t st) {
     // slabs: the fewest with <= SLAB_MAX columns each and >= 2 (ideally 3) stages next to the activations
     const int64_t xbytes = (int64_t)NS * P.K * 2;
     const int64_t ring = CTA_SMEM - xbytes;
-    int n_slab = (P.K + SLAB_MAX - 1) / SLAB_MAX;
+    static int slab_max = -1;  // ATTNPRED_GEMV_SLAB: tuning override (<= SLAB_MAX, multiple of 8)
+    if (slab_max < 0) {
+        const char* e = getenv("ATTNPRED_GEMV_SLAB");
+        slab_max = e ? atoi(e) : SLAB_MAX;
+        if (slab_max < 256 || slab_max > SLAB_MAX) slab_max = SLAB_MAX;
+    }
+    int n_slab = (P.K + slab_max - 1) / slab_max;
     auto slab_of = [&](int n) { return ((P.K + n - 1) / n + 7) / 8 * 8; };
     while (ring < 3 * (int64_t)GROUP * slab_of(n_slab) * 2 && slab_of(n_slab) > 512) ++n_slab;
     P.n_slab = n_slab;
     P.slab = slab_of(n_slab);
     P.pitch = P.slab * 2;
     const int64_t stage_bytes = (int64_t)GROUP * P.pitch;
+    static int nst_max = -1;  // ATTNPRED_GEMV_STAGES: tuning override
+    if (nst_max < 0) {
+        const char* e = getenv("ATTNPRED_GEMV_STAGES");
+        nst_max = e ? atoi(e) : MAX_STAGES;
+        if (nst_max < 2 || nst_max > MAX_STAGES) nst_max = MAX_STAGES;
+    }
     int64_t nst = ring / stage_bytes;
+    nst = nst > nst_max ? nst_max : nst;
     nst = nst > MAX_STAGES ? MAX_STAGES : nst;
     AP_REQUIRE(nst >= 2, AP_EPARAM, "ap_gemv: K = %d too large for the shared-memory stage ring", P.K);
     P.nst = (int)nst;

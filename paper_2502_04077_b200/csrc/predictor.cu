@@ -603,7 +603,19 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
 
 }  // namespace ap
 #include "forecast_ws.cuh"
+#include "forecast_ts.cuh"
 namespace ap {
+
+template <int PREC>
+static int grid_ctas_ts() {
+    static int cached = 0;
+    if (!cached) {
+        cudaFuncSetAttribute(ts::conv_forecast_ts_kernel<PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ts::Smem::total);
+        cached = ap_device_sm_count();  // one 14-warp CTA (and all 512 TMEM columns) per SM
+    }
+    return cached;
+}
 
 template <int PREC>
 static int grid_ctas_ws() {
@@ -641,14 +653,16 @@ static int grid_ctas() {
     return cached;
 }
 
-// ATTNPRED_FORECAST_KERNEL=bands selects the non-specialised kernel (A/B comparisons)
-static bool ws_enabled() {
+// Tensor-core forecaster variant: 1 = shared-memory-operand warp-specialised kernel (default),
+// 2 = register-fed TS kernel (ATTNPRED_FORECAST_KERNEL=ts; measured 10% slower),
+// 0 = single-role band kernel (=bands); the alternatives stay for A/B measurements.
+static int tc_kernel() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("ATTNPRED_FORECAST_KERNEL");
-        v = !(e && strcmp(e, "bands") == 0);
+        v = (e && strcmp(e, "bands") == 0) ? 0 : (e && strcmp(e, "ts") == 0) ? 2 : 1;
     }
-    return v == 1;
+    return v;
 }
 
 static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
@@ -670,7 +684,10 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
             break;
         }
         case AP_PREC_F16X3: {
-            if (P.pitch % 4 == 0 && ws_enabled()) {
+            if (P.pitch % 4 == 0 && tc_kernel() == 2) {
+                int g = grid_ctas_ts<AP_PREC_F16X3>();
+                ts::conv_forecast_ts_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, ts::NT, ts::Smem::total, st>>>(P);
+            } else if (P.pitch % 4 == 0 && tc_kernel() == 1) {
                 int g = grid_ctas_ws<AP_PREC_F16X3>();
                 ws::conv_forecast_ws_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, ws::NT, ws::Smem<AP_PREC_F16X3>::total, st>>>(P);
             } else {
@@ -680,7 +697,10 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
             break;
         }
         case AP_PREC_F16: {
-            if (P.pitch % 4 == 0 && ws_enabled()) {
+            if (P.pitch % 4 == 0 && tc_kernel() == 2) {
+                int g = grid_ctas_ts<AP_PREC_F16>();
+                ts::conv_forecast_ts_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, ts::NT, ts::Smem::total, st>>>(P);
+            } else if (P.pitch % 4 == 0 && tc_kernel() == 1) {
                 int g = grid_ctas_ws<AP_PREC_F16>();
                 ws::conv_forecast_ws_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, ws::NT, ws::Smem<AP_PREC_F16>::total, st>>>(P);
             } else {
@@ -778,6 +798,12 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream) {
 int ap_debug_prof(unsigned long long* host_out, int n) {
     return cudaMemcpyFromSymbol(host_out, ws::g_prof, sizeof(unsigned long long) * (n < 16 * 160 ? n : 16 * 160)) ==
                    cudaSuccess ? AP_OK : AP_ECUDA;
+}
+
+int ap_debug_trace(long long* host_out) {
+    const bool ts = tc_kernel() == 2;
+    return (ts ? cudaMemcpyFromSymbol(host_out, ts::g_trace, sizeof(long long) * 64 * 8)
+               : cudaMemcpyFromSymbol(host_out, ws::g_trace, sizeof(long long) * 64 * 8)) == cudaSuccess ? AP_OK : AP_ECUDA;
 }
 
 int ap_sel_grid_ctas(int precision) {

@@ -1,5 +1,6 @@
-mkdir -p gpurun_out/gsweep8
-timeout 300 python -m pytest tests/test_gpu_gemv.py tests/test_gpu_decode.py -x -q > gpurun_out/gsweep8/tests.log 2>&1
-timeout 120 python scripts/bench_gemv.py --rows 1 > gpurun_out/gsweep8/ns1.json 2>&1
-timeout 120 python scripts/bench_gemv.py --rows 1 --ns 4 > gpurun_out/gsweep8/ns4.json 2>&1
-timeout 600 python bench.py --no-alt > gpurun_out/gsweep8/bench.json 2> gpurun_out/gsweep8/bench.err
+mkdir -p gpurun_out/gsweep9
+for cfg in "4096 8" "4096 2" "2048 3" "2048 4" "1024 6"; do
+ set -- $cfg
+ ATTNPRED_GEMV_SLAB=$1 ATTNPRED_GEMV_STAGES=$2 timeout 120 python scripts/bench_gemv.py --rows 1 > gpurun_out/gsweep9/s$1_n$2.json 2>&1
+ ATTNPRED_GEMV_SLAB=$1 ATTNPRED_GEMV_STAGES=$2 timeout 600 python bench.py --no-alt --no-dense --steps 20 > gpurun_out/gsweep9/bench_s$1_n$2.json 2> /dev/null
+done
