@@ -330,6 +330,14 @@ int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream);
 int ap_gemv(const void* W, const void* x, void* y, int32_t N, int32_t K, int32_t n_seq, int32_t rows_per_warp,
             int32_t flags, const void* residual, void* residual_out, const void* ln_w, float eps,
             void* arg_workspace, void* tokens, void* stream);
+/* Fused qkv projection + rotary embedding + KV append for batch-1..4 decode: y = W x (W [(Hq+2Hkv)*128][K],
+ * optional RMSNORM prologue as ap_gemv flag bit 0), y stored as ap_gemv would, then for position
+ * seq_len[s]-1 the arithmetic of ap_rope_append on the bf16 projection output: rotated q -> q_out,
+ * rotated k and v appended to the caches (v_cache NULL: V only in y, for the offload path). */
+int ap_gemv_qkv_rope(const void* W, const void* x, void* y, int32_t n_q_heads, int32_t n_kv_heads, int32_t K,
+                     int32_t n_seq, int32_t flags, const void* residual, void* residual_out, const void* ln_w, float eps,
+                     const int32_t* seq_len, void* q_out, void* k_cache, void* v_cache, int32_t t_max, float theta,
+                     void* stream);
 
 #ifdef __cplusplus
 }

@@ -124,6 +124,8 @@ SIGNATURES = {
     "ap_silu_mul": (ctypes.c_int, [_P, _P, _I32, _I32, _P]),
     "ap_advance": (ctypes.c_int, [_P, _I32, _I32, _P]),
     "ap_gemv": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, ctypes.c_float, _P, _P, _P]),
+    "ap_gemv_qkv_rope": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, ctypes.c_float, _P, _P,
+                                        _P, _P, _I32, ctypes.c_float, _P]),
     # .att1 trace container (host code)
     "ap_trace_check_header": (ctypes.c_int, [ctypes.POINTER(TraceHeaderC)]),
     "ap_trace_check_row": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32]),

@@ -29,6 +29,11 @@ constexpr int ATT_THREADS = 256;        // 8 warps
 constexpr int ATT_WARPS = ATT_THREADS / 32;
 constexpr float LOG2E = 1.4426950408889634f;
 
+__device__ long long g_att_trace[16 * 16];  // debug: clock64 per phase, CTAs (split, 0, 0)
+__device__ int g_att_trace_on;
+#define ATT_TRACE(e) \
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && g_att_trace_on) g_att_trace[blockIdx.x * 16 + (e)] = clock64();
+
 struct AttnParams {
     int32_t n_seq, n_q_heads, n_kv_heads, t_max, n_splits, block;
     const __nv_bfloat16* q;       // [S][Hq][D]
@@ -539,6 +544,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     __shared__ float s_lse[NH];          // LSE of head h, valid in the CTA of rank h
     extern __shared__ float sm_att[];    // [warps][NH][HD+2] merge scratch, then [units][NH] block maxima
     const int split = (int)cluster.block_rank(), g = blockIdx.y, s = blockIdx.z;
+    ATT_TRACE(0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane & 15;
     pdl_trigger();
     // Until pdl_wait: only data older than the previous kernel (positions, map state and selection,
@@ -589,8 +595,10 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
         prefetch_l2(kb + lane * 128);
         if (!P.paged) prefetch_l2(vb + lane * 128);
     }
+    ATT_TRACE(1);
     pdl_wait();
     const float qscale = LOG2E * rsqrtf((float)HD);
+    ATT_TRACE(2);
     float qf[NH][8];
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
@@ -625,8 +633,11 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
         process_block<NH, true, EMIT>(kh, v_of(u, j, is_mid), j, b, qf, st, take,
                                       [&](int h, float v) { if (lane == 0) s_bm[(u - u0) * NH + h] = v; });
     }
+    ATT_TRACE(3);
     merge_warps_to_smem<NH>(st, sm_att, cpart);
+    ATT_TRACE(4);
     cluster.sync();  // (1) every split's partial is visible in its shared memory
+    ATT_TRACE(5);
     if (split < NH) {  // rank h finalises q-head h over the CL partials
         const int h = split;
         float mr[CL], wr[CL];
@@ -653,6 +664,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
             if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = M + log2f(L);
         }
     }
+    ATT_TRACE(6);
     if constexpr (EMIT) {
         cluster.sync();  // (2) the LSEs are visible
         float lse[NH];
@@ -684,7 +696,9 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
             }
         }
     }
+    ATT_TRACE(7);
     cluster.sync();  // no CTA leaves while a peer may still read its shared memory
+    ATT_TRACE(8);
 }
 
 template <int NH>
@@ -754,6 +768,11 @@ static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t m
 using namespace ap;
 
 extern "C" {
+
+int ap_attn_debug_trace(int on, long long* host_out) {
+    if (host_out) return cudaMemcpyFromSymbol(host_out, g_att_trace, sizeof(long long) * 256) == cudaSuccess ? 0 : 5;
+    return cudaMemcpyToSymbol(g_att_trace_on, &on, sizeof(int)) == cudaSuccess ? 0 : 5;
+}
 
 int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
                   int32_t group, int emit, void* stream) {

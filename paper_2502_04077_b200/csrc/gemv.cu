@@ -41,7 +41,9 @@ constexpr int CTA_SMEM = 220 * 1024;       // stage ring + activations
 
 
 enum Prologue { PRO_NONE = 0, PRO_RMSNORM = 1 };
-enum Epilogue { EPI_STORE = 0, EPI_SILU = 1, EPI_ARGMAX = 2 };
+enum Epilogue { EPI_STORE = 0, EPI_SILU = 1, EPI_ARGMAX = 2, EPI_ROPE = 3 };
+// paired epilogues: a stage holds GROUP/2 rows and their GROUP/2 partner rows
+__host__ __device__ constexpr bool paired(int epi) { return epi == EPI_SILU || epi == EPI_ROPE; }
 
 struct Params {
     const __nv_bfloat16* W;  // [N][K]
@@ -58,7 +60,27 @@ struct Params {
     int slab, n_slab;        // columns per slab (multiple of 16), slabs per row
     int pitch;               // shared-memory bytes per staged row (slab * 2 + 16)
     int nst;                 // stages in the ring
+    // ROPE epilogue (fused qkv projection + rotary embedding + KV append, as ap_rope_append)
+    const int32_t* seq_len;  // [NS] positions + 1
+    __nv_bfloat16* q_out;    // [NS][Hq][128]
+    __nv_bfloat16* k_cache;  // [NS][Hkv][t_max][128]
+    __nv_bfloat16* v_cache;  // same, or null (offload mode: V is read back from y)
+    int Hq, Hkv, t_max;
+    float theta;
 };
+
+// Paired units: SILU unit o = gate row o and up row N/2 + o; ROPE unit u = rows 128 h + i and 128 h + i + 64
+// (h = u / 64, i = u % 64).  first_row(u) + k for k < cnt stays inside one head since units are
+// dealt in groups of GROUP/2 and 64 % (GROUP/2) == 0.
+template <int EPI>
+__device__ __forceinline__ int64_t first_row(const Params& P, int u) {
+    if constexpr (EPI == EPI_ROPE) return (int64_t)(u >> 6) * 128 + (u & 63);
+    return u;
+}
+template <int EPI>
+__device__ __forceinline__ int64_t partner_offset(const Params& P) {
+    return EPI == EPI_ROPE ? 64 : P.N / 2;
+}
 
 __device__ __forceinline__ uint32_t order_f32(float f) {  // monotone float -> u32
     const uint32_t u = __float_as_uint(f);
@@ -73,10 +95,11 @@ __global__ void __launch_bounds__(THREADS, 1) gemv_stream_kernel(Params P) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int K = P.K, NST = P.nst, n_slab = P.n_slab, slab = P.slab, pitch = P.pitch;
     const int stage_bytes = GROUP * pitch;
-    constexpr int per_group = (EPI == EPI_SILU) ? GROUP / 2 : GROUP;
-    const int U = (EPI == EPI_SILU) ? P.N / 2 : P.N;
-    const int u0 = (int)((int64_t)blockIdx.x * U / gridDim.x);
-    const int u1 = (int)((int64_t)(blockIdx.x + 1) * U / gridDim.x);
+    constexpr int per_group = paired(EPI) ? GROUP / 2 : GROUP;
+    const int U = paired(EPI) ? P.N / 2 : P.N;
+    const int n_pg = (U + per_group - 1) / per_group;  // groups dealt to CTAs whole
+    const int u0 = min(U, (int)((int64_t)blockIdx.x * n_pg / gridDim.x) * per_group);
+    const int u1 = min(U, (int)((int64_t)(blockIdx.x + 1) * n_pg / gridDim.x) * per_group);
     const int n_group = (u1 - u0 + per_group - 1) / per_group;
     const int n_stage = n_group * n_slab;
     uint8_t* xs = smem + (size_t)NST * stage_bytes;  // [NS][K] bf16
@@ -100,17 +123,18 @@ __global__ void __launch_bounds__(THREADS, 1) gemv_stream_kernel(Params P) {
             uint8_t* dst = smem + slot * stage_bytes;
             const int a = u0 + g * per_group, cnt = min(per_group, u1 - a);
             const int c0 = sl * slab, len = min(slab, K - c0);
-            constexpr int halves = (EPI == EPI_SILU) ? 2 : 1;
+            constexpr int halves = paired(EPI) ? 2 : 1;
+            const int64_t row0 = first_row<EPI>(P, a), off = partner_offset<EPI>(P);
             if (lane == 0) mbar_arrive_tx(&full[slot], (uint32_t)(halves * cnt * len * 2));
             __syncwarp();
             if (n_slab == 1) {  // rows are contiguous in global and in the stage (pitch = row bytes)
                 if (lane < halves) {
-                    const int64_t row = (lane == 0) ? (int64_t)a : (int64_t)(P.N / 2 + a);
+                    const int64_t row = row0 + lane * off;
                     bulk_g2s(dst + lane * (GROUP / 2) * pitch, P.W + row * K, (uint32_t)(cnt * len * 2), &full[slot]);
                 }
             } else if (lane < halves * cnt) {
                 const int h = lane / cnt, r = lane - h * cnt;
-                const int64_t row = (h == 0) ? (int64_t)(a + r) : (int64_t)(P.N / 2 + a + r);
+                const int64_t row = row0 + r + h * off;
                 bulk_g2s(dst + (h * (GROUP / 2) + r) * pitch, P.W + row * K + c0, (uint32_t)len * 2, &full[slot]);
             }
             if (++sl == n_slab) { sl = 0; ++g; }
@@ -241,6 +265,45 @@ __global__ void __launch_bounds__(THREADS, 1) gemv_stream_kernel(Params P) {
                         P.y[(int64_t)s * (P.N / 2) + a + o] = __float2bfloat16_rn(gt / (1.f + __expf(-gt)) * up);
                     }
                 }
+            } else if constexpr (EPI == EPI_ROPE) {
+                if (tid < (GROUP / 2) * NS) {
+                    const int o = tid % (GROUP / 2), s = tid / (GROUP / 2);
+                    if (o < cnt) {
+                        float x1 = 0.f, x2 = 0.f;
+#pragma unroll
+                        for (int w = 0; w < CWARPS; ++w) {
+                            x1 += red[g & 1][w][o][s];
+                            x2 += red[g & 1][w][GROUP / 2 + o][s];
+                        }
+                        const int u = a + o, head = u >> 6, i = u & 63;
+                        const int64_t r1 = (int64_t)head * 128 + i;
+                        const __nv_bfloat16 b1 = __float2bfloat16_rn(x1), b2 = __float2bfloat16_rn(x2);
+                        P.y[(int64_t)s * P.N + r1] = b1;  // the projection output, as ap_gemv stores it
+                        P.y[(int64_t)s * P.N + r1 + 64] = b2;
+                        // ap_rope_append's arithmetic on the bf16 projection output
+                        x1 = __bfloat162float(b1);
+                        x2 = __bfloat162float(b2);
+                        const int pos = P.seq_len[s] - 1;
+                        if (head < P.Hq + P.Hkv) {
+                            const float inv_freq = exp2f(-(float)(2 * i) / 128.f * log2f(P.theta));
+                            float sn, cs;
+                            sincosf((float)pos * inv_freq, &sn, &cs);
+                            const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
+                            x1 = y1;
+                            x2 = y2;
+                        }
+                        __nv_bfloat16* dstp = nullptr;
+                        if (head < P.Hq) dstp = P.q_out + ((int64_t)s * P.Hq + head) * 128;
+                        else if (head < P.Hq + P.Hkv)
+                            dstp = P.k_cache + (((int64_t)s * P.Hkv + (head - P.Hq)) * P.t_max + pos) * 128;
+                        else if (P.v_cache)
+                            dstp = P.v_cache + (((int64_t)s * P.Hkv + (head - P.Hq - P.Hkv)) * P.t_max + pos) * 128;
+                        if (dstp) {
+                            dstp[i] = __float2bfloat16_rn(x1);
+                            dstp[i + 64] = __float2bfloat16_rn(x2);
+                        }
+                    }
+                }
             } else {
                 if (tid < GROUP * NS) {
                     const int rr = tid % GROUP, s = tid / GROUP;
@@ -321,8 +384,8 @@ int launch(Params P, cudaStream_t st) {
     AP_REQUIRE(nst >= 2, AP_EPARAM, "ap_gemv: K = %d too large for the shared-memory stage ring", P.K);
     P.nst = (int)nst;
     const size_t smem = (size_t)(nst * stage_bytes + xbytes);
-    const int units = (EPI == EPI_SILU) ? P.N / 2 : P.N;
-    const int per_group = (EPI == EPI_SILU) ? GROUP / 2 : GROUP;
+    const int units = paired(EPI) ? P.N / 2 : P.N;
+    const int per_group = paired(EPI) ? GROUP / 2 : GROUP;
     int grid = (units + per_group - 1) / per_group;
     const int sms = ap_device_sm_count();
     grid = grid < sms ? grid : sms;
@@ -392,4 +455,42 @@ extern "C" int ap_gemv(const void* W, const void* x, void* y, int32_t N, int32_t
     if (epi == EPI_STORE) return dispatch_ns<PRO_NONE, EPI_STORE>(P, st);
     if (epi == EPI_SILU) return dispatch_ns<PRO_NONE, EPI_SILU>(P, st);
     return dispatch_ns<PRO_NONE, EPI_ARGMAX>(P, st);
+}
+
+extern "C" int ap_gemv_qkv_rope(const void* W, const void* x, void* y, int32_t n_q_heads, int32_t n_kv_heads,
+                                int32_t K, int32_t n_seq, int32_t flags, const void* residual, void* residual_out,
+                                const void* ln_w, float eps, const int32_t* seq_len, void* q_out, void* k_cache,
+                                void* v_cache, int32_t t_max, float theta, void* stream) {
+    using namespace gemv;
+    AP_REQUIRE(W && x && y && seq_len && q_out && k_cache, AP_EPARAM, "bad qkv/rope operands");
+    AP_REQUIRE(n_q_heads > 0 && n_kv_heads > 0 && n_q_heads % n_kv_heads == 0, AP_EPARAM, "bad head counts");
+    AP_REQUIRE(K > 0 && K % 8 == 0, AP_EPARAM, "K must be a multiple of 8 (16-byte rows)");
+    AP_REQUIRE(n_seq >= 1 && n_seq <= MAX_NS, AP_EPARAM, "ap_gemv serves 1..4 activation rows");
+    AP_REQUIRE((int64_t)n_seq * K * 2 <= 150 * 1024, AP_EPARAM, "activations exceed shared memory");
+    AP_REQUIRE((flags & ~1) == 0, AP_EPARAM, "only the RMSNORM prologue flag applies");
+    AP_REQUIRE(!(flags & 1) || ln_w, AP_EPARAM, "RMSNORM prologue needs ln_w");
+    AP_REQUIRE(!residual_out || (residual_out != residual && residual_out != x), AP_EPARAM,
+               "residual_out must not alias the residual or x");
+    Params P{};
+    P.W = (const __nv_bfloat16*)W;
+    P.x = (const __nv_bfloat16*)x;
+    P.residual = (const __nv_bfloat16*)residual;
+    P.residual_out = (__nv_bfloat16*)residual_out;
+    P.ln_w = (const __nv_bfloat16*)ln_w;
+    P.eps = eps;
+    P.y = (__nv_bfloat16*)y;
+    P.N = (n_q_heads + 2 * n_kv_heads) * 128;
+    P.K = K;
+    P.NS = n_seq;
+    P.seq_len = seq_len;
+    P.q_out = (__nv_bfloat16*)q_out;
+    P.k_cache = (__nv_bfloat16*)k_cache;
+    P.v_cache = (__nv_bfloat16*)v_cache;
+    P.Hq = n_q_heads;
+    P.Hkv = n_kv_heads;
+    P.t_max = t_max;
+    P.theta = theta;
+    cudaStream_t st = as_stream(stream);
+    if (flags & 1) return dispatch_ns<PRO_RMSNORM, EPI_ROPE>(P, st);
+    return dispatch_ns<PRO_NONE, EPI_ROPE>(P, st);
 }

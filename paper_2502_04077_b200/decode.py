@@ -222,12 +222,16 @@ class DecodeEngine:
         sh = self.shape
         S = self.n_seq
         s = _lib.stream_handle()
+        kc = self.k_cache[l]
+        vc = self.v_cache[l] if self.voff is None else self.voff.layer_view(l)
         if self.fused:  # residual stream ping-pong: qkv reads r2 and writes r, gate/up the reverse
-            if l == 0:
-                self._gemv(self.wqkv[l], self.r, self.qkv, GEMV_RMS, ln=self.ln1[0])
-            else:
-                self._gemv(self.wqkv[l], self.mlp, self.qkv, GEMV_RMS, residual=self.r2, residual_out=self.r,
-                           ln=self.ln1[l])
+            # projection + RoPE + KV append in one pass over the qkv weights
+            x_in, res, res_out = (self.r, None, None) if l == 0 else (self.mlp, self.r2, self.r)
+            _lib.check(_lib.fn("ap_gemv_qkv_rope")(
+                _lib.ptr(self.wqkv[l]), _lib.ptr(x_in), _lib.ptr(self.qkv), sh.n_q_heads, sh.n_kv_heads, sh.hidden,
+                S, GEMV_RMS, _lib.ptr(res), _lib.ptr(res_out), _lib.ptr(self.ln1[l]), sh.eps, _lib.ptr(self.seq_len),
+                _lib.ptr(self.q), _lib.ptr(kc), None if self.voff is not None else _lib.ptr(vc), self.t_max,
+                sh.rope_theta, s), "ap_gemv_qkv_rope")
         else:
             if l == 0:
                 _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.r), None, _lib.ptr(self.ln1[0]), _lib.ptr(self.y), S,
@@ -236,12 +240,10 @@ class DecodeEngine:
                 _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.ln1[l]),
                                                  _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
             torch.matmul(self.y, self.wqkv[l].t(), out=self.qkv)
-        kc = self.k_cache[l]
-        vc = self.v_cache[l] if self.voff is None else self.voff.layer_view(l)
-        _lib.check(_lib.fn("ap_rope_append")(_lib.ptr(self.qkv), S, sh.n_q_heads, sh.n_kv_heads,
-                                             _lib.ptr(self.seq_len), _lib.ptr(self.q), _lib.ptr(kc),
-                                             None if self.voff is not None else _lib.ptr(vc),
-                                             self.t_max, sh.rope_theta, s))
+            _lib.check(_lib.fn("ap_rope_append")(_lib.ptr(self.qkv), S, sh.n_q_heads, sh.n_kv_heads,
+                                                 _lib.ptr(self.seq_len), _lib.ptr(self.q), _lib.ptr(kc),
+                                                 None if self.voff is not None else _lib.ptr(vc),
+                                                 self.t_max, sh.rope_theta, s))
         if self.voff is not None:
             self.voff.append(self.qkv, sh.n_q_heads, self.seq_len, l)
             if variant in ("plain", "calib"):  # this layer's predicted V blocks must have arrived
@@ -423,7 +425,7 @@ class DecodeEngine:
     def kernels_per_step(self, variant: str) -> int:
         """Launches of libattnpred kernels in one step (the bench's gpu_launches claim)."""
         L = self.shape.n_layers
-        per_layer = 4 + 1 if self.fused else 2 + 1 + 1  # gemv x4 + rope | rmsnorm x2, rope_append, silu_mul
+        per_layer = 4 if self.fused else 2 + 1 + 1  # gemv x4 (qkv+rope fused) | rmsnorm x2, rope_append, silu_mul
         att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
         att_total = self.dense_layers + (L - self.dense_layers) * att
         sel = 2 if (self.sel is not None and variant != "dense") else 0

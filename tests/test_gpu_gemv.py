@@ -111,3 +111,40 @@ def test_fused_engine_matches_unfused():
     ok, err = _close(l1, l0)
     assert ok, err
     assert torch.equal(t1, torch.argmax(eng.logits, dim=-1))
+
+
+@pytest.mark.parametrize("ns", [1, 3])
+def test_qkv_rope_fused_matches_separate(ns):
+    """ap_gemv_qkv_rope == ap_gemv (RMSNORM prologue) followed by ap_rope_append, bit for bit."""
+    import torch
+    from paper_2502_04077_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(11 + ns)
+    Hq, Hkv, K, t_max = 8, 2, 1024, 64
+    N = (Hq + 2 * Hkv) * 128
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.03).bfloat16()
+    x = torch.randn(ns, K, device="cuda", generator=g).bfloat16()
+    r = torch.randn(ns, K, device="cuda", generator=g).bfloat16()
+    ln = (1 + 0.1 * torch.randn(K, device="cuda", generator=g)).bfloat16()
+    seq_len = torch.tensor([5, 17, 40, 63][:ns], dtype=torch.int32, device="cuda")
+    outs = []
+    for fused in (False, True):
+        y = torch.zeros(ns, N, device="cuda", dtype=torch.bfloat16)
+        q = torch.zeros(ns, Hq, 128, device="cuda", dtype=torch.bfloat16)
+        kc = torch.zeros(ns, Hkv, t_max, 128, device="cuda", dtype=torch.bfloat16)
+        vc = torch.zeros_like(kc)
+        r_out = torch.zeros_like(r)
+        if fused:
+            _lib.check(_lib.fn("ap_gemv_qkv_rope")(W.data_ptr(), x.data_ptr(), y.data_ptr(), Hq, Hkv, K, ns, RMS,
+                                                    r.data_ptr(), r_out.data_ptr(), ln.data_ptr(), 1e-5,
+                                                    seq_len.data_ptr(), q.data_ptr(), kc.data_ptr(), vc.data_ptr(),
+                                                    t_max, 500000.0, _lib.stream_handle()), "ap_gemv_qkv_rope")
+        else:
+            _call(W, x, y, ns, RMS, residual=r, residual_out=r_out, ln=ln)
+            _lib.check(_lib.fn("ap_rope_append")(y.data_ptr(), ns, Hq, Hkv, seq_len.data_ptr(), q.data_ptr(),
+                                                 kc.data_ptr(), vc.data_ptr(), t_max, 500000.0,
+                                                 _lib.stream_handle()), "ap_rope_append")
+        torch.cuda.synchronize()
+        outs.append((y, q, kc, vc, r_out))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    assert outs[0][2].abs().sum() > 0  # keys were appended
