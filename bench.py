@@ -100,17 +100,41 @@ def max_over_ranks(x: float, world: int) -> float:
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML every 5 ms (nvidia-smi as the
+    fallback, ~10 Hz)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    NVML_BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason{HwSlowdown, HwThermal, SwThermal, SwPowerCap}
 
     def __init__(self, gpu: int):
         self.gpu, self.rows, self._stop = gpu, [], threading.Event()
         self.t = threading.Thread(target=self._run, daemon=True)
+        self.source = "nvidia-smi"
+
+    def _run_nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        self.source = "nvml"
+        while not self._stop.is_set():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            try:
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:
+                rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self.rows.append([str(sm), str(mx), "-"] + ["Active" if rs & b else "Not Active" for b in self.NVML_BITS])
+            self._stop.wait(0.005)
 
     def _run(self):
+        try:
+            self._run_nvml()
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -119,10 +143,11 @@ class ClockSampler:
                     self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self.t.start()
+        time.sleep(0.02)  # first sample before the timed region starts
         return self
 
     def __exit__(self, *a):
@@ -131,13 +156,12 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 def measured_peak():
@@ -183,6 +207,32 @@ def cpu_oracle_rate(ctx: int, budget: int, n_map_steps: int, seed: int = 0):
     dt = (time.perf_counter() - t0) / n_map_steps
     cores = len(os.sched_getaffinity(0))
     return dt, cores
+
+
+# ---------------------------------------------------------------- whole-step HBM accounting
+def step_bytes(eng, variant: str) -> int:
+    """Algorithmic HBM bytes of one decode step: every weight matrix read once (projections, LM head),
+    the selected K/V blocks of every map (sparse), all of K and V (dense) or all of K on calibration
+    steps, the history-window reads of the forecaster."""
+    sh = eng.shape
+    S, L = eng.n_seq, sh.n_layers
+    hd = 128
+    w = sum(t.numel() * t.element_size() for t in (*eng.wqkv, *eng.wo, *eng.wgu, *eng.wdown, eng.lm_head))
+    t = eng.ctx_len
+    kv_dense = 2 * S * sh.n_kv_heads * t * hd * 2  # K + V of one layer
+    if variant == "dense":
+        return w + L * kv_dense
+    cfg = eng.sel.cfg
+    units = -(-cfg.sink_tokens // cfg.block_size) + cfg.local_tokens // cfg.block_size + 1 + cfg.middle_blocks
+    maps_layer = S * sh.n_q_heads // eng.group  # a KV-group map reads each selected K/V block once
+    kv_sparse = maps_layer * units * cfg.block_size * hd * 2 * 2
+    W = -(-t // cfg.block_size)
+    hist = eng.sel.n_maps * ((cfg.history + 1) * W * 4 + 4 * cfg.middle_blocks)
+    Ld = eng.dense_layers
+    b = w + Ld * kv_dense + (L - Ld) * kv_sparse + hist
+    if variant == "calib":
+        b += (L - Ld) * kv_dense // 2  # the K-only calibration pass
+    return b
 
 
 # ---------------------------------------------------------------- our arm
@@ -336,6 +386,12 @@ def run_ours(args, rank, world):
                     "note": "K resident (calibration reads all of K); V blocks predicted at step t are gathered "
                             "from pinned host memory on a side stream during step t+1, per layer"}
     launches = sum(eng.kernels_per_step(v) for v in variants)
+    peak, peak_kind = measured_peak()
+    sb = sum(step_bytes(eng, v) for v in variants) / len(variants)
+    step_hbm = {"bytes_per_step": int(sb), "achieved_GBps": round(sb * args.steps / elapsed / 1e9, 1), "peak": peak,
+                "frac": round(sb * args.steps / elapsed / 1e9 / peak, 4), "peak_kind": peak_kind,
+                "note": "algorithmic bytes of the whole decode step (weights once, selected KV, calibration K "
+                        "share, history window) over the device-timed step"}
     e2e = measure_e2e(eng, args.steps, args.batch, world, units)
     us, W = measure_selector(eng)
     roofline = roofline_for(eng, args, us, W, f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
@@ -387,7 +443,7 @@ def run_ours(args, rank, world):
                    "parallelism": f"replicas x{world}" if split is None else f"kv-head split x{world} + all-gather",
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
-        "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "step_hbm": step_hbm, "cpu_baseline": cpu,
         "alt_selection": alt, "prefetch": prefetch,
         "dense_tok_s": None if dense is None else round(dense, 2),
         "sparse_over_dense": None if dense is None else round(value / dense, 4),
