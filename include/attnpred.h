@@ -181,7 +181,7 @@ int ap_sel_grid_ctas(int precision);
  * seq_len[s] = number of keys the current query attends (t, incl. itself).
  * Workspaces: partial = n_seq*n_q_heads*n_splits*130 floats;
  * bmax = n_seq*n_q_heads*w_max floats, initialised to -inf once;
- * counters = n_seq*n_q_heads int32, zeroed once.  The split-K partials are
+ * counters = 2*n_seq*n_q_heads int32, zeroed once (split counters, then calibration LSE-ready epochs).  The split-K partials are
  * merged by the last CTA of each (sequence, head group) to finish — one
  * launch per call, no separate combine kernel.
  * ------------------------------------------------------------------------- */
@@ -195,7 +195,7 @@ typedef struct ap_attn_layer {
     float* lse;             /* [n_seq][n_q_heads] log2-domain LSE, may be NULL */
     float* partial;
     float* bmax;
-    int32_t* counters;      /* [n_seq][n_q_heads] zeroed once; split-completion counters */
+    int32_t* counters;      /* [2][n_seq][n_q_heads] zeroed once; split counters, calibration epochs */
 } ap_attn_layer;
 
 /* Dense decode attention over keys [0, t) (with_v = 1: output + LSE, the
@@ -204,6 +204,9 @@ typedef struct ap_attn_layer {
  * compressed dense row exp(blockmax - LSE) = max_pool(softmax row, b)
  * appended to the selector ring (selector.py:112-120).  K-only when
  * with_v = 0.  map(s, h) = s*maps_per_seq + map_base + h/group. */
+/* Kernel of the K-only calibration pass (ap_attn_dense with with_v == 0): 1 = TMA + tcgen05
+ * (default), 0 = the SIMT dense kernel.  Returns the previous mode.  Same outputs either way. */
+int ap_attn_set_calib_kernel(int mode);
 int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, int32_t map_base,
                   int32_t maps_per_seq, int32_t group, int emit, void* stream);
 

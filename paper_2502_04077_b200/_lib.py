@@ -112,6 +112,7 @@ SIGNATURES = {
     "ap_sel_grid_ctas": (ctypes.c_int, [ctypes.c_int]),
     "ap_attn_dense": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.c_int, ctypes.POINTER(Selector),
                                      _I32, _I32, _I32, ctypes.c_int, _P]),
+    "ap_attn_set_calib_kernel": (ctypes.c_int, [ctypes.c_int]),
     "ap_attn_sparse": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.POINTER(Selector), _I32, _I32, _I32,
                                       ctypes.c_int, _P]),
     "ap_prefetch": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.POINTER(VPages), _I32, _I32, _I32, _I32, _P]),

@@ -46,7 +46,8 @@ class DecodeAttention:
         self.partial = torch.empty(n_seq * n_q_heads * ns * (HEAD_DIM + 2), dtype=torch.float32, device=dev)
         self.bmax = torch.full((n_seq * n_q_heads * self.w_max,), float("-inf"), dtype=torch.float32, device=dev)
         self.lse = torch.empty(n_seq, n_q_heads, dtype=torch.float32, device=dev)
-        self.counters = torch.zeros(n_seq * n_q_heads, dtype=torch.int32, device=dev)
+        # split-completion counters, then the calibration pass's LSE-ready epochs
+        self.counters = torch.zeros(2 * n_seq * n_q_heads, dtype=torch.int32, device=dev)
 
     def _desc(self, q, k_cache, v_cache, seq_len, out, n_splits):
         return AttnLayerDesc(

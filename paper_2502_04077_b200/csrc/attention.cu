@@ -18,6 +18,9 @@
 // (token parity, 8-dim slice), 16-byte loads, half-warp shuffle reductions.
 // Flash-decoding split over blocks; a combine kernel merges the splits.
 #include <cooperative_groups.h>
+#include <cuda.h>  // CUtensorMap (driver types only; the encoder comes via cudaGetDriverEntryPoint)
+#include <cudaTypedefs.h>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -31,6 +34,8 @@ constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ long long g_att_trace[16 * 16];  // debug: clock64 per phase, CTAs (split, 0, 0)
 __device__ int g_att_trace_on;
+#define ATT_TRACE2(e) \
+    if (lane == 0 && blockIdx.y == 0 && blockIdx.z == 0 && g_att_trace_on && blockIdx.x < 16) g_att_trace[blockIdx.x * 16 + (e)] = clock64();
 #define ATT_TRACE(e) \
     if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && g_att_trace_on) g_att_trace[blockIdx.x * 16 + (e)] = clock64();
 
@@ -327,8 +332,32 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
                     const int64_t j = u < sb ? u : (u < sb + n_local ? lb + (u - sb) : mid[u - sb - n_local]);
                     emit_block(j);
                 }
-            } else {
-                for (int64_t j = threadIdx.x; j < W; j += ATT_THREADS) emit_block(j);
+            } else {  // every block: the bm loads of 8 blocks x all heads in flight at once
+                constexpr int U = 8;
+                for (int64_t base = threadIdx.x; base < W; base += (int64_t)ATT_THREADS * U) {
+                    float lg[U][8];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int hh = 0; hh < 8; ++hh) {
+                            const int64_t j = base + (int64_t)u * ATT_THREADS;
+                            lg[u][hh] = (hh < P.group && j < W) ? __ldcg(bm0 + hh * (int64_t)P.w_max + j) : -INFINITY;
+                        }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int64_t j = base + (int64_t)u * ATT_THREADS;
+                        if (j >= W) break;
+                        float v = 0.f;
+#pragma unroll
+                        for (int hh = 0; hh < 8; ++hh)
+                            if (hh < P.group) {
+                                if (lg[u][hh] != -INFINITY) v = fmaxf(v, exp2f(lg[u][hh] - s_lse[g0 + hh]));
+                                bm0[hh * (int64_t)P.w_max + j] = -INFINITY;  // untouched marker for the next step
+                            }
+                        dst[j] = v;
+                        mx = track_row_max(mx, v, P.sel.status);
+                    }
+                }
             }
             const int old_w = P.sel.slot_width[(int64_t)map * Hh + slot];
             for (int64_t j = W + threadIdx.x; j < old_w; j += ATT_THREADS) dst[j] = 0.f;  // zero beyond W
@@ -763,11 +792,372 @@ static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t m
     return AP_OK;
 }
 
+
+// ------------------------------------------------------------------ calibration pass on tcgen05
+// The K-only dense pass of calibration steps (every M-th step reads all of K: 64 MiB per layer at
+// 32K for LLaMA-3.1-8B) as a TMA + tensor-core stream.  Per 128-token tile: two TMA boxes
+// {64 dims, 128 tokens} land the K rows in the 128-byte-swizzled K-major layout tcgen05 reads
+// directly; one thread issues 8 MMAs (M = 128 tokens, N = 16 (the NH q-heads of this KV head,
+// zero-padded), K = 16 dims each, bf16 x bf16 -> fp32 in TMEM); four epilogue warps (lane =
+// token) read the tile's logits, scale them to log2 units, take each 16-token block's max per head
+// (the calibration row's compressed value is exp2(blockmax - LSE), by monotonicity) and fold the
+// tokens into a per-thread online log-sum-exp.  Splits meet in the same last-CTA-done combine and
+// emission as the SIMT dense kernel (combine_heads), so the outputs have the same layout and
+// meaning.  Roles: warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue (warps 6-7 only
+// join the combine).
+namespace ctc {
+
+constexpr int TILE = 128, NST = 4, NACC = 4, NCOL = 16;
+constexpr int STAGE_BYTES = TILE * HD * 2;  // 32 KB: two 16 KB swizzled boxes (dims 0-63 | 64-127)
+constexpr int B_BYTES = 2 * NCOL * 128;     // q: two 64-dim atoms x 16 rows x 128 B
+
+struct Smem {
+    static constexpr int off_a = 0;                          // [NST] stages, 1024-aligned
+    static constexpr int off_b = off_a + NST * STAGE_BYTES;  // q (B operand)
+    static constexpr int off_red = off_b + B_BYTES;          // [4 warps][8 heads][2]
+    static constexpr int off_lse = off_red + 4 * 8 * 2 * 4;  // [8] LSE per head (log2 units)
+    static constexpr int off_bar = off_lse + 8 * 4;
+    static constexpr int off_bm = off_bar + 8 * (2 * NST + 2 * NACC) + 16;  // [NH][tiles * 8] block maxima
+    static int total(int nh, int max_tiles) { return off_bm + nh * max_tiles * (TILE / 16) * 4 + 1024; }
+};
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;                      // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;            // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                      // descriptor version (Blackwell)
+    d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// grid (n_splits, Hkv, S), one wave (every CTA resident; the splits of a KV head wait for each other
+// once, for the LSE); 256 threads.  P.counters[s * Hq + h0]: split arrivals (self-resetting);
+// P.counters[S * Hq + s * Hq + h0]: LSE-ready epoch (= the map's n_pushed + 1 of this step).
+template <int NH>
+__global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                                  AttnParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::off_bar);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + NST;
+    uint64_t* acc_full = bars + 2 * NST;
+    uint64_t* acc_empty = acc_full + NACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
+    float* red = reinterpret_cast<float*>(smem + Smem::off_red);
+    float* s_lse = reinterpret_cast<float*>(smem + Smem::off_lse);
+    float* s_bm = reinterpret_cast<float*>(smem + Smem::off_bm);
+    const int split = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h0 = kvh * NH;
+    ATT_TRACE(0);
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < NACC; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 4);
+        }
+    }
+    if (warp == 0) tmem_alloc(tmem_slot, NACC * NCOL);
+    // this step's map states (read before this CTA counts itself in, so before any update)
+    const int Hh = P.sel.history;
+    int64_t epoch = 0;
+    pdl_wait();  // q and the newest K token come from earlier kernels in the stream
+    {
+        const int map0 = s * P.maps_per_seq + P.map_base + h0 / P.group;
+        epoch = P.sel.state[map0].n_pushed + 1;
+    }
+    const int64_t t = P.seq_len[s];
+    const int n_tiles = (int)((t + TILE - 1) / TILE);
+    const int tile0 = (int)((int64_t)split * n_tiles / gridDim.x), tile1 = (int)((int64_t)(split + 1) * n_tiles / gridDim.x);
+    const int my_blocks = (tile1 - tile0) * (TILE / 16);
+    {  // q of this KV head's NH q-heads -> the swizzled B tile (rows >= NH zero)
+        __nv_bfloat16* bq = reinterpret_cast<__nv_bfloat16*>(smem + Smem::off_b);
+        for (int i = threadIdx.x; i < NCOL * HD; i += ATT_THREADS) {
+            const int n = i / HD, d = i % HD;
+            const __nv_bfloat16 v = n < NH ? P.q[((int64_t)s * P.n_q_heads + h0 + n) * HD + d] : __float2bfloat16_rn(0.f);
+            const int atom = d >> 6, dd = d & 63;
+            const int byte = atom * (NCOL * 128) + n * 128 + ((((dd >> 3) ^ (n & 7))) << 4) + (dd & 7) * 2;
+            bq[byte >> 1] = v;
+        }
+    }
+    fence_async_smem();  // the generic-proxy q writes -> visible to the tensor core
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    ATT_TRACE(1);
+    const int64_t row0 = ((int64_t)s * P.n_kv_heads + kvh) * P.t_max;  // tensor-map row of token 0
+
+    if (warp == 0) {
+        // ---------------------------------------------------------- TMA producer
+        if (lane == 0)
+            for (int i = 0, tl = tile0; tl < tile1; ++i, ++tl) {
+                const int st = i % NST;
+                if (i >= NST) mbar_wait(&empty[st], ((i / NST) & 1) ^ 1);
+                uint8_t* dst = smem + Smem::off_a + st * STAGE_BYTES;
+                mbar_arrive_tx(&full[st], STAGE_BYTES);
+                tma_load_2d(dst, &kmap, 0, (int)(row0 + (int64_t)tl * TILE), &full[st]);
+                tma_load_2d(dst + STAGE_BYTES / 2, &kmap, 64, (int)(row0 + (int64_t)tl * TILE), &full[st]);
+            }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_f16_f32(TILE, NCOL, 1);  // bf16 x bf16 -> fp32
+            const uint32_t b_addr = smem_u32(smem + Smem::off_b);
+            for (int i = 0, tl = tile0; tl < tile1; ++i, ++tl) {
+                const int st = i % NST, ab = i % NACC;
+                mbar_wait(&full[st], (i / NST) & 1);
+                mbar_wait(&acc_empty[ab], ((i / NACC) & 1) ^ 1);  // (first use: free)
+                tc_fence_after();
+                const uint32_t a_addr = smem_u32(smem + Smem::off_a + st * STAGE_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t ka = a_addr + (kk >> 2) * (STAGE_BYTES / 2) + (kk & 3) * 32;
+                    const uint32_t kb = b_addr + (kk >> 2) * (NCOL * 128) + (kk & 3) * 32;
+                    mma_f16(tmem_base + ab * NCOL, desc_sw128(ka), desc_sw128(kb), idesc, kk > 0);
+                }
+                mma_commit(&empty[st]);      // K tile consumed
+                mma_commit(&acc_full[ab]);   // logits ready
+            }
+        }
+    } else if (warp < 6) {
+        // ---------------------------------------------------------- epilogue (lane = token of the tile)
+        const int quad = warp & 3;
+        const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
+        const float qscale = LOG2E * rsqrtf((float)HD);
+        float m[NH], l[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) { m[h] = -INFINITY; l[h] = 0.f; }
+        for (int i = 0, tl = tile0; tl < tile1; ++i, ++tl) {
+            const int ab = i % NACC;
+            mbar_wait(&acc_full[ab], (i / NACC) & 1);
+            tc_fence_after();
+            float v[8];
+            tmem_ld8(lane_base + ab * NCOL, v);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+            const int64_t p = (int64_t)tl * TILE + quad * 32 + lane;
+            const int jb = i * (TILE / 16) + quad * 2 + (lane >> 4);  // this CTA's block index
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                const float lg = p < t ? v[h] * qscale : -INFINITY;
+                float bmx = lg;
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, o));
+                if ((lane & 15) == 0) s_bm[h * my_blocks + jb] = bmx;
+                if (lg != -INFINITY) {
+                    const float mn = fmaxf(m[h], lg);
+                    l[h] = l[h] * exp2f(m[h] - mn) + exp2f(lg - mn);
+                    m[h] = mn;
+                }
+            }
+        }
+        // (m, l) of the split: over the 32 lanes, then the 4 warps
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            float M = m[h];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            float L = (m[h] == -INFINITY) ? 0.f : l[h] * exp2f(m[h] - M);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+            if (lane == 0) {
+                red[(quad * 8 + h) * 2 + 0] = M;
+                red[(quad * 8 + h) * 2 + 1] = L;
+            }
+        }
+    }
+    ATT_TRACE(2);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem_base, NACC * NCOL);
+    if (threadIdx.x < NH) {
+        const int h = threadIdx.x;
+        float M = -INFINITY;
+        for (int q = 0; q < 4; ++q) M = fmaxf(M, red[(q * 8 + h) * 2]);
+        float L = 0.f;
+        for (int q = 0; q < 4; ++q) {
+            const float mq = red[(q * 8 + h) * 2];
+            if (mq != -INFINITY) L += red[(q * 8 + h) * 2 + 1] * exp2f(mq - M);
+        }
+        float* part = P.partial + (((int64_t)s * P.n_q_heads + h0 + h) * P.n_splits + split) * (HD + 2);
+        part[0] = M;
+        part[1] = L;
+    }
+    // ---- the last split of this KV head combines the (m, l) into the LSE and publishes it
+    volatile int32_t* ready = P.counters + (int64_t)P.n_seq * P.n_q_heads + (int64_t)s * P.n_q_heads + h0;
+    const int64_t W = (t + P.block - 1) / P.block;
+    ATT_TRACE(7);
+    if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) {
+        ATT_TRACE(8);
+        if (warp < NH) {  // warp h: lane = split (one round trip for all partials)
+            const int h = warp;
+            const float* part = P.partial + ((int64_t)s * P.n_q_heads + h0 + h) * P.n_splits * (HD + 2);
+            const float ms = lane < P.n_splits ? __ldcg(part + lane * (HD + 2)) : -INFINITY;
+            const float ls = lane < P.n_splits ? __ldcg(part + lane * (HD + 2) + 1) : 0.f;
+            float M = ms;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            float L = (ms == -INFINITY) ? 0.f : ls * exp2f(ms - M);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+            if (lane == 0) {
+                const float lse = M + log2f(L);
+                if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = lse;
+                P.partial[((int64_t)s * P.n_q_heads + h0 + h) * P.n_splits * (HD + 2) + 2] = lse;
+            }
+        }
+        if (threadIdx.x < NH / P.group + (NH % P.group != 0)) {  // per map: the row max starts from 0
+            const int map = s * P.maps_per_seq + P.map_base + (h0 + threadIdx.x * P.group) / P.group;
+            P.sel.slot_xmax[(int64_t)map * Hh + (int)((epoch - 1) % Hh)] = 0.f;
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicExch((int32_t*)ready, (int32_t)epoch);
+        ATT_TRACE(9);
+        for (int g0 = 0; g0 < NH; g0 += P.group) {  // zero the ring row beyond W (rarely any)
+            const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;
+            const int slot = (int)((epoch - 1) % Hh);
+            float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
+            const int old_w = P.sel.slot_width[(int64_t)map * Hh + slot];
+            for (int64_t j = W + threadIdx.x; j < old_w; j += ATT_THREADS) dst[j] = 0.f;
+        }
+    }
+    // ---- every split emits the compressed-row values of its own blocks once the LSE is out
+    if (threadIdx.x == 0)
+        while (*ready != (int32_t)epoch) __nanosleep(64);
+    __syncthreads();
+    __threadfence();
+    ATT_TRACE(4);
+    if (threadIdx.x < NH)
+        s_lse[threadIdx.x] = __ldcg(P.partial + ((int64_t)s * P.n_q_heads + h0 + threadIdx.x) * P.n_splits * (HD + 2) + 2);
+    __syncthreads();
+    for (int g0 = 0; g0 < NH; g0 += P.group) {
+        const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;
+        const int slot = (int)((epoch - 1) % Hh);
+        float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
+        float mx = 0.f;
+        const int64_t jbase = (int64_t)tile0 * (TILE / 16);
+        for (int jb = threadIdx.x; jb < my_blocks; jb += ATT_THREADS) {
+            const int64_t j = jbase + jb;
+            if (j >= W) break;
+            float v = 0.f;
+            for (int hh = 0; hh < P.group; ++hh) {
+                const float lg = s_bm[(g0 + hh) * my_blocks + jb];
+                if (lg != -INFINITY) v = fmaxf(v, exp2f(lg - s_lse[g0 + hh]));
+            }
+            dst[j] = v;
+            mx = track_row_max(mx, v, P.sel.status);
+        }
+        mx = cta_max_nonneg(mx);
+        if (threadIdx.x == 0)
+            atomicMax(reinterpret_cast<int*>(P.sel.slot_xmax + (int64_t)map * Hh + slot), __float_as_int(mx));
+    }
+    ATT_TRACE(5);
+    // ---- map state: the last CTA to finish emitting advances it (everyone has read the old one)
+    __syncthreads();
+    if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) {
+        if (threadIdx.x == 0) *ready = 0;  // every split is past its wait: no stale epoch can match later
+        if (threadIdx.x == 0)
+            for (int g0 = 0; g0 < NH; g0 += P.group) {
+                const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;
+                const int slot = (int)((epoch - 1) % Hh);
+                ap_map_state st = P.sel.state[map];
+                P.sel.slot_width[(int64_t)map * Hh + slot] = (int32_t)W;
+                st.n_pushed += 1;
+                st.row_len = t;
+                st.width = (int32_t)W;
+                P.sel.state[map] = st;
+            }
+    }
+    ATT_TRACE(6);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+template <int NH>
+static int launch(AttnParams P, cudaStream_t st) {
+    auto enc = encoder();
+    AP_REQUIRE(enc != nullptr, AP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)P.n_seq * P.n_kv_heads * P.t_max};
+    const cuuint64_t strides[1] = {(cuuint64_t)HD * 2};
+    const cuuint32_t box[2] = {64, TILE}, estr[2] = {1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(P.k), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    AP_REQUIRE(r == CUDA_SUCCESS, AP_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    auto k = calib_tc_kernel<NH>;
+    // splits: one wave of one CTA per SM over the whole (KV head, sequence) grid (the splits of a KV
+    // head wait for each other once, so they must all be resident)
+    int splits = ap_device_sm_count() / (P.n_kv_heads * P.n_seq);
+    AP_REQUIRE(splits >= 1, AP_EPARAM, "calibration pass: more (sequence, KV head) pairs than SMs");
+    splits = splits > P.n_splits ? P.n_splits : splits;
+    P.n_splits = splits;
+    const int max_tiles = (P.t_max / TILE + 1 + splits - 1) / splits + 1;
+    const int smem = Smem::total(NH, max_tiles);
+    AP_REQUIRE(smem <= 227 * 1024, AP_EPARAM, "calibration pass: t_max too large for the block-max buffer");
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    launch_ex(k, dim3(splits, P.n_kv_heads, P.n_seq), dim3(ATT_THREADS), (size_t)smem, st, 1, map, P);
+    return launch_status("calib_tc_kernel");
+}
+
+}  // namespace ctc
+
 }  // namespace ap
 
 using namespace ap;
 
+static int g_calib_mode = -1;  // 1: TMA + tcgen05 calibration pass, 0: SIMT dense kernel
+static bool calib_tc_enabled() {
+    if (g_calib_mode < 0) {
+        const char* e = getenv("ATTNPRED_CALIB_KERNEL");
+        g_calib_mode = !(e && strcmp(e, "simt") == 0);
+    }
+    return g_calib_mode == 1;
+}
+
 extern "C" {
+
+int ap_attn_set_calib_kernel(int mode) {
+    const int prev = calib_tc_enabled() ? 1 : 0;
+    g_calib_mode = mode ? 1 : 0;
+    return prev;
+}
 
 int ap_attn_debug_trace(int on, long long* host_out) {
     if (host_out) return cudaMemcpyFromSymbol(host_out, g_att_trace, sizeof(long long) * 256) == cudaSuccess ? 0 : 5;
@@ -784,6 +1174,14 @@ int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, in
     AP_REQUIRE(!emit || sel, AP_EPARAM, "emit needs a selector");
     cudaStream_t st = as_stream(stream);
     const int G = a->n_q_heads / a->n_kv_heads;
+    if (!with_v && calib_tc_enabled()) {  // calibration pass: TMA + tcgen05 (ATTNPRED_CALIB_KERNEL=simt: SIMT)
+        switch (G) {
+            case 1: return ctc::launch<1>(P, st);
+            case 2: return ctc::launch<2>(P, st);
+            case 4: return ctc::launch<4>(P, st);
+            default: return ctc::launch<8>(P, st);
+        }
+    }
     switch (G) {
         case 1: launch_dense<1>(P, with_v, emit, st); break;
         case 2: launch_dense<2>(P, with_v, emit, st); break;

@@ -172,3 +172,50 @@ def test_sparse_with_full_selection_equals_dense(splits):
     att.sparse(qd, kd, vd, seq_len, o2, sel, emit=False)
     torch.cuda.synchronize()
     assert torch.allclose(o1.float(), o2.float(), atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("kernel", [1, 0])  # 1: TMA + tcgen05 calibration pass, 0: SIMT dense kernel
+@pytest.mark.parametrize("group", [1, 4])
+def test_calibration_pass_k_only(group, kernel):
+    """ap_attn_dense(with_v=0, emit) — the K-only pass of calibration steps — against the float64
+    oracle: LSE and the compressed calibration row max_pool(softmax row) pushed into the ring; two
+    consecutive steps (ring slot, per-step synchronisation state and map state advance)."""
+    import torch
+    from paper_2502_04077_b200 import _lib
+    from paper_2502_04077_b200.attention import DecodeAttention
+    S, Hq, Hkv, t_max = 2, 8, 2, 2048
+    q, k, _ = _setup(S, Hq, Hkv, t_max, seed=5)
+    maps = Hq // group
+    sel = _selector(S * maps, t_max // 16)
+    att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_dense=32)
+    kd = k.cuda()
+    prev = _lib.fn("ap_attn_set_calib_kernel")(kernel)
+    try:
+        for step, lens in enumerate(([700, 2039], [701, 1300])):
+            qs = q if step == 0 else (q.float() * -0.7).to(torch.bfloat16)
+            seq_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+            att.dense(qs.cuda(), kd, kd, seq_len, None, with_v=False, emit=True, selector=sel, map_base=0,
+                      maps_per_seq=maps, group=group)
+            torch.cuda.synchronize()
+            lse2 = att.lse.cpu().numpy()
+            ring = sel.ring.cpu().numpy()
+            for s in range(S):
+                t = lens[s]
+                rows = []
+                for h in range(Hq):
+                    K = _f64(k[s, h // (Hq // Hkv), :t])
+                    _, lse, p = A.dense_decode(_f64(qs[s, h]), K, K)
+                    assert abs(lse2[s, h] * LN2 - lse) <= 1e-3, (step, s, h)
+                    rows.append(O.max_pool(p, 16))
+                for g in range(maps):
+                    want = np.max(rows[g * group:(g + 1) * group], axis=0)
+                    got = ring[s * maps + g, step, :]
+                    assert np.allclose(got[: want.size], want, rtol=1e-3, atol=1e-7 * want.max()), (step, s, g)
+                    assert not got[want.size:].any()  # zero beyond the row's width
+            st = sel.states()
+            assert (st["n_pushed"] == step + 1).all()
+            assert list(st["row_len"][::maps]) == lens
+            xmax = sel.slot_xmax.cpu().numpy()[:, step]
+            assert np.allclose(xmax, ring[:, step, :].max(axis=1))
+    finally:
+        _lib.fn("ap_attn_set_calib_kernel")(prev)
