@@ -604,7 +604,19 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
 }  // namespace ap
 #include "forecast_ws.cuh"
 #include "forecast_ts.cuh"
+#include "forecast_wsm.cuh"
 namespace ap {
+
+template <int PREC>
+static int grid_ctas_wsm() {
+    static int cached = 0;
+    if (!cached) {
+        cudaFuncSetAttribute(wsm::conv_forecast_wsm_kernel<PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             wsm::Smem::total);
+        cached = ap_device_sm_count();  // one 16-warp CTA (and all 512 TMEM columns) per SM
+    }
+    return cached;
+}
 
 template <int PREC>
 static int grid_ctas_ts() {
@@ -653,14 +665,14 @@ static int grid_ctas() {
     return cached;
 }
 
-// Tensor-core forecaster variant: 1 = shared-memory-operand warp-specialised kernel (default),
-// 2 = register-fed TS kernel (ATTNPRED_FORECAST_KERNEL=ts; measured 10% slower),
-// 0 = single-role band kernel (=bands); the alternatives stay for A/B measurements.
+// Tensor-core forecaster variant: 3 = merged-band warp-specialised kernel (default), 1 = one band
+// per segment (ATTNPRED_FORECAST_KERNEL=ws), 2 = register-fed TS kernel (=ts), 0 = single-role band
+// kernel (=bands); the alternatives stay for A/B measurements.
 static int tc_kernel() {
     static int v = -1;
     if (v < 0) {
         const char* e = getenv("ATTNPRED_FORECAST_KERNEL");
-        v = (e && strcmp(e, "bands") == 0) ? 0 : (e && strcmp(e, "ts") == 0) ? 2 : 1;
+        v = (e && strcmp(e, "bands") == 0) ? 0 : (e && strcmp(e, "ts") == 0) ? 2 : (e && strcmp(e, "ws") == 0) ? 1 : 3;
     }
     return v;
 }
@@ -684,7 +696,10 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
             break;
         }
         case AP_PREC_F16X3: {
-            if (P.pitch % 4 == 0 && tc_kernel() == 2) {
+            if (P.pitch % 4 == 0 && tc_kernel() == 3) {
+                int g = grid_ctas_wsm<AP_PREC_F16X3>();
+                wsm::conv_forecast_wsm_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, wsm::NT, wsm::Smem::total, st>>>(P);
+            } else if (P.pitch % 4 == 0 && tc_kernel() == 2) {
                 int g = grid_ctas_ts<AP_PREC_F16X3>();
                 ts::conv_forecast_ts_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, ts::NT, ts::Smem::total, st>>>(P);
             } else if (P.pitch % 4 == 0 && tc_kernel() == 1) {
@@ -697,7 +712,10 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
             break;
         }
         case AP_PREC_F16: {
-            if (P.pitch % 4 == 0 && tc_kernel() == 2) {
+            if (P.pitch % 4 == 0 && tc_kernel() == 3) {
+                int g = grid_ctas_wsm<AP_PREC_F16>();
+                wsm::conv_forecast_wsm_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, wsm::NT, wsm::Smem::total, st>>>(P);
+            } else if (P.pitch % 4 == 0 && tc_kernel() == 2) {
                 int g = grid_ctas_ts<AP_PREC_F16>();
                 ts::conv_forecast_ts_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, ts::NT, ts::Smem::total, st>>>(P);
             } else if (P.pitch % 4 == 0 && tc_kernel() == 1) {
@@ -801,9 +819,11 @@ int ap_debug_prof(unsigned long long* host_out, int n) {
 }
 
 int ap_debug_trace(long long* host_out) {
-    const bool ts = tc_kernel() == 2;
-    return (ts ? cudaMemcpyFromSymbol(host_out, ts::g_trace, sizeof(long long) * 64 * 8)
-               : cudaMemcpyFromSymbol(host_out, ws::g_trace, sizeof(long long) * 64 * 8)) == cudaSuccess ? AP_OK : AP_ECUDA;
+    const int k = tc_kernel();
+    const cudaError_t e = k == 2   ? cudaMemcpyFromSymbol(host_out, ts::g_trace, sizeof(long long) * 64 * 8)
+                          : k == 3 ? cudaMemcpyFromSymbol(host_out, wsm::g_trace, sizeof(long long) * 64 * 8)
+                                   : cudaMemcpyFromSymbol(host_out, ws::g_trace, sizeof(long long) * 64 * 8);
+    return e == cudaSuccess ? AP_OK : AP_ECUDA;
 }
 
 int ap_sel_grid_ctas(int precision) {

@@ -10,7 +10,7 @@ buf = (ctypes.c_longlong * 512)()
 _lib.load().ap_debug_trace(buf)
 a = np.array(buf, dtype=np.int64).reshape(64, 8)
 t0 = a[0][a[0] > 0].min()
-names = ["prod_issued", "conv_last_warp_done", "conv_start", "conv_w0_done", "mma_start", "mma_issued", "epi_start", "epi_end"]
+names = ["prod_issued", "conv_w0_begin", "conv_start", "conv_w0_done", "mma_start", "mma_issued", "epi_start", "epi_end"]
 print("band " + " ".join(f"{n:>20s}" for n in names))
 for b in range(40):
     print(f"{b:4d} " + " ".join(f"{(v - t0) if v else -1:20d}" for v in a[b]))
