@@ -203,8 +203,141 @@ __global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s) {
     }
 }
 
+
+// Register-resident variant for rows of <= NT * IPT blocks (the usual case: W = 2048 at 32K): thread
+// t owns blocks [t * IPT, t * IPT + IPT), loaded once; the radix passes and the ordered emission run
+// on registers (the generic kernel re-reads the row from global memory on every pass).
+template <int NT, int IPT>
+__global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s) {
+    __shared__ int hist[256];
+    __shared__ int scan_tmp[NT / 32 + 2];
+    __shared__ int s_nan;
+    const int m = blockIdx.x;
+    ap_map_state st = s.state[m];
+    const bool update = (st.counter % s.update_interval) == 0;
+    const int words = (s.w_max + 31) / 32;
+    uint32_t* mask = s.mid_mask + (int64_t)m * words;
+    int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
+    if (threadIdx.x == 0) s_nan = 0;
+    __syncthreads();
+    int count = st.n_mid;
+    if (update && s.k_mid > 0 && st.width > 0) {
+        const int W = st.width;
+        const int b = s.block;
+        const int64_t t = st.row_len;
+        const int64_t nl = t + 1;
+        // covering blocks of sink [0, min(sink, nl)) and local [max(0, nl-local), nl) — selector.py:84-88,134-142
+        const int64_t sink_end = s.sink < nl ? s.sink : nl;
+        int sink_hi = sink_end > 0 ? (int)cdiv64(sink_end, b) : 0;
+        const int64_t ls = nl - s.local > 0 ? nl - s.local : 0;
+        const int local_lo = ls < nl ? (int)(ls / b) : 0;
+        int local_hi = ls < nl ? (int)cdiv64(nl, b) : 0;
+        sink_hi = sink_hi > W ? W : sink_hi;
+        local_hi = local_hi > W ? W : local_hi;
+        const float* sc = s.scores + (int64_t)m * s.w_max;
+        const int i0 = threadIdx.x * IPT;
+        uint32_t key[IPT];
+        int n_masked_local = 0;
+        bool nan = false;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+            const int i = i0 + q;
+            const float v = i < W ? sc[i] : -INFINITY;
+            nan |= v != v;
+            const bool masked = i >= W || (i < sink_hi) || (i >= local_lo && i < local_hi);
+            key[q] = masked ? 0u : order_key(v);  // 0 sorts below every real key (and is never taken)
+            n_masked_local += i < W && (masked || v == -INFINITY);
+        }
+        if (nan) s_nan = 1;
+        int n_masked = 0;
+        block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
+        if (s_nan) raise_status(s.status, AP_ENUMERIC);
+        const int available = W - n_masked;
+        const int k = s.k_mid < available ? s.k_mid : available;
+        for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
+        if (k > 0) {
+            // radix select of the k-th largest key, 8 bits per pass
+            uint32_t prefix = 0, hi_mask = 0;
+            int remaining = k;
+#pragma unroll 1
+            for (int pass = 3; pass >= 0; --pass) {
+                const int shift = pass * 8;
+                for (int d = threadIdx.x; d < 256; d += NT) hist[d] = 0;
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < IPT; ++q)
+                    if (((key[q] ^ prefix) & hi_mask) == 0) atomicAdd(&hist[(key[q] >> shift) & 0xFF], 1);
+                __syncthreads();
+                const int c = threadIdx.x < 256 ? hist[255 - threadIdx.x] : 0;
+                int total = 0;
+                const int excl = block_excl_scan<NT>(c, scan_tmp, total);
+                if (threadIdx.x < 256 && excl < remaining && excl + c >= remaining) {
+                    scan_tmp[NT / 32] = 255 - threadIdx.x;
+                    scan_tmp[NT / 32 + 1] = excl;
+                }
+                __syncthreads();
+                const int digit = scan_tmp[NT / 32];
+                remaining -= scan_tmp[NT / 32 + 1];
+                prefix |= (uint32_t)digit << shift;
+                hi_mask |= 0xFFu << shift;
+                __syncthreads();
+            }
+            const uint32_t T = prefix;
+            const int take_eq = remaining;
+            // ordered emission: keys > T and the lowest-index take_eq keys == T, ascending
+            int n_eq = 0;
+#pragma unroll
+            for (int q = 0; q < IPT; ++q) n_eq += key[q] == T;
+            int tot = 0;
+            const int eq_base = block_excl_scan<NT>(n_eq, scan_tmp, tot);
+            int n_sel = 0, eq_rank = eq_base;
+#pragma unroll
+            for (int q = 0; q < IPT; ++q) {
+                if (key[q] > T) ++n_sel;
+                else if (key[q] == T) { n_sel += eq_rank < take_eq; ++eq_rank; }
+            }
+            int total = 0;
+            int pos = block_excl_scan<NT>(n_sel, scan_tmp, total);
+            eq_rank = eq_base;
+            uint32_t bits[(IPT + 31) / 32 + 1] = {};  // this thread's ids span IPT / 32 (+1) mask words
+#pragma unroll
+            for (int q = 0; q < IPT; ++q) {
+                bool take = false;
+                if (key[q] > T) take = true;
+                else if (key[q] == T) { take = eq_rank < take_eq; ++eq_rank; }
+                if (take) {
+                    mid[pos++] = i0 + q;
+                    bits[((i0 + q) >> 5) - (i0 >> 5)] |= 1u << ((i0 + q) & 31);
+                }
+            }
+            __syncthreads();  // the mask words were cleared above by other threads
+#pragma unroll
+            for (int wq = 0; wq < (IPT + 31) / 32 + 1; ++wq)
+                if (bits[wq]) atomicOr(&mask[(i0 >> 5) + wq], bits[wq]);
+            count = total;
+        } else {
+            count = 0;
+        }
+        if (threadIdx.x == 0) {
+            st.n_mid = count;
+            st.mid_clip = t;
+            st.r_pushed = st.n_pushed;
+            st.r_width = st.width;
+        }
+    } else if (update && s.k_mid <= 0) {
+        for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
+        if (threadIdx.x == 0) st.n_mid = 0;
+    }
+    if (threadIdx.x == 0) {
+        st.counter += 1;
+        s.state[m] = st;
+    }
+}
+
 void launch_sel_topk(const ap_selector& s, cudaStream_t stream) {
-    sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s);
+    if (s.w_max <= 256 * 8) sel_topk_reg_kernel<256, 8><<<s.n_maps, 256, 0, stream>>>(s);
+    else if (s.w_max <= 256 * 16) sel_topk_reg_kernel<256, 16><<<s.n_maps, 256, 0, stream>>>(s);
+    else sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s);
 }
 
 }  // namespace ap
