@@ -459,12 +459,18 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                 const float* rm = P.rmap + (int64_t)m.map * P.map_stride + col;
                 if (P.rsum) g_S = P.rsum[(int64_t)m.map * P.pitch + col];
                 const int n_old = 2 + H - m.lo2;  // positions {0, 1} ∪ [lo2, H)
-                for (int k = 0; k < n_old; ++k) {
+                auto old_r = [&](int k) {
                     const int pp = k < 2 ? k : m.lo2 + k - 2;
                     int sl = sel ? m.base_slot + pp : pp;
                     sl = sl >= H ? sl - H : sl;
-                    g_os += rm[(int64_t)sl * P.pitch];
-                }
+                    return rm[(int64_t)sl * P.pitch];
+                };
+                float ov[8];  // all loads in flight before the first use
+#pragma unroll
+                for (int k = 0; k < 8; ++k) ov[k] = k < n_old ? old_r(k) : 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) g_os += ov[k];
+                for (int k = 8; k < n_old; ++k) g_os += old_r(k);
             }
             if (b >= NA) mbar_wait(&a1_empty[a], ((b / NA) & 1) ^ 1);
             if (ct == 0) WSM_TRACE(b, 2);
