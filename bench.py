@@ -147,12 +147,18 @@ class ClockSampler:
 
     def __enter__(self):
         self.t.start()
-        time.sleep(0.02)  # first sample before the timed region starts
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 5.0:  # sampler running before the timed region starts
+            time.sleep(0.005)
+        self._n0 = len(self.rows)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self.t.join(timeout=10)
+        # keep the samples taken inside the timed region (plus the one just before it, if that is all)
+        inside = self.rows[self._n0:]
+        self.rows = inside if inside else self.rows[-1:]
 
     def summary(self):
         if not self.rows:
