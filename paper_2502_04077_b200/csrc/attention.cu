@@ -545,20 +545,23 @@ __device__ void merge_warps_to_smem(WarpState<NH, true>& st, float* scratch, flo
         }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < NH * (HD + 2); idx += ATT_THREADS) {
-        const int h = idx / (HD + 2), e = idx % (HD + 2);
+    // per head: the CTA max and each warp's rescale factor, once
+    __shared__ float s_scale[NH][ATT_WARPS];
+    if (threadIdx.x < NH * ATT_WARPS) {
+        const int h = threadIdx.x / ATT_WARPS, ww = threadIdx.x % ATT_WARPS;
         float M = -INFINITY;
-        for (int ww = 0; ww < ATT_WARPS; ++ww) M = fmaxf(M, scratch[(ww * NH + h) * (HD + 2)]);
+#pragma unroll
+        for (int v = 0; v < ATT_WARPS; ++v) M = fmaxf(M, scratch[(v * NH + h) * (HD + 2)]);
+        const float mw = scratch[(ww * NH + h) * (HD + 2)];
+        s_scale[h][ww] = mw == -INFINITY ? 0.f : exp2f(mw - M);
+        if (ww == 0) cpart[h][0] = M;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < NH * (HD + 1); idx += ATT_THREADS) {
+        const int h = idx / (HD + 1), e = 1 + idx % (HD + 1);  // l and the 128 accumulators
         float val = 0.f;
-        if (e == 0) {
-            val = M;
-        } else if (M != -INFINITY) {
-            for (int ww = 0; ww < ATT_WARPS; ++ww) {
-                const float mw = scratch[(ww * NH + h) * (HD + 2)];
-                if (mw == -INFINITY) continue;
-                val += scratch[(ww * NH + h) * (HD + 2) + e] * exp2f(mw - M);
-            }
-        }
+#pragma unroll
+        for (int ww = 0; ww < ATT_WARPS; ++ww) val = fmaf(scratch[(ww * NH + h) * (HD + 2) + e], s_scale[h][ww], val);
         cpart[h][e] = val;
     }
 }
@@ -570,7 +573,8 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     __shared__ float cpart[NH][HD + 2];  // this split's (m, l, acc) per head
-    __shared__ float s_lse[NH];          // LSE of head h, valid in the CTA of rank h
+    __shared__ float s_lse[NH];          // LSE of every head (each CTA derives all of them)
+    __shared__ float s_w[CL];            // rank h: weight of split r in q-head h's output
     extern __shared__ float sm_att[];    // [warps][NH][HD+2] merge scratch, then [units][NH] block maxima
     const int split = (int)cluster.block_rank(), g = blockIdx.y, s = blockIdx.z;
     ATT_TRACE(0);
@@ -667,38 +671,36 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     ATT_TRACE(4);
     cluster.sync();  // (1) every split's partial is visible in its shared memory
     ATT_TRACE(5);
-    if (split < NH) {  // rank h finalises q-head h over the CL partials
+    // every CTA derives the LSE of all NH heads from the CL partial (m, l) (no second barrier)
+    if (threadIdx.x < (NH * CL + 31) / 32 * 32) {  // whole warps (the shuffles below use full masks)
+        const bool valid = threadIdx.x < NH * CL;
+        const int h = valid ? threadIdx.x / CL : 0, r = threadIdx.x % CL;
+        const float mr = valid ? cluster.map_shared_rank(&cpart[h][0], r)[0] : -INFINITY;
+        const float lr = valid ? cluster.map_shared_rank(&cpart[h][1], r)[0] : 0.f;
+        float M = mr;
+#pragma unroll
+        for (int o = CL / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o, CL));
+        const float wr = mr == -INFINITY ? 0.f : exp2f(mr - M);
+        float L = lr * wr;
+#pragma unroll
+        for (int o = CL / 2; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o, CL);
+        if (valid && r == 0) s_lse[h] = M + log2f(L);
+        if (valid && split == h) s_w[r] = wr / L;  // rank h finalises q-head h: split r's weight in its output
+    }
+    __syncthreads();
+    if (split < NH && threadIdx.x < HD) {  // rank h finalises q-head h over the CL partials
         const int h = split;
-        float mr[CL], wr[CL];
-        float M = -INFINITY;
+        float o = 0.f;
 #pragma unroll
-        for (int r = 0; r < CL; ++r) {
-            mr[r] = cluster.map_shared_rank(&cpart[h][0], r)[0];
-            M = fmaxf(M, mr[r]);
-        }
-        float L = 0.f;
-#pragma unroll
-        for (int r = 0; r < CL; ++r) {
-            wr[r] = (mr[r] == -INFINITY) ? 0.f : exp2f(mr[r] - M);
-            L += cluster.map_shared_rank(&cpart[h][1], r)[0] * wr[r];
-        }
-        if (threadIdx.x < HD) {
-            float o = 0.f;
-#pragma unroll
-            for (int r = 0; r < CL; ++r) o = fmaf(cluster.map_shared_rank(&cpart[h][2 + threadIdx.x], r)[0], wr[r], o);
-            P.out[((int64_t)s * P.n_q_heads + h0 + h) * HD + threadIdx.x] = __float2bfloat16_rn(o / L);
-        }
-        if (threadIdx.x == 0) {
-            s_lse[h] = M + log2f(L);
-            if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = M + log2f(L);
-        }
+        for (int r = 0; r < CL; ++r) o = fmaf(cluster.map_shared_rank(&cpart[h][2 + threadIdx.x], r)[0], s_w[r], o);
+        P.out[((int64_t)s * P.n_q_heads + h0 + h) * HD + threadIdx.x] = __float2bfloat16_rn(o);
+        if (threadIdx.x == 0 && P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = s_lse[h];
     }
     ATT_TRACE(6);
     if constexpr (EMIT) {
-        cluster.sync();  // (2) the LSEs are visible
         float lse[NH];
 #pragma unroll
-        for (int h = 0; h < NH; ++h) lse[h] = cluster.map_shared_rank(&s_lse[h], h)[0];
+        for (int h = 0; h < NH; ++h) lse[h] = s_lse[h];
         float mx = 0.f;
         for (int u = u0 + threadIdx.x; u < u1; u += ATT_THREADS) {
             bool is_mid;
