@@ -16,13 +16,14 @@
 namespace ap {
 namespace wsm {
 
-constexpr int NT = 512;
+constexpr int NCONV = 10;                   // conv1 warps (16 measured slower: shared-memory port)
 constexpr int MO = 5;                       // output rows per band
 constexpr int MA = MO + 4;                  // a1 tile rows per band (2 segments x (n + 2))
 constexpr int MX = MO + 8;                  // x tile rows per band (2 segments x (n + 4))
 constexpr int NX = 4;                       // x tile stages
 constexpr int NA = 2;                       // a1 tile / accumulator stages
-constexpr int WARP_PROD = 0, WARP_MMA = 1, EPI0 = 2, NEPI = 4, CONV0 = 6, NCONV = 10;
+constexpr int WARP_PROD = 0, WARP_MMA = 1, EPI0 = 2, NEPI = 4, CONV0 = 6;
+constexpr int NT = (CONV0 + NCONV) * 32;
 constexpr int NCONV_T = NCONV * 32;
 constexpr int TMEM = 512;
 constexpr int ACC_COLS = MO * 32;           // 160
@@ -453,24 +454,20 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
             // one column per thread (loads issued now, stored after the a1 tile)
             const bool gather = m.first && !m.full && ct < TW && w0 + ct < W;
             double g_S = 0.0;
-            float g_os = 0.f;
+            float g_os = 0.f, ov[8];  // loads issued now, summed after the a1 tile (latency under conv1)
+            int n_old = 0;
             if (gather) {
                 const int col = w0 + ct;
                 const float* rm = P.rmap + (int64_t)m.map * P.map_stride + col;
-                if (P.rsum) g_S = P.rsum[(int64_t)m.map * P.pitch + col];
-                const int n_old = 2 + H - m.lo2;  // positions {0, 1} ∪ [lo2, H)
-                auto old_r = [&](int k) {
+                if (P.rsum) g_S = __ldcg(P.rsum + (int64_t)m.map * P.pitch + col);
+                n_old = 2 + H - m.lo2;  // positions {0, 1} ∪ [lo2, H)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
                     const int pp = k < 2 ? k : m.lo2 + k - 2;
                     int sl = sel ? m.base_slot + pp : pp;
                     sl = sl >= H ? sl - H : sl;
-                    return rm[(int64_t)sl * P.pitch];
-                };
-                float ov[8];  // all loads in flight before the first use
-#pragma unroll
-                for (int k = 0; k < 8; ++k) ov[k] = k < n_old ? old_r(k) : 0.f;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) g_os += ov[k];
-                for (int k = 8; k < n_old; ++k) g_os += old_r(k);
+                    ov[k] = k < n_old ? __ldcg(rm + (int64_t)sl * P.pitch) : 0.f;
+                }
             }
             if (b >= NA) mbar_wait(&a1_empty[a], ((b / NA) & 1) ^ 1);
             if (ct == 0) WSM_TRACE(b, 2);
@@ -525,6 +522,17 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                         *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE_M + px * 16) = l0;
                         *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE_M + px * 16 + 16) = l1;
                     }
+                }
+            }
+            if (gather) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) g_os += ov[k];
+                const float* rm = P.rmap + (int64_t)m.map * P.map_stride + w0 + ct;
+                for (int k = 8; k < n_old; ++k) {  // more than 6 new rows since the last update (rare)
+                    const int pp = m.lo2 + k - 2;
+                    int sl = sel ? m.base_slot + pp : pp;
+                    sl = sl >= H ? sl - H : sl;
+                    g_os += __ldcg(rm + (int64_t)sl * P.pitch);
                 }
             }
             mbar_wait(&eold_empty[a], (b / NA) & 1);  // completion 0 = start-up; then the epilogue read band b - NA's
