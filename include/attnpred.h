@@ -320,6 +320,11 @@ int ap_rope_append(const void* qkv, int32_t n_seq, int32_t n_q_heads, int32_t n_
                    void* q_out, void* k_cache, void* v_cache, int32_t t_max, float theta, void* stream);
 /* out [rows][ffn] = silu(gate_up[:, :ffn]) * gate_up[:, ffn:] */
 int ap_silu_mul(const void* gate_up, void* out, int32_t rows, int32_t ffn, void* stream);
+/* tokens[r] = argmax of bf16 logits row r ([rows][n] row-major; torch.argmax semantics, ties to the lowest
+ * index).  workspace: ap_argmax_workspace_bytes(rows) bytes, zeroed once, self-resetting. */
+int64_t ap_argmax_workspace_bytes(int32_t rows);
+int ap_argmax_rows(const void* logits, int32_t rows, int64_t n, void* workspace, int64_t workspace_bytes,
+                   int64_t* tokens, void* stream);
 /* seq_len[i] += by */
 int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream);
 
@@ -341,6 +346,16 @@ int ap_gemv_qkv_rope(const void* W, const void* x, void* y, int32_t n_q_heads, i
                      int32_t n_seq, int32_t flags, const void* residual, void* residual_out, const void* ln_w, float eps,
                      const int32_t* seq_len, void* q_out, void* k_cache, void* v_cache, int32_t t_max, float theta,
                      void* stream);
+
+/* Batch-5..16 bf16 GEMM y[s][n] = sum_k x[s][k] W[n][k] (W [N][K], x [n_seq][K], y [n_seq][N], all
+ * row-major; fp32 accumulate) on tcgen05 tensor cores, TMA-fed, one persistent wave over the SMs.
+ * K % 256 == 0, n_seq in 1..16, N <= 524288.  workspace: ap_gemm_tc_workspace_bytes(N, K, n_seq) bytes,
+ * zeroed once (self-resetting per-tile counters, then fp32 partials of row tiles split across CTAs); one
+ * workspace of the largest size serves GEMMs of every shape on a stream; the sum over
+ * splits runs in a fixed order, so results are run-to-run deterministic. */
+int64_t ap_gemm_tc_workspace_bytes(int32_t N, int32_t K, int32_t n_seq);
+int ap_gemm_tc(const void* W, const void* x, void* y, int32_t N, int32_t K, int32_t n_seq, void* workspace,
+               int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

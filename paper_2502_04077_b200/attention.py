@@ -26,6 +26,17 @@ HEAD_DIM = 128
 BLOCK = 16
 
 
+def sparse_splits(n_maps: int, sm_count: int) -> int:
+    """Cluster size (splits per map) of the sparse pass for n_maps maps per launch: the largest of
+    8, 4, 2 that keeps one wave (n_maps x splits <= SMs; the kernel runs one CTA per SM).  Measured
+    on B200 (scripts/bench_attention.py, LLaMA-3.1-8B layer at 32K): 8 maps -> 8 (9.2 us; 16: 16.8),
+    32 maps -> 4 (10.4 us; 8: 11.2), 64 maps -> 2 (21.9 us; 4: 28.0, 8: 48.0)."""
+    cl = 8
+    while cl > 2 and n_maps * cl > sm_count:
+        cl //= 2
+    return cl
+
+
 class DecodeAttention:
     """Workspaces + launchers for one layer shape (reused by every layer of a model).
 

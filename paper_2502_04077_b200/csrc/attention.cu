@@ -24,6 +24,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ap {
 
@@ -574,7 +575,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     cg::cluster_group cluster = cg::this_cluster();
     __shared__ float cpart[NH][HD + 2];  // this split's (m, l, acc) per head
     __shared__ float s_lse[NH];          // LSE of every head (each CTA derives all of them)
-    __shared__ float s_w[CL];            // rank h: weight of split r in q-head h's output
+    __shared__ float s_w[NH][CL];        // weight of split r in q-head h's output
     extern __shared__ float sm_att[];    // [warps][NH][HD+2] merge scratch, then [units][NH] block maxima
     const int split = (int)cluster.block_rank(), g = blockIdx.y, s = blockIdx.z;
     ATT_TRACE(0);
@@ -685,16 +686,18 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
 #pragma unroll
         for (int o = CL / 2; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o, CL);
         if (valid && r == 0) s_lse[h] = M + log2f(L);
-        if (valid && split == h) s_w[r] = wr / L;  // rank h finalises q-head h: split r's weight in its output
+        if (valid && h % CL == split) s_w[h][r] = wr / L;  // split r's weight in q-head h's output
     }
     __syncthreads();
-    if (split < NH && threadIdx.x < HD) {  // rank h finalises q-head h over the CL partials
-        const int h = split;
-        float o = 0.f;
+    if (threadIdx.x < HD) {  // rank r finalises q-heads r, r + CL, ... over the CL partials
+        for (int h = split; h < NH; h += CL) {
+            float o = 0.f;
 #pragma unroll
-        for (int r = 0; r < CL; ++r) o = fmaf(cluster.map_shared_rank(&cpart[h][2 + threadIdx.x], r)[0], s_w[r], o);
-        P.out[((int64_t)s * P.n_q_heads + h0 + h) * HD + threadIdx.x] = __float2bfloat16_rn(o);
-        if (threadIdx.x == 0 && P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = s_lse[h];
+            for (int r = 0; r < CL; ++r)
+                o = fmaf(cluster.map_shared_rank(&cpart[h][2 + threadIdx.x], r)[0], s_w[h][r], o);
+            P.out[((int64_t)s * P.n_q_heads + h0 + h) * HD + threadIdx.x] = __float2bfloat16_rn(o);
+            if (threadIdx.x == 0 && P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = s_lse[h];
+        }
     }
     ATT_TRACE(6);
     if constexpr (EMIT) {
@@ -753,15 +756,12 @@ static void launch_cluster(const AttnParams& P, cudaStream_t st) {
 
 template <int NH>
 static void launch_sparse(const AttnParams& P, bool emit, cudaStream_t st) {
-    if (P.n_splits == 8 || P.n_splits == 16) {  // cluster form
-        if (P.n_splits == 8) {
-            if (emit) launch_cluster<NH, true, 8>(P, st);
-            else launch_cluster<NH, false, 8>(P, st);
-        } else {
-            if (emit) launch_cluster<NH, true, 16>(P, st);
-            else launch_cluster<NH, false, 16>(P, st);
-        }
-        return;
+    switch (P.n_splits) {  // cluster form: the splits of a map are one thread-block cluster
+        case 2: return emit ? launch_cluster<NH, true, 2>(P, st) : launch_cluster<NH, false, 2>(P, st);
+        case 4: return emit ? launch_cluster<NH, true, 4>(P, st) : launch_cluster<NH, false, 4>(P, st);
+        case 8: return emit ? launch_cluster<NH, true, 8>(P, st) : launch_cluster<NH, false, 8>(P, st);
+        case 16: return emit ? launch_cluster<NH, true, 16>(P, st) : launch_cluster<NH, false, 16>(P, st);
+        default: break;
     }
     dim3 grid(P.n_splits, P.n_q_heads / NH, P.n_seq);
     const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
@@ -822,23 +822,6 @@ struct Smem {
     static constexpr int off_bm = off_bar + 8 * (2 * NST + 2 * NACC) + 16;  // [NH][tiles * 8] block maxima
     static int total(int nh, int max_tiles) { return off_bm + nh * max_tiles * (TILE / 16) * 4 + 1024; }
 };
-
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)1 << 16;                      // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;            // SBO: 8 rows x 128 B
-    d |= (uint64_t)1 << 46;                      // descriptor version (Blackwell)
-    d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
-    return d;
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-        :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     uint32_t r[8];
@@ -1099,21 +1082,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_c
     ATT_TRACE(6);
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
 template <int NH>
 static int launch(AttnParams P, cudaStream_t st) {
-    auto enc = encoder();
+    auto enc = tensor_map_encoder();
     AP_REQUIRE(enc != nullptr, AP_ECUDA, "cuTensorMapEncodeTiled unavailable");
     CUtensorMap map;
     const cuuint64_t dims[2] = {(cuuint64_t)HD, (cuuint64_t)P.n_seq * P.n_kv_heads * P.t_max};

@@ -103,6 +103,52 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
     }
 }
 
+// Greedy token of each row of bf16 logits [rows][n] (torch.argmax semantics: ties -> lowest index).
+// grid (chunks, rows): each CTA reduces a chunk to a packed key (orderable value << 32 | ~index),
+// merged per row with a 64-bit atomicMax; the row's last CTA decodes it and resets the workspace.
+__global__ void __launch_bounds__(256) argmax_rows_kernel(const __nv_bfloat16* __restrict__ logits, int64_t n,
+                                                          int64_t chunk, unsigned long long* best, int32_t* done,
+                                                          int64_t* tokens) {
+    const int row = blockIdx.y;
+    const __nv_bfloat16* x = logits + row * n;
+    const int64_t c0 = blockIdx.x * chunk, c1 = c0 + chunk < n ? c0 + chunk : n;
+    unsigned long long key = 0;
+    auto take = [&](float v, int64_t i) {
+        const unsigned long long k = ((unsigned long long)order_key(v) << 32) | (uint32_t)~(uint32_t)i;
+        key = k > key ? k : key;
+    };
+    if ((n & 7) == 0) {  // 16-byte loads (chunk is a multiple of 8)
+        for (int64_t i = c0 + threadIdx.x * 8; i < c1; i += 256 * 8) {
+            const uint4 u = __ldcs(reinterpret_cast<const uint4*>(x + i));
+            const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) take(__bfloat162float(h[e]), i + e);
+        }
+    } else {
+        for (int64_t i = c0 + threadIdx.x; i < c1; i += 256) take(__bfloat162float(x[i]), i);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long k = __shfl_xor_sync(0xffffffffu, key, o);
+        key = k > key ? k : key;
+    }
+    __shared__ unsigned long long s_key[8];
+    __shared__ int s_last;
+    if ((threadIdx.x & 31) == 0) s_key[threadIdx.x >> 5] = key;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) key = s_key[w] > key ? s_key[w] : key;
+        atomicMax(best + row, key);
+        __threadfence();
+        s_last = atomicAdd(done + row, 1) == (int)gridDim.x - 1;
+        if (s_last) {
+            const unsigned long long k = atomicExch(best + row, 0ull);
+            tokens[row] = (int64_t)(uint32_t)~(uint32_t)(k & 0xffffffffu);
+            done[row] = 0;
+        }
+    }
+}
+
 __global__ void advance_kernel(int32_t* seq_len, int n, int by) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) seq_len[i] += by;
@@ -137,6 +183,27 @@ int ap_silu_mul(const void* gate_up, void* out, int32_t rows, int32_t ffn, void*
     if (blocks > 4096) blocks = 4096;
     silu_mul_kernel<<<blocks, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)gate_up, (__nv_bfloat16*)out, ffn, n);
     return launch_status("ap_silu_mul");
+}
+
+int64_t ap_argmax_workspace_bytes(int32_t rows) { return rows > 0 ? (int64_t)rows * 12 : -1; }
+
+int ap_argmax_rows(const void* logits, int32_t rows, int64_t n, void* workspace, int64_t workspace_bytes,
+                   int64_t* tokens, void* stream) {
+    AP_REQUIRE(logits && tokens && rows > 0 && n > 0 && n < (1ll << 32), AP_EPARAM, "bad argmax operands");
+    AP_REQUIRE(workspace && workspace_bytes >= (int64_t)rows * 12, AP_EPARAM, "argmax workspace too small");
+    const int sms = ap_device_sm_count();
+    int64_t chunks = 2 * (int64_t)sms / rows;
+    const int64_t max_chunks = (n + 2047) / 2048;
+    if (chunks > max_chunks) chunks = max_chunks;
+    if (chunks < 1) chunks = 1;
+    int64_t chunk = (n + chunks - 1) / chunks;
+    chunk = (chunk + 7) / 8 * 8;
+    chunks = (n + chunk - 1) / chunk;
+    auto* best = (unsigned long long*)workspace;
+    auto* done = (int32_t*)((char*)workspace + (int64_t)rows * 8);
+    argmax_rows_kernel<<<dim3((unsigned)chunks, rows), 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)logits, n,
+                                                                                     chunk, best, done, tokens);
+    return launch_status("ap_argmax_rows");
 }
 
 int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream) {

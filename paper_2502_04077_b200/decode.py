@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 from . import _device as D
 from . import _lib
-from .attention import DecodeAttention
+from .attention import DecodeAttention, sparse_splits
 from .batched import BatchedSelector
 from .errors import ConfigError
 from .predictor import PredictorWeights, init_weights, install_weights
@@ -135,7 +135,15 @@ class DecodeEngine:
         self.r = torch.zeros(S, Hd, dtype=bf, device=dev)
         self.r2 = torch.zeros(S, Hd, dtype=bf, device=dev)  # fused path: residual stream ping-pong
         self.fused = fused and S <= 4
-        self.argws = torch.zeros(48, dtype=torch.uint8, device=dev)  # ap_gemv ARGMAX workspace
+        # ap_gemv ARGMAX (batch <= 4) / ap_argmax_rows (larger batches) workspace
+        self.argws = torch.zeros(max(48, _lib.fn("ap_argmax_workspace_bytes")(S)), dtype=torch.uint8, device=dev)
+        # batch 5..16: projections on the tcgen05 skinny GEMM (ap_gemm_tc); larger batches: library GEMM
+        self.tc = not self.fused and S <= 16
+        self.tcws = None
+        if self.tc:
+            need = max(_lib.fn("ap_gemm_tc_workspace_bytes")(n, k, S)
+                       for n, k in ((shape.qkv_dim, Hd), (Hd, Hq_full * 128), (2 * F, Hd), (Hd, F), (V, Hd)))
+            self.tcws = torch.zeros(need, dtype=torch.uint8, device=dev)
         self.y = torch.zeros(S, Hd, dtype=bf, device=dev)
         self.qkv = torch.zeros(S, shape.qkv_dim, dtype=bf, device=dev)
         self.q = torch.zeros(S, Hq, 128, dtype=bf, device=dev)
@@ -148,9 +156,10 @@ class DecodeEngine:
         self.tok = torch.zeros(S, dtype=torch.int64, device=dev)
         self.logits = torch.zeros(S, V, dtype=bf, device=dev)
         self.seq_len = torch.full((S,), ctx_len, dtype=torch.int32, device=dev)
-        self.att = DecodeAttention(S, Hq, Hkv, self.t_max, n_splits_dense=min(64, self.t_max // 1024),
-                                   n_splits_sparse=8, device=dev)
         self.maps_per_layer = Hq // group
+        self.att = DecodeAttention(S, Hq, Hkv, self.t_max, n_splits_dense=min(64, self.t_max // 1024),
+                                   n_splits_sparse=sparse_splits(S * self.maps_per_layer,
+                                                                 _lib.fn("ap_device_sm_count")()), device=dev)
         self.sel = None
         from .selector import SelectorConfig
         self.cfg = cfg or SelectorConfig(budget=1024)
@@ -239,7 +248,7 @@ class DecodeEngine:
             else:
                 _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.ln1[l]),
                                                  _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
-            torch.matmul(self.y, self.wqkv[l].t(), out=self.qkv)
+            self._mm(self.y, self.wqkv[l], self.qkv)
             _lib.check(_lib.fn("ap_rope_append")(_lib.ptr(self.qkv), S, sh.n_q_heads, sh.n_kv_heads,
                                                  _lib.ptr(self.seq_len), _lib.ptr(self.q), _lib.ptr(kc),
                                                  None if self.voff is not None else _lib.ptr(vc),
@@ -274,15 +283,25 @@ class DecodeEngine:
             self._gemv(self.wgu[l], self.o, self.act, GEMV_RMS | GEMV_SILU, residual=self.r, residual_out=self.r2,
                        ln=self.ln2[l])
         else:
-            torch.matmul(self.att_full.view(S, -1), self.wo[l].t(), out=self.o)
+            self._mm(self.att_full.view(S, -1), self.wo[l], self.o)
             _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.o), _lib.ptr(self.r), _lib.ptr(self.ln2[l]),
                                              _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
-            torch.matmul(self.y, self.wgu[l].t(), out=self.gu)
+            self._mm(self.y, self.wgu[l], self.gu)
             _lib.check(_lib.fn("ap_silu_mul")(_lib.ptr(self.gu), _lib.ptr(self.act), S, sh.ffn, s))
         if self.fused:
             self._gemv(self.wdown[l], self.act, self.mlp, 0)
         else:
-            torch.matmul(self.act, self.wdown[l].t(), out=self.mlp)
+            self._mm(self.act, self.wdown[l], self.mlp)
+
+    def _mm(self, x, W, y):
+        """y = x W^T: ap_gemm_tc (tcgen05) for batch 5..16, the library GEMM above that."""
+        N, K = W.shape
+        if self.tc and K % 256 == 0:
+            _lib.check(_lib.fn("ap_gemm_tc")(_lib.ptr(W), _lib.ptr(x), _lib.ptr(y), N, K, self.n_seq,
+                                             _lib.ptr(self.tcws), self.tcws.numel(), _lib.stream_handle()),
+                       "ap_gemm_tc")
+        else:
+            D.torch().matmul(x, W.t(), out=y)
 
     def _gemv(self, W, x, y, flags, residual=None, residual_out=None, ln=None, tokens=None):
         """ap_gemv: y = W x for this step's sequences with the fused prologue / epilogue in flags."""
@@ -318,8 +337,9 @@ class DecodeEngine:
         else:
             _lib.check(_lib.fn("ap_rmsnorm")(_lib.ptr(self.mlp), _lib.ptr(self.r), _lib.ptr(self.lnf),
                                              _lib.ptr(self.y), S, sh.hidden, sh.eps, s))
-            torch.matmul(self.y, self.lm_head.t(), out=self.logits)
-            torch.argmax(self.logits, dim=-1, out=self.tok)
+            self._mm(self.y, self.lm_head, self.logits)
+            _lib.check(_lib.fn("ap_argmax_rows")(_lib.ptr(self.logits), S, sh.vocab, _lib.ptr(self.argws),
+                                                 self.argws.numel(), _lib.ptr(self.tok), s), "ap_argmax_rows")
         if self.sel is not None and variant != "dense":
             self.sel.step()  # forecast + top-k for the next token, every layer and head at once
 
@@ -425,11 +445,13 @@ class DecodeEngine:
     def kernels_per_step(self, variant: str) -> int:
         """Launches of libattnpred kernels in one step (the bench's gpu_launches claim)."""
         L = self.shape.n_layers
-        per_layer = 4 if self.fused else 2 + 1 + 1  # gemv x4 (qkv+rope fused) | rmsnorm x2, rope_append, silu_mul
+        # gemv x4 (qkv+rope fused) | rmsnorm x2, rope_append, silu_mul (+ 4 ap_gemm_tc at batch 5..16)
+        per_layer = 4 if self.fused else 2 + 1 + 1 + (4 if self.tc else 0)
         att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
         att_total = self.dense_layers + (L - self.dense_layers) * att
         sel = 2 if (self.sel is not None and variant != "dense") else 0
         off = 0
         if self.voff is not None:
             off = L * (1 + (1 if variant in ("plain", "calib") else 0))  # v_append (+ prefetch) per layer
-        return 1 + L * per_layer + att_total + 1 + sel + off  # advance + layers + final norm/LM head + selector
+        head = 1 if self.fused else (3 if self.tc else 2)  # final norm (+ LM head on ap_gemm_tc) + argmax
+        return 1 + L * per_layer + att_total + head + sel + off  # advance + layers + final norm/LM head + selector

@@ -31,8 +31,9 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--splits", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=1)
     args = ap.parse_args()
-    S, Hq, Hkv, L = 1, 32, 8, args.layers
+    S, Hq, Hkv, L = args.batch, 32, 8, args.layers
     t_max = -(-(args.t + 16) // 1024) * 1024
     G = 1 if args.group == "head" else Hq // Hkv
     maps = Hq // G
@@ -40,7 +41,7 @@ def main():
     v = torch.randn(L, S, Hkv, t_max, 128, device="cuda", dtype=torch.bfloat16)
     q = torch.randn(S, Hq, 128, device="cuda", dtype=torch.bfloat16)
     out = torch.empty(S, Hq, 128, device="cuda", dtype=torch.bfloat16)
-    seq_len = torch.tensor([args.t], dtype=torch.int32, device="cuda")
+    seq_len = torch.full((S,), args.t, dtype=torch.int32, device="cuda")
     cfg = SelectorConfig(budget=1024)
     sel = BatchedSelector(cfg, S * L * maps, t_max // 16)
     rng = np.random.default_rng(0)
@@ -75,19 +76,19 @@ def main():
 
     res = {}
     n_units = 4 + 5 + cfg.middle_blocks
-    sparse_bytes = maps * n_units * 4096 * 2 if G > 1 else Hq * n_units * 4096 * 2
+    sparse_bytes = S * (maps * n_units * 4096 * 2 if G > 1 else Hq * n_units * 4096 * 2)
     res["sparse_emit_us"] = timeit(lambda l: att.sparse(q, k[l], v[l], seq_len, out, sel, emit=True, map_base=l * maps,
                                                          maps_per_seq=L * maps, group=G))
     res["sparse_noemit_us"] = timeit(lambda l: att.sparse(q, k[l], v[l], seq_len, out, sel, emit=False,
                                                            map_base=l * maps, maps_per_seq=L * maps, group=G))
     res["sparse_GBps"] = sparse_bytes / (res["sparse_noemit_us"] * 1e-6) / 1e9
-    dense_bytes = Hkv * args.t * 256 * 2
+    dense_bytes = S * Hkv * args.t * 256 * 2
     res["dense_us"] = timeit(lambda l: att.dense(q, k[l], v[l], seq_len, out, with_v=True))
     res["dense_GBps"] = dense_bytes / (res["dense_us"] * 1e-6) / 1e9
     res["calib_us"] = timeit(lambda l: att.dense(q, k[l], k[l], seq_len, None, with_v=False, emit=True, selector=sel,
                                                  map_base=l * maps, maps_per_seq=L * maps, group=G))
     res["calib_GBps"] = dense_bytes / 2 / (res["calib_us"] * 1e-6) / 1e9
-    res.update(t=args.t, group=args.group, sparse_bytes=sparse_bytes, dense_bytes=dense_bytes)
+    res.update(batch=S, t=args.t, group=args.group, sparse_bytes=sparse_bytes, dense_bytes=dense_bytes)
     print(json.dumps({k_: (round(v_, 2) if isinstance(v_, float) else v_) for k_, v_ in res.items()}))
 
 

@@ -28,11 +28,15 @@ def main():
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--model", default="llama-3.1-8b")
     ap.add_argument("--precision", default="fp16x3")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--no-tc", action="store_true", help="batch 5..16: library GEMMs instead of ap_gemm_tc")
     args = ap.parse_args()
     shape = SHAPES[args.model]
     G = shape.n_q_heads // shape.n_kv_heads
-    eng = DecodeEngine(shape, 1, args.ctx, max_new=64, cfg=SelectorConfig(budget=1024),
+    eng = DecodeEngine(shape, args.batch, args.ctx, max_new=64, cfg=SelectorConfig(budget=1024),
                        group=1 if args.group == "head" else G, precision=args.precision)
+    if args.no_tc:
+        eng.tc = False
     eng.init_history()
     eng.step(use_graph=False)
     eng.capture_all()

@@ -100,7 +100,7 @@ def _set_selection(sel, rng, lens, maps, k_mid, b=16):
     return blocks_per_map
 
 
-@pytest.mark.parametrize("splits", [4, 8])  # 8 = the thread-block-cluster form
+@pytest.mark.parametrize("splits", [2, 3, 4, 8, 16])  # 3: global-memory combine; others: one cluster per map
 @pytest.mark.parametrize("group", [1, 4])
 def test_sparse_attention_and_observed_row(group, splits):
     import torch
@@ -146,7 +146,7 @@ def test_sparse_attention_and_observed_row(group, splits):
     assert list(st["width"][::maps]) == [-(-t // 16) for t in lens]
 
 
-@pytest.mark.parametrize("splits", [3, 8])
+@pytest.mark.parametrize("splits", [2, 3, 8])
 def test_sparse_with_full_selection_equals_dense(splits):
     """With a budget that covers every block, sparse attention reproduces dense attention."""
     import torch
