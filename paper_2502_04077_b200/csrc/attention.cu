@@ -567,17 +567,50 @@ __device__ void merge_warps_to_smem(WarpState<NH, true>& st, float* scratch, flo
     }
 }
 
-// CL = cluster size = splits per map (8 portable, 16 with the non-portable opt-in); launched with
-// the cluster dimension as a launch attribute.
+// DSMEM push helpers: 32-bit shared::cluster address of a local variable in CTA `rank`, and
+// register -> remote shared memory stores that complete_tx on the receiver's mbarrier.
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, float c, float d, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+                 :: "r"(addr), "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+                 :: "r"(addr), "f"(a), "f"(b), "r"(mbar) : "memory");
+}
+
+// CL = cluster size = splits per map (2/4/8 portable, 16 with the non-portable opt-in); launched with
+// the cluster dimension as a launch attribute.  The splits exchange their partials by pushing them
+// (st.async) into the peers' shared memory: every rank receives every split's (m, l) of all NH heads,
+// and rank h % CL the accumulators of q-head h; each waits on its own mbarrier only (no cluster-wide
+// barrier on the critical path, nobody reads a peer's shared memory, so no exit barrier either).
 template <int NH, bool EMIT, int CL>
 __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams P) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
-    __shared__ float cpart[NH][HD + 2];  // this split's (m, l, acc) per head
-    __shared__ float s_lse[NH];          // LSE of every head (each CTA derives all of them)
-    __shared__ float s_w[NH][CL];        // weight of split r in q-head h's output
+    constexpr int NFIN = (NH + CL - 1) / CL;                // q-heads a rank finalises (at most)
+    __shared__ float cpart[NH][HD + 2];                     // this split's (m, l, acc) per head
+    __shared__ __align__(16) float s_ml_in[CL][NH][2];      // every split's (m, l) per head
+    __shared__ __align__(16) float s_acc_in[NFIN][CL][HD];  // every split's acc of the heads finalised here
+    __shared__ __align__(8) uint64_t s_rx;                  // completes when all of the above has landed
+    __shared__ float s_lse[NH];                             // LSE of every head
+    __shared__ float s_w[NH][CL];                           // weight of split r in q-head h's output
     extern __shared__ float sm_att[];    // [warps][NH][HD+2] merge scratch, then [units][NH] block maxima
     const int split = (int)cluster.block_rank(), g = blockIdx.y, s = blockIdx.z;
+    if (threadIdx.x == 0) {
+        const int n_fin = split < NH ? (NH - split + CL - 1) / CL : 0;
+        mbar_init(&s_rx, 1);
+        mbar_arrive_tx(&s_rx, (uint32_t)(CL * NH * 2 * 4 + n_fin * CL * HD * 4));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // every peer's receive barrier must be initialised before anyone pushes: arrive now, wait (free by
+    // then) just before the pushes
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     ATT_TRACE(0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane & 15;
     pdl_trigger();
@@ -669,32 +702,43 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     }
     ATT_TRACE(3);
     merge_warps_to_smem<NH>(st, sm_att, cpart);
+    __syncthreads();
     ATT_TRACE(4);
-    cluster.sync();  // (1) every split's partial is visible in its shared memory
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    // push: (m, l) of head h to every rank; acc of head h (32 x 16 B) to rank h % CL
+    if (threadIdx.x < CL * NH) {
+        const int q = threadIdx.x / NH, h = threadIdx.x % NH;
+        st_async_v2(mapa_u32(&s_ml_in[split][h][0], q), cpart[h][0], cpart[h][1], mapa_u32(&s_rx, q));
+    }
+    for (int idx = threadIdx.x; idx < NH * (HD / 4); idx += ATT_THREADS) {
+        const int h = idx / (HD / 4), c = idx % (HD / 4), q = h % CL;
+        const float* a = &cpart[h][2 + 4 * c];
+        st_async_v4(mapa_u32(&s_acc_in[h / CL][split][4 * c], q), a[0], a[1], a[2], a[3], mapa_u32(&s_rx, q));
+    }
+    mbar_wait(&s_rx, 0);
     ATT_TRACE(5);
-    // every CTA derives the LSE of all NH heads from the CL partial (m, l) (no second barrier)
-    if (threadIdx.x < (NH * CL + 31) / 32 * 32) {  // whole warps (the shuffles below use full masks)
-        const bool valid = threadIdx.x < NH * CL;
-        const int h = valid ? threadIdx.x / CL : 0, r = threadIdx.x % CL;
-        const float mr = valid ? cluster.map_shared_rank(&cpart[h][0], r)[0] : -INFINITY;
-        const float lr = valid ? cluster.map_shared_rank(&cpart[h][1], r)[0] : 0.f;
-        float M = mr;
+    if (threadIdx.x < NH) {  // LSE and split weights of every head
+        const int h = threadIdx.x;
+        float M = -INFINITY;
 #pragma unroll
-        for (int o = CL / 2; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o, CL));
-        const float wr = mr == -INFINITY ? 0.f : exp2f(mr - M);
-        float L = lr * wr;
+        for (int r = 0; r < CL; ++r) M = fmaxf(M, s_ml_in[r][h][0]);
+        float wr[CL], L = 0.f;
 #pragma unroll
-        for (int o = CL / 2; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o, CL);
-        if (valid && r == 0) s_lse[h] = M + log2f(L);
-        if (valid && h % CL == split) s_w[h][r] = wr / L;  // split r's weight in q-head h's output
+        for (int r = 0; r < CL; ++r) {
+            const float mr = s_ml_in[r][h][0];
+            wr[r] = mr == -INFINITY ? 0.f : exp2f(mr - M);
+            L += s_ml_in[r][h][1] * wr[r];
+        }
+        s_lse[h] = M + log2f(L);
+#pragma unroll
+        for (int r = 0; r < CL; ++r) s_w[h][r] = wr[r] / L;
     }
     __syncthreads();
     if (threadIdx.x < HD) {  // rank r finalises q-heads r, r + CL, ... over the CL partials
         for (int h = split; h < NH; h += CL) {
             float o = 0.f;
 #pragma unroll
-            for (int r = 0; r < CL; ++r)
-                o = fmaf(cluster.map_shared_rank(&cpart[h][2 + threadIdx.x], r)[0], s_w[h][r], o);
+            for (int r = 0; r < CL; ++r) o = fmaf(s_acc_in[h / CL][r][threadIdx.x], s_w[h][r], o);
             P.out[((int64_t)s * P.n_q_heads + h0 + h) * HD + threadIdx.x] = __float2bfloat16_rn(o);
             if (threadIdx.x == 0 && P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = s_lse[h];
         }
@@ -731,7 +775,6 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
         }
     }
     ATT_TRACE(7);
-    cluster.sync();  // no CTA leaves while a peer may still read its shared memory
     ATT_TRACE(8);
 }
 

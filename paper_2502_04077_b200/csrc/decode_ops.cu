@@ -1,7 +1,7 @@
 // Small fused ops of the decode engine around the critical-token path:
 // residual-add + RMSNorm, RoPE + KV-cache append, SiLU-gate, sequence advance.
-// (The model's GEMMs are plain library GEMMs; attention and selection are the
-// hot path in attention.cu / predictor.cu / topk.cu.)
+// All launched with programmatic dependent launch: each triggers its dependents at entry and waits
+// for its predecessor before touching memory, so the next projection's weight prefetch overlaps.
 #include "common.cuh"
 
 namespace ap {
@@ -11,6 +11,8 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __res
                                                       __nv_bfloat16* __restrict__ residual, const __nv_bfloat16* __restrict__ w,
                                                       __nv_bfloat16* __restrict__ y, int D, float eps) {
     __shared__ float red[8];
+    pdl_trigger();
+    pdl_wait();  // x / residual come from the kernels just before
     const int row = blockIdx.x;
     const __nv_bfloat16* xr = x + (int64_t)row * D;
     __nv_bfloat16* rr = residual ? residual + (int64_t)row * D : nullptr;
@@ -96,6 +98,8 @@ __global__ void rope_append_kernel(const __nv_bfloat16* __restrict__ qkv, int Hq
 // gu: [S][2*F] (gate | up) -> out [S][F] = silu(gate) * up
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int F,
                                 int64_t n) {
+    pdl_trigger();
+    pdl_wait();
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = idx / F, f = idx % F;
         const float g = __bfloat162float(gu[s * 2 * F + f]), u = __bfloat162float(gu[s * 2 * F + F + f]);
@@ -109,6 +113,8 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
 __global__ void __launch_bounds__(256) argmax_rows_kernel(const __nv_bfloat16* __restrict__ logits, int64_t n,
                                                           int64_t chunk, unsigned long long* best, int32_t* done,
                                                           int64_t* tokens) {
+    pdl_trigger();
+    pdl_wait();
     const int row = blockIdx.y;
     const __nv_bfloat16* x = logits + row * n;
     const int64_t c0 = blockIdx.x * chunk, c1 = c0 + chunk < n ? c0 + chunk : n;
@@ -163,8 +169,8 @@ extern "C" {
 int ap_rmsnorm(const void* x, void* residual, const void* weight, void* y, int32_t rows, int32_t dim, float eps,
                void* stream) {
     AP_REQUIRE(dim % 8 == 0, AP_EPARAM, "dim must be a multiple of 8");
-    rmsnorm_kernel<<<rows, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)x, (__nv_bfloat16*)residual,
-                                                        (const __nv_bfloat16*)weight, (__nv_bfloat16*)y, dim, eps);
+    launch_ex(rmsnorm_kernel, dim3(rows), dim3(256), 0, as_stream(stream), 1, (const __nv_bfloat16*)x,
+              (__nv_bfloat16*)residual, (const __nv_bfloat16*)weight, (__nv_bfloat16*)y, (int)dim, eps);
     return launch_status("ap_rmsnorm");
 }
 
@@ -181,7 +187,8 @@ int ap_silu_mul(const void* gate_up, void* out, int32_t rows, int32_t ffn, void*
     const int64_t n = (int64_t)rows * ffn;
     int blocks = (int)((n + 255) / 256);
     if (blocks > 4096) blocks = 4096;
-    silu_mul_kernel<<<blocks, 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)gate_up, (__nv_bfloat16*)out, ffn, n);
+    launch_ex(silu_mul_kernel, dim3(blocks), dim3(256), 0, as_stream(stream), 1, (const __nv_bfloat16*)gate_up,
+              (__nv_bfloat16*)out, (int)ffn, n);
     return launch_status("ap_silu_mul");
 }
 
@@ -201,8 +208,8 @@ int ap_argmax_rows(const void* logits, int32_t rows, int64_t n, void* workspace,
     chunks = (n + chunk - 1) / chunk;
     auto* best = (unsigned long long*)workspace;
     auto* done = (int32_t*)((char*)workspace + (int64_t)rows * 8);
-    argmax_rows_kernel<<<dim3((unsigned)chunks, rows), 256, 0, as_stream(stream)>>>((const __nv_bfloat16*)logits, n,
-                                                                                     chunk, best, done, tokens);
+    launch_ex(argmax_rows_kernel, dim3((unsigned)chunks, rows), dim3(256), 0, as_stream(stream), 1,
+              (const __nv_bfloat16*)logits, n, chunk, best, done, tokens);
     return launch_status("ap_argmax_rows");
 }
 

@@ -22,10 +22,20 @@
 namespace ap {
 namespace gtc {
 
-constexpr int BM = 128, BN = 16, SLAB = 64, SLABS = 4;      // stage = 4 slabs of 64 K-elements
+#ifndef GTC_SLABS
+#define GTC_SLABS 2
+#endif
+#ifndef GTC_NST
+#define GTC_NST 3
+#endif
+#ifndef GTC_CTAS
+#define GTC_CTAS 1
+#endif
+constexpr int BM = 128, BN = 16, SLAB = 64, SLABS = GTC_SLABS;  // stage = SLABS slabs of 64 K-elements
 constexpr int A_BOX = BM * SLAB * 2, B_BOX = BN * SLAB * 2;  // 16 KB, 2 KB
-constexpr int STAGE = SLABS * (A_BOX + B_BOX);               // 72 KB
-constexpr int NST = 3, NACC = 2;
+constexpr int STAGE = SLABS * (A_BOX + B_BOX);               // 36 KB
+constexpr int NST = GTC_NST, NACC = 2;
+constexpr int CTAS_PER_SM = GTC_CTAS;
 constexpr int THREADS = 192;
 // workspace: a fixed counter area first (so GEMMs of any shape can share one workspace: every one
 // of them leaves its counters at zero), then the fp32 partials
@@ -37,6 +47,7 @@ struct Params {
     float* ws;               // [tiles][max_pieces][S][BM] partials
     int32_t* counters;       // [tiles], zero between launches
     int N, K, S, n_tiles, stages_per_tile, max_pieces;
+    int grouped;             // W tensor map is the grouped 4-D view (one copy per stage)
     int trace;               // debug (ATTNPRED_GEMM_TRACE=1): per-CTA globaltimer events into g_trace
 };
 
@@ -71,7 +82,7 @@ __device__ __forceinline__ int owner_of(const Params& P, int64_t g) {
     return c;
 }
 
-__global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_constant__ CUtensorMap wmap,
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) gemm_tc_kernel(const __grid_constant__ CUtensorMap wmap,
                                                              const __grid_constant__ CUtensorMap xmap, Params P) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -122,9 +133,13 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 stage_coords(g0 + i, tile, ks);
                 uint8_t* dst = smem + Smem::off_stage + i * STAGE;
                 mbar_arrive_tx(&full[i], STAGE);
+                if (P.grouped) {
+                    tma_load_4d(dst, &wmap, 0, 0, ks * SLABS, tile * (BM / 8), &full[i]);
+                } else {
 #pragma unroll
-                for (int sl = 0; sl < SLABS; ++sl)
-                    tma_load_2d(dst + sl * A_BOX, &wmap, (ks * SLABS + sl) * SLAB, tile * BM, &full[i]);
+                    for (int sl = 0; sl < SLABS; ++sl)
+                        tma_load_2d(dst + sl * A_BOX, &wmap, (ks * SLABS + sl) * SLAB, tile * BM, &full[i]);
+                }
             }
             pdl_wait();
             trace_event(P, 2);
@@ -144,10 +159,11 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                 stage_coords(g, tile, ks);
                 uint8_t* dst = smem + Smem::off_stage + st * STAGE;
                 mbar_arrive_tx(&full[st], STAGE);
+                if (P.grouped) tma_load_4d(dst, &wmap, 0, 0, ks * SLABS, tile * (BM / 8), &full[st]);
 #pragma unroll
                 for (int sl = 0; sl < SLABS; ++sl) {
                     const int kx = (ks * SLABS + sl) * SLAB;
-                    tma_load_2d(dst + sl * A_BOX, &wmap, kx, tile * BM, &full[st]);
+                    if (!P.grouped) tma_load_2d(dst + sl * A_BOX, &wmap, kx, tile * BM, &full[st]);
                     tma_load_2d(dst + SLABS * A_BOX + sl * B_BOX, &xmap, kx, 0, &full[st]);
                 }
             }
@@ -175,7 +191,9 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_tc_kernel(const __grid_consta
                     for (int sl = 0; sl < SLABS; ++sl)
 #pragma unroll
                         for (int kk = 0; kk < SLAB / 16; ++kk) {
-                            mma_f16(tmem_base + ab * BN, desc_sw128(a + sl * A_BOX + kk * 32),
+                            const uint64_t ad = P.grouped ? desc_sw128_sbo(a + sl * 1024 + kk * 32, SLABS * 1024)
+                                                          : desc_sw128(a + sl * A_BOX + kk * 32);
+                            mma_f16(tmem_base + ab * BN, ad,
                                     desc_sw128(b + sl * B_BOX + kk * 32), idesc, first ? 0u : 1u);
                             first = false;
                         }
@@ -284,7 +302,7 @@ static Geometry geometry(int N, int K) {
     G.n_tiles = (N + BM - 1) / BM;
     G.stages_per_tile = K / (SLAB * SLABS);
     const int64_t T = (int64_t)G.n_tiles * G.stages_per_tile;
-    const int sms = ap_device_sm_count();
+    const int sms = ap_device_sm_count() * CTAS_PER_SM;
     G.grid = (int)(T < sms ? T : sms);
     const int64_t per = T / G.grid;  // >= 1
     G.max_pieces = (int)((G.stages_per_tile + per - 1) / per + 1);
@@ -317,7 +335,13 @@ extern "C" int ap_gemm_tc(const void* W, const void* x, void* y, int32_t N, int3
     AP_REQUIRE(workspace && workspace_bytes >= need, AP_EPARAM, "workspace too small (%lld bytes needed)",
                (long long)need);
     CUtensorMap wmap, xmap;
-    AP_REQUIRE(make_tmap_bf16_sw128(&wmap, W, (uint64_t)N, (uint64_t)K, BM), AP_ECUDA, "tensor map (W) failed");
+    static const int want_grouped = getenv("ATTNPRED_GEMM_GROUPED") ? atoi(getenv("ATTNPRED_GEMM_GROUPED")) : 1;
+    const bool grouped = want_grouped && N % 8 == 0;
+    if (grouped)
+        AP_REQUIRE(make_tmap_bf16_sw128_grouped(&wmap, W, (uint64_t)N, (uint64_t)K, SLABS, BM / 8), AP_ECUDA,
+                   "tensor map (W) failed");
+    else
+        AP_REQUIRE(make_tmap_bf16_sw128(&wmap, W, (uint64_t)N, (uint64_t)K, BM), AP_ECUDA, "tensor map (W) failed");
     AP_REQUIRE(make_tmap_bf16_sw128(&xmap, x, (uint64_t)n_seq, (uint64_t)K, BN), AP_ECUDA, "tensor map (x) failed");
     Params P{};
     P.y = (__nv_bfloat16*)y;
@@ -329,6 +353,7 @@ extern "C" int ap_gemm_tc(const void* W, const void* x, void* y, int32_t N, int3
     P.n_tiles = G.n_tiles;
     P.stages_per_tile = G.stages_per_tile;
     P.max_pieces = G.max_pieces;
+    P.grouped = grouped;
     static const int trace = getenv("ATTNPRED_GEMM_TRACE") ? atoi(getenv("ATTNPRED_GEMM_TRACE")) : 0;
     P.trace = trace;
     static bool attr = false;

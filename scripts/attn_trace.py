@@ -7,15 +7,15 @@ from paper_2502_04077_b200.attention import DecodeAttention
 from paper_2502_04077_b200.batched import BatchedSelector
 from paper_2502_04077_b200.selector import SelectorConfig
 L = _lib.load()
-S, Hq, Hkv, t = 1, 32, 8, 32768
+S, Hq, Hkv, t = int(os.environ.get("BATCH", "1")), 32, 8, 32768
 t_max = 33792
 k = torch.randn(S, Hkv, t_max, 128, device="cuda", dtype=torch.bfloat16)
 v = torch.randn(S, Hkv, t_max, 128, device="cuda", dtype=torch.bfloat16)
 q = torch.randn(S, Hq, 128, device="cuda", dtype=torch.bfloat16)
 out = torch.empty(S, Hq, 128, device="cuda", dtype=torch.bfloat16)
-seq_len = torch.tensor([t], dtype=torch.int32, device="cuda")
+seq_len = torch.full((S,), t, dtype=torch.int32, device="cuda")
 cfg = SelectorConfig(budget=1024)
-maps = 8
+maps = 8 * S
 sel = BatchedSelector(cfg, maps, t_max // 16)
 st = sel.states().copy()
 rng = np.random.default_rng(0)
@@ -27,7 +27,7 @@ sel.state.copy_(torch.from_numpy(st.view(np.uint8).copy()))
 att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_sparse=int(os.environ.get("SPLITS", "8")))
 for it in range(4):
     L.ap_attn_debug_trace(1 if it == 3 else 0, None)
-    att.sparse(q, k, v, seq_len, out, sel, emit=True, map_base=0, maps_per_seq=maps, group=4)
+    att.sparse(q, k, v, seq_len, out, sel, emit=True, map_base=0, maps_per_seq=8, group=4)
     torch.cuda.synchronize()
 buf = (ctypes.c_longlong * 256)()
 L.ap_attn_debug_trace(0, buf)
