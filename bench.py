@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--precision", default="fp16x3")
     ap.add_argument("--no-dense", action="store_true", help="skip the full-attention comparator arm")
     ap.add_argument("--no-alt", action="store_true", help="skip the other selection granularity")
+    ap.add_argument("--gemm", choices=["auto", "tc"], default="auto",
+                    help="batch 5..16 projections: library GEMM (auto) or ap_gemm_tc (tc)")
     ap.add_argument("--parallel", choices=["replicas", "heads"], default="replicas",
                     help="N>1: independent sequences per GPU (weak) or one sequence with KV heads split (strong)")
     ap.add_argument("--offload", action="store_true",
@@ -370,7 +372,7 @@ def run_ours(args, rank, world):
         args.no_alt = True
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
                        precision=args.precision, seed=rank if split is None else 0, offload_v=args.offload,
-                       head_split=split, dense_layers=args.dense_layers)
+                       head_split=split, dense_layers=args.dense_layers, gemm=args.gemm)
     units = world if split is None else 1  # replicas: every rank decodes its own sequences
     eng.init_history()
     first_token(eng)

@@ -74,12 +74,13 @@ class DecodeEngine:
     fused: batch <= 4 runs the projections through ap_gemv with the neighbouring elementwise ops
     fused (RMSNorm prologues, SiLU-gate epilogue, LM head + greedy argmax) and the down projection
     as a plain ap_gemv.  fused=False keeps one library GEMM + one elementwise kernel per op.
+    gemm: "auto" (library GEMM above batch 4) or "tc" (ap_gemm_tc for batch 5..16).
     """
 
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
                  seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0,
-                 fused: bool = True):
+                 fused: bool = True, gemm: str = "auto"):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -137,8 +138,11 @@ class DecodeEngine:
         self.fused = fused and S <= 4
         # ap_gemv ARGMAX (batch <= 4) / ap_argmax_rows (larger batches) workspace
         self.argws = torch.zeros(max(48, _lib.fn("ap_argmax_workspace_bytes")(S)), dtype=torch.uint8, device=dev)
-        # batch 5..16: projections on the tcgen05 skinny GEMM (ap_gemm_tc); larger batches: library GEMM
-        self.tc = not self.fused and S <= 16
+        # gemm="tc": batch 5..16 projections on the tcgen05 skinny GEMM (ap_gemm_tc).  Default off: in the
+        # batch-8 step the library GEMM measured faster (1437 vs 1358 tok/s)
+        if gemm not in ("auto", "tc"):
+            raise ConfigError("gemm must be 'auto' or 'tc'")
+        self.tc = gemm == "tc" and not self.fused and S <= 16
         self.tcws = None
         if self.tc:
             need = max(_lib.fn("ap_gemm_tc_workspace_bytes")(n, k, S)

@@ -29,14 +29,12 @@ def main():
     ap.add_argument("--model", default="llama-3.1-8b")
     ap.add_argument("--precision", default="fp16x3")
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--no-tc", action="store_true", help="batch 5..16: library GEMMs instead of ap_gemm_tc")
+    ap.add_argument("--gemm", choices=["auto", "tc"], default="auto")
     args = ap.parse_args()
     shape = SHAPES[args.model]
     G = shape.n_q_heads // shape.n_kv_heads
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=64, cfg=SelectorConfig(budget=1024),
-                       group=1 if args.group == "head" else G, precision=args.precision)
-    if args.no_tc:
-        eng.tc = False
+                       group=1 if args.group == "head" else G, precision=args.precision, gemm=args.gemm)
     eng.init_history()
     eng.step(use_graph=False)
     eng.capture_all()

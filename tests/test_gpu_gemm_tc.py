@@ -88,7 +88,7 @@ def test_engine_tc_matches_library_gemm():
     from paper_2502_04077_b200.decode import DecodeEngine, ModelShape
     sh = ModelShape("tiny", n_layers=2, hidden=1024, n_q_heads=8, n_kv_heads=2, ffn=2816, vocab=4096,
                      rope_theta=500000.0)
-    a = DecodeEngine(sh, 8, 2048, 8, mode="dense", seed=3)
+    a = DecodeEngine(sh, 8, 2048, 8, mode="dense", seed=3, gemm="tc")
     assert a.tc
     b = DecodeEngine(sh, 8, 2048, 8, mode="dense", seed=3)
     b.tc = False
