@@ -31,6 +31,7 @@ namespace ap {
 constexpr int HD = 128;                 // head dim
 constexpr int ATT_THREADS = 256;        // 8 warps
 constexpr int ATT_WARPS = ATT_THREADS / 32;
+constexpr int KV_STAGE = 2 * 16 * 128 * 2;  // one 16-token block of K and of V, bf16 (sparse cluster staging)
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ long long g_att_trace[16 * 16];  // debug: clock64 per phase, CTAs (split, 0, 0)
@@ -114,16 +115,29 @@ __device__ __forceinline__ void load_block(const __nv_bfloat16* kh, const __nv_b
     }
 }
 
+// KSrc / VSrc: jj -> the 16 bytes (8 dims) of token jj*2 + half this lane holds (registers, or
+// shared memory read just in time)
+template <int NH, bool WITH_V, bool EMIT, typename KSrc, typename VSrc, typename Take, typename BmOut>
+__device__ __forceinline__ void compute_block_src(KSrc kv, VSrc vv, int64_t j, int b, const float (&qf)[NH][8],
+                                                  WarpState<NH, WITH_V>& st, Take take, BmOut bm_out);
+
 template <int NH, bool WITH_V, bool EMIT, typename Take, typename BmOut>
 __device__ __forceinline__ void compute_block(const uint4 (&kv)[8], const uint4 (&vv)[8], int64_t j, int b,
                                               const float (&qf)[NH][8], WarpState<NH, WITH_V>& st, Take take,
                                               BmOut bm_out) {
+    compute_block_src<NH, WITH_V, EMIT>([&](int jj) { return kv[jj]; }, [&](int jj) { return vv[jj]; }, j, b, qf,
+                                        st, take, bm_out);
+}
+
+template <int NH, bool WITH_V, bool EMIT, typename KSrc, typename VSrc, typename Take, typename BmOut>
+__device__ __forceinline__ void compute_block_src(KSrc kv, VSrc vv, int64_t j, int b, const float (&qf)[NH][8],
+                                                  WarpState<NH, WITH_V>& st, Take take, BmOut bm_out) {
     const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
     float d[NH][8];
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
         float kf[8];
-        bf16x8_to_f32(kv[jj], kf);
+        bf16x8_to_f32(kv(jj), kf);
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
             float a = 0.f;
@@ -196,7 +210,7 @@ __device__ __forceinline__ void compute_block(const uint4 (&kv)[8], const uint4 
             }
             if (!nz) continue;  // unselected / beyond t: never touch its V (may be garbage)
             float vf[8];
-            bf16x8_to_f32(vv[jj], vf);  // once per token, shared by every head
+            bf16x8_to_f32(vv(jj), vf);  // once per token, shared by every head
 #pragma unroll
             for (int h = 0; h < NH; ++h)
 #pragma unroll
@@ -567,6 +581,151 @@ __device__ void merge_warps_to_smem(WarpState<NH, true>& st, float* scratch, flo
     }
 }
 
+// ------------------------------------------------------------------ tensor-core block path
+// (sparse cluster kernel) One warp, one 16-token block, all NH <= 8 q-heads of the map:
+// S = Q Kᵀ and O += P V as mma.sync m16n8k16 (bf16 in, fp32 accumulate); rows = q-heads (NH real
+// of 16), K/V read from the warp's shared-memory stage with ldmatrix.  The stage holds K then V,
+// each as two TMA boxes {64 dims, 16 tokens} in the 128-byte-swizzled layout (16-byte chunk c of
+// token row r at chunk c ^ (r & 7)), so the 8 rows of every ldmatrix fragment hit distinct banks.
+// Thread (g = lane/4, t = lane%4) holds row g.
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+// d += A(16x16, rows g / g+8) B(16x8); a1 = a3 = 0 (rows 8-15 are padding)
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+                 "{%0, %1, %2, %3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+struct MmaState {
+    float m, l;       // row g's running max (log2 units) and sum, replicated over the quad
+    float o[16][4];   // O row g (o[nt][0..1] = dims nt*8 + 2t, +1); [2..3] = padding rows
+    __device__ void init() {
+        m = -INFINITY;
+        l = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[nt][e] = 0.f;
+    }
+};
+
+// kb / vb: the block's K / V tile in shared memory (two swizzled 2 KB halves each).
+// qa[kk][0/1]: the Q A-fragment (a0, a2) of k-step kk (zero for rows >= NH).
+template <int NH, bool EMIT, typename Take, typename BmOut>
+__device__ __forceinline__ void block_mma(uint32_t kb, uint32_t vb, int64_t j, int b, const uint32_t (&qa)[8][2],
+                                          float qscale, MmaState& st, Take take, BmOut bm_out) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, mi = lane >> 3, r = lane & 7;
+    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    // K fragments: matrices (tokens 0-7 | 8-15) x (dims +0..7 | +8..15) of k-step kk
+    const uint32_t krow = kb + (uint32_t)((((mi >> 1) << 3) | r) * 128);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+        uint32_t bk[4];
+        const int c = ((kk & 3) << 1) | (mi & 1);
+        ldsm_x4(krow + (kk >> 2) * 2048 + ((c ^ r) << 4), bk);
+        mma_bf16_16816(sc[0], qa[kk][0], qa[kk][1], bk[0], bk[1]);
+        mma_bf16_16816(sc[1], qa[kk][0], qa[kk][1], bk[2], bk[3]);
+    }
+    const bool real = g < NH;
+    float s[4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int64_t p = j * b + nt * 8 + 2 * t + e;
+            const float v = (real && take(p)) ? sc[nt][e] * qscale : -INFINITY;
+            s[nt * 2 + e] = v;
+            mx = fmaxf(mx, v);
+        }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    if constexpr (EMIT) {
+        if (real && t == 0) bm_out(g, mx);
+    }
+    float pr[4] = {0.f, 0.f, 0.f, 0.f};
+    float corr = 1.f;
+    if (mx != -INFINITY) {  // quad-uniform
+        const float m_new = fmaxf(st.m, mx);
+        corr = exp2f(st.m - m_new);  // 0 when st.m = -inf
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pr[e] = exp2f(s[e] - m_new);  // 0 for masked tokens
+        st.m = m_new;
+    }
+    float rs = (pr[0] + pr[1]) + (pr[2] + pr[3]);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+    st.l = st.l * corr + rs;
+    const bool any = __any_sync(0xffffffffu, mx != -INFINITY);
+    if (!any) return;  // nothing selected in this block for any head: never touch its V
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+        st.o[nt][0] *= corr;
+        st.o[nt][1] *= corr;
+    }
+    const uint32_t a0 = pack_bf16x2(pr[0], pr[1]), a2 = pack_bf16x2(pr[2], pr[3]);
+    // V fragments (transposed): matrices (tokens 0-7 | 8-15) x (dims n0 + 0..7 | n0 + 8..15)
+    const uint32_t vrow = vb + (uint32_t)((((mi & 1) << 3) | r) * 128);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        uint32_t bv[4];
+        const int c = ((q & 3) << 1) | (mi >> 1);
+        ldsm_x4_t(vrow + (q >> 2) * 2048 + ((c ^ r) << 4), bv);
+        mma_bf16_16816(st.o[2 * q], a0, a2, bv[0], bv[1]);
+        mma_bf16_16816(st.o[2 * q + 1], a0, a2, bv[2], bv[3]);
+    }
+}
+
+// CTA merge of the warps' MmaStates into cpart[h] = (max, sum, acc[128]) (same result layout as
+// merge_warps_to_smem).
+template <int NH>
+__device__ void merge_mma_to_smem(const MmaState& st, float* scratch, float (*cpart)[HD + 2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+    if (g < NH) {
+        float* w = scratch + (warp * NH + g) * (HD + 2);
+        if (t == 0) {
+            w[0] = st.m;
+            w[1] = st.l;
+        }
+#pragma unroll
+        for (int nt = 0; nt < 16; ++nt) {
+            w[2 + nt * 8 + 2 * t] = st.o[nt][0];
+            w[2 + nt * 8 + 2 * t + 1] = st.o[nt][1];
+        }
+    }
+    __syncthreads();
+    __shared__ float s_scale[NH][ATT_WARPS];
+    if (threadIdx.x < NH * ATT_WARPS) {
+        const int h = threadIdx.x / ATT_WARPS, ww = threadIdx.x % ATT_WARPS;
+        float M = -INFINITY;
+#pragma unroll
+        for (int v = 0; v < ATT_WARPS; ++v) M = fmaxf(M, scratch[(v * NH + h) * (HD + 2)]);
+        const float mw = scratch[(ww * NH + h) * (HD + 2)];
+        s_scale[h][ww] = mw == -INFINITY ? 0.f : exp2f(mw - M);
+        if (ww == 0) cpart[h][0] = M;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < NH * (HD + 1); idx += ATT_THREADS) {
+        const int h = idx / (HD + 1), e = 1 + idx % (HD + 1);  // l and the 128 accumulators
+        float val = 0.f;
+#pragma unroll
+        for (int ww = 0; ww < ATT_WARPS; ++ww) val = fmaf(scratch[(ww * NH + h) * (HD + 2) + e], s_scale[h][ww], val);
+        cpart[h][e] = val;
+    }
+}
+
 // DSMEM push helpers: 32-bit shared::cluster address of a local variable in CTA `rank`, and
 // register -> remote shared memory stores that complete_tx on the receiver's mbarrier.
 __device__ __forceinline__ uint32_t mapa_u32(const void* p, int rank) {
@@ -589,7 +748,9 @@ __device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uin
 // and rank h % CL the accumulators of q-head h; each waits on its own mbarrier only (no cluster-wide
 // barrier on the critical path, nobody reads a peer's shared memory, so no exit barrier either).
 template <int NH, bool EMIT, int CL>
-__global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams P) {
+__global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                                     const __grid_constant__ CUtensorMap vmap,
+                                                                     AttnParams P) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     constexpr int NFIN = (NH + CL - 1) / CL;                // q-heads a rank finalises (at most)
@@ -612,7 +773,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     // then) just before the pushes
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     ATT_TRACE(0);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane & 15;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     pdl_trigger();
     // Until pdl_wait: only data older than the previous kernel (positions, map state and selection,
     // the ring slot being replaced) — q and the newest K/V token come from the kernel just before.
@@ -636,6 +797,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
     const __nv_bfloat16* kh = P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
     const __nv_bfloat16* vh = P.v + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
     float* s_bm = sm_att + ATT_WARPS * NH * (HD + 2);  // [per][NH]
+
     const int Hh = P.sel.history;
     const int slot = (int)(ms.n_pushed % Hh);
     float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
@@ -654,29 +816,6 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
         is_mid = true;
         return mid[u - sb - n_local];
     };
-    for (int u = u0 + warp; u < u1; u += ATT_WARPS) {  // K/V of this CTA's blocks into L2 (8 KB each)
-        bool is_mid;
-        const int64_t j = block_of(u, is_mid);
-        const char* kb = reinterpret_cast<const char*>(kh + j * b * HD);
-        const char* vb = reinterpret_cast<const char*>(vh + j * b * HD);
-        prefetch_l2(kb + lane * 128);
-        if (!P.paged) prefetch_l2(vb + lane * 128);
-    }
-    ATT_TRACE(1);
-    pdl_wait();
-    const float qscale = LOG2E * rsqrtf((float)HD);
-    ATT_TRACE(2);
-    float qf[NH][8];
-#pragma unroll
-    for (int h = 0; h < NH; ++h) {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(P.q + ((int64_t)s * P.n_q_heads + h0 + h) * HD + sub * 8));
-        bf16x8_to_f32(u, qf[h]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) qf[h][i] *= qscale;
-    }
-    WarpState<NH, true> st;
-    st.init();
-    const int64_t mid_clip = ms.mid_clip;
     auto v_of = [&](int u, int64_t j, bool is_mid) -> const __nv_bfloat16* {
         if (!P.paged) return vh;
         // page of block j: sink | recent ring | middle page (prefetched, kernel 5); rebased so that
@@ -689,19 +828,104 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(AttnParams 
         else page = P.vp.sink_pages + (int)(j % P.vp.recent_pages);
         return reinterpret_cast<const __nv_bfloat16*>(P.vp.pages) + ((vmap * npg + page) * 16 - j * b) * HD;
     };
-    for (int u = u0 + warp; u < u1; u += ATT_WARPS) {
+    // K/V staging: each warp owns a 2-slot ring of 8 KB (K block | V block) filled by cp.async.bulk,
+    // so the next block's copy is in flight while this one is computed.  The first two blocks are
+    // requested before the programmatic-dependent-launch wait unless they hold the newest token
+    // (written by the kernel just before) or their V lives in the prefetched pages.
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_bm + per * NH) + 1023) & ~uintptr_t(1023));
+    uint8_t* my_ring = ring + warp * 2 * KV_STAGE;
+    __shared__ __align__(8) uint64_t s_kvbar[ATT_WARPS][2];
+    if (lane == 0) {
+        mbar_init(&s_kvbar[warp][0], 1);
+        mbar_init(&s_kvbar[warp][1], 1);
+    }
+    __syncwarp();
+    auto issue = [&](int slot, int u) {  // whole warp (lane 0 issues): four TMA boxes {64 dims, 16 tokens}
         bool is_mid;
         const int64_t j = block_of(u, is_mid);
-        auto take = [&](int64_t p) {
-            if (p >= t) return false;
-            if (p < sink_end || p >= local_start) return true;
-            return is_mid && p < mid_clip;
-        };
-        process_block<NH, true, EMIT>(kh, v_of(u, j, is_mid), j, b, qf, st, take,
-                                      [&](int h, float v) { if (lane == 0) s_bm[(u - u0) * NH + h] = v; });
+        if (lane == 0) {
+            uint8_t* d = my_ring + slot * KV_STAGE;
+            const int krow = (int)(((int64_t)s * P.n_kv_heads + kvh) * P.t_max + j * b);
+            int vrow = krow;
+            if (P.paged) {  // page of block j (as v_of), row index in the page store
+                const int64_t vm = ((int64_t)P.layer * P.n_seq + s) * P.n_kv_heads + kvh;
+                const int npg = P.vp.sink_pages + P.vp.recent_pages + P.vp.k_cap;
+                int page;
+                if (is_mid) page = P.vp.sink_pages + P.vp.recent_pages + P.vp.mid_page[vm * P.vp.k_cap + (u - sb - n_local)];
+                else if (j < P.vp.sink_pages) page = (int)j;
+                else page = P.vp.sink_pages + (int)(j % P.vp.recent_pages);
+                vrow = (int)((vm * npg + page) * 16);
+            }
+            mbar_arrive_tx(&s_kvbar[warp][slot], KV_STAGE);
+            tma_load_2d(d, &kmap, 0, krow, &s_kvbar[warp][slot]);
+            tma_load_2d(d + 2048, &kmap, 64, krow, &s_kvbar[warp][slot]);
+            tma_load_2d(d + 4096, &vmap, 0, vrow, &s_kvbar[warp][slot]);
+            tma_load_2d(d + 6144, &vmap, 64, vrow, &s_kvbar[warp][slot]);
+        }
+    };
+    bool issued[2] = {false, false};
+    if (!P.paged)
+        for (int i = 0; i < 2; ++i) {
+            const int u = u0 + warp + i * ATT_WARPS;
+            if (u >= u1) break;
+            bool is_mid;
+            if (block_of(u, is_mid) == eb - 1) continue;
+            issue(i, u);
+            issued[i] = true;
+        }
+    for (int u = u0 + warp + 2 * ATT_WARPS; u < u1; u += ATT_WARPS) {  // later blocks into L2 (8 KB each)
+        bool is_mid;
+        const int64_t j = block_of(u, is_mid);
+        const char* kb = reinterpret_cast<const char*>(kh + j * b * HD);
+        const char* vb = reinterpret_cast<const char*>(vh + j * b * HD);
+        prefetch_l2(kb + lane * 128);
+        if (!P.paged) prefetch_l2(vb + lane * 128);
+    }
+    ATT_TRACE(1);
+    pdl_wait();
+    const float qscale = LOG2E * rsqrtf((float)HD);
+    ATT_TRACE(2);
+    uint32_t qa[8][2];  // Q A-fragments (row g = q-head h0 + g), zero for padding rows
+    {
+        const int g = lane >> 2, t = lane & 3;
+        const uint32_t* qrow = reinterpret_cast<const uint32_t*>(P.q + ((int64_t)s * P.n_q_heads + h0 + (g < NH ? g : 0)) * HD);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            qa[kk][0] = g < NH ? qrow[kk * 8 + t] : 0u;
+            qa[kk][1] = g < NH ? qrow[kk * 8 + 4 + t] : 0u;
+        }
+    }
+    MmaState st;
+    st.init();
+    const int64_t mid_clip = ms.mid_clip;
+    for (int i = 0; i < 2; ++i) {
+        const int u = u0 + warp + i * ATT_WARPS;
+        if (u < u1 && !issued[i]) issue(i, u);
+    }
+    {
+        int i = 0;
+        for (int u = u0 + warp; u < u1; u += ATT_WARPS, ++i) {
+            bool is_mid;
+            const int64_t j = block_of(u, is_mid);
+            auto take = [&](int64_t p) {
+                if (p >= t) return false;
+                if (p < sink_end || p >= local_start) return true;
+                return is_mid && p < mid_clip;
+            };
+            const int slot = i & 1;
+            mbar_wait(&s_kvbar[warp][slot], (uint32_t)((i >> 1) & 1));
+            const uint32_t kb = smem_u32(my_ring + slot * KV_STAGE);
+            block_mma<NH, EMIT>(kb, kb + KV_STAGE / 2, j, b, qa, qscale, st, take,
+                                [&](int h, float v) { s_bm[(u - u0) * NH + h] = v; });
+            __syncwarp();
+            if (u + 2 * ATT_WARPS < u1) {  // refill this slot with the block after next
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(slot, u + 2 * ATT_WARPS);
+            }
+        }
     }
     ATT_TRACE(3);
-    merge_warps_to_smem<NH>(st, sm_att, cpart);
+    merge_mma_to_smem<NH>(st, sm_att, cpart);
     __syncthreads();
     ATT_TRACE(4);
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -788,17 +1012,31 @@ static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream
 }
 
 template <int NH, bool EMIT, int CL>
-static void launch_cluster(const AttnParams& P, cudaStream_t st) {
+static int launch_cluster(const AttnParams& P, cudaStream_t st) {
     const int units_max = (P.sel.sink + P.block - 1) / P.block + P.sel.local / P.block + 2 + P.sel.k_mid;
-    const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * NH) * sizeof(float);
+    const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * NH) * sizeof(float) +
+                      1024 + (size_t)ATT_WARPS * 2 * KV_STAGE;  // + the per-warp K/V staging rings (128 KB)
     auto k = sparse_cluster_kernel<NH, EMIT, CL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (CL > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    launch_ex(k, dim3(CL, P.n_q_heads / NH, P.n_seq), dim3(ATT_THREADS), sm, st, CL, P);
+    // K (and V, or the offload page store) as [rows][128] bf16 for {64, 16} TMA boxes
+    CUtensorMap kmap, vmap;
+    const uint64_t kv_rows = (uint64_t)P.n_seq * P.n_kv_heads * P.t_max;
+    bool ok = make_tmap_bf16_sw128(&kmap, P.k, kv_rows, HD, 16);
+    if (P.paged) {
+        const uint64_t npg = (uint64_t)(P.vp.sink_pages + P.vp.recent_pages + P.vp.k_cap);
+        ok = ok && make_tmap_bf16_sw128(&vmap, P.vp.pages, (uint64_t)(P.layer + 1) * P.n_seq * P.n_kv_heads * npg * 16,
+                                        HD, 16);
+    } else {
+        ok = ok && make_tmap_bf16_sw128(&vmap, P.v, kv_rows, HD, 16);
+    }
+    AP_REQUIRE(ok, AP_ECUDA, "tensor map for the sparse attention failed");
+    launch_ex(k, dim3(CL, P.n_q_heads / NH, P.n_seq), dim3(ATT_THREADS), sm, st, CL, kmap, vmap, P);
+    return AP_OK;
 }
 
 template <int NH>
-static void launch_sparse(const AttnParams& P, bool emit, cudaStream_t st) {
+static int launch_sparse(const AttnParams& P, bool emit, cudaStream_t st) {
     switch (P.n_splits) {  // cluster form: the splits of a map are one thread-block cluster
         case 2: return emit ? launch_cluster<NH, true, 2>(P, st) : launch_cluster<NH, false, 2>(P, st);
         case 4: return emit ? launch_cluster<NH, true, 4>(P, st) : launch_cluster<NH, false, 4>(P, st);
@@ -810,6 +1048,7 @@ static void launch_sparse(const AttnParams& P, bool emit, cudaStream_t st) {
     const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
     if (emit) sparse_partial_kernel<NH, true><<<grid, ATT_THREADS, sm, st>>>(P);
     else sparse_partial_kernel<NH, false><<<grid, ATT_THREADS, sm, st>>>(P);
+    return AP_OK;
 }
 
 static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
@@ -1231,11 +1470,12 @@ int ap_attn_sparse_paged(const ap_attn_layer* a, const ap_selector* sel, int32_t
     P.with_v = 1; P.emit = emit; P.sparse_units = 1;
     cudaStream_t st = as_stream(stream);
     switch (P.group) {
-        case 1: launch_sparse<1>(P, emit, st); break;
-        case 2: launch_sparse<2>(P, emit, st); break;
-        case 4: launch_sparse<4>(P, emit, st); break;
-        default: launch_sparse<8>(P, emit, st); break;
+        case 1: rc = launch_sparse<1>(P, emit, st); break;
+        case 2: rc = launch_sparse<2>(P, emit, st); break;
+        case 4: rc = launch_sparse<4>(P, emit, st); break;
+        default: rc = launch_sparse<8>(P, emit, st); break;
     }
+    if (rc != AP_OK) return rc;
     return launch_status("sparse_partial_kernel");
 }
 
