@@ -828,14 +828,18 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
         else page = P.vp.sink_pages + (int)(j % P.vp.recent_pages);
         return reinterpret_cast<const __nv_bfloat16*>(P.vp.pages) + ((vmap * npg + page) * 16 - j * b) * HD;
     };
-    // K/V staging: each warp owns a 2-slot ring of 8 KB (K block | V block) filled by cp.async.bulk,
-    // so the next block's copy is in flight while this one is computed.  The first two blocks are
-    // requested before the programmatic-dependent-launch wait unless they hold the newest token
-    // (written by the kernel just before) or their V lives in the prefetched pages.
+    // NH >= 2 (q-heads sharing a map): tensor-core path.  K/V staging: each warp owns a 2-slot ring
+    // of 8 KB (K block | V block) filled by TMA, so the next block's copy is in flight while this one
+    // is computed.  The first two blocks are requested before the programmatic-dependent-launch wait
+    // unless they hold the newest token (written by the kernel just before) or their V lives in the
+    // prefetched pages.  NH == 1 (one map per q-head): the SIMT path (one MMA row of 16 would be
+    // busy) with the blocks prefetched into L2 and no staging, so the kernel's small shared-memory
+    // footprint lets the next projection's CTAs start on the same SMs.
+    constexpr bool TC = NH >= 2;
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_bm + per * NH) + 1023) & ~uintptr_t(1023));
     uint8_t* my_ring = ring + warp * 2 * KV_STAGE;
     __shared__ __align__(8) uint64_t s_kvbar[ATT_WARPS][2];
-    if (lane == 0) {
+    if (TC && lane == 0) {
         mbar_init(&s_kvbar[warp][0], 1);
         mbar_init(&s_kvbar[warp][1], 1);
     }
@@ -864,7 +868,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
         }
     };
     bool issued[2] = {false, false};
-    if (!P.paged)
+    if (TC && !P.paged)
         for (int i = 0; i < 2; ++i) {
             const int u = u0 + warp + i * ATT_WARPS;
             if (u >= u1) break;
@@ -873,7 +877,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
             issue(i, u);
             issued[i] = true;
         }
-    for (int u = u0 + warp + 2 * ATT_WARPS; u < u1; u += ATT_WARPS) {  // later blocks into L2 (8 KB each)
+    for (int u = u0 + warp + (TC ? 2 * ATT_WARPS : 0); u < u1; u += ATT_WARPS) {  // blocks into L2 (8 KB each)
         bool is_mid;
         const int64_t j = block_of(u, is_mid);
         const char* kb = reinterpret_cast<const char*>(kh + j * b * HD);
@@ -885,37 +889,40 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
     pdl_wait();
     const float qscale = LOG2E * rsqrtf((float)HD);
     ATT_TRACE(2);
-    uint32_t qa[8][2];  // Q A-fragments (row g = q-head h0 + g), zero for padding rows
-    {
-        const int g = lane >> 2, t = lane & 3;
-        const uint32_t* qrow = reinterpret_cast<const uint32_t*>(P.q + ((int64_t)s * P.n_q_heads + h0 + (g < NH ? g : 0)) * HD);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-            qa[kk][0] = g < NH ? qrow[kk * 8 + t] : 0u;
-            qa[kk][1] = g < NH ? qrow[kk * 8 + 4 + t] : 0u;
-        }
-    }
-    MmaState st;
-    st.init();
     const int64_t mid_clip = ms.mid_clip;
-    for (int i = 0; i < 2; ++i) {
-        const int u = u0 + warp + i * ATT_WARPS;
-        if (u < u1 && !issued[i]) issue(i, u);
-    }
-    {
+    auto take_of = [&](bool is_mid) {
+        return [=](int64_t p) {
+            if (p >= t) return false;
+            if (p < sink_end || p >= local_start) return true;
+            return is_mid && p < mid_clip;
+        };
+    };
+    if constexpr (TC) {
+        uint32_t qa[8][2];  // Q A-fragments (row g = q-head h0 + g), zero for padding rows
+        {
+            const int g = lane >> 2, t4 = lane & 3;
+            const uint32_t* qrow =
+                reinterpret_cast<const uint32_t*>(P.q + ((int64_t)s * P.n_q_heads + h0 + (g < NH ? g : 0)) * HD);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                qa[kk][0] = g < NH ? qrow[kk * 8 + t4] : 0u;
+                qa[kk][1] = g < NH ? qrow[kk * 8 + 4 + t4] : 0u;
+            }
+        }
+        MmaState st;
+        st.init();
+        for (int i = 0; i < 2; ++i) {
+            const int u = u0 + warp + i * ATT_WARPS;
+            if (u < u1 && !issued[i]) issue(i, u);
+        }
         int i = 0;
         for (int u = u0 + warp; u < u1; u += ATT_WARPS, ++i) {
             bool is_mid;
             const int64_t j = block_of(u, is_mid);
-            auto take = [&](int64_t p) {
-                if (p >= t) return false;
-                if (p < sink_end || p >= local_start) return true;
-                return is_mid && p < mid_clip;
-            };
             const int slot = i & 1;
             mbar_wait(&s_kvbar[warp][slot], (uint32_t)((i >> 1) & 1));
             const uint32_t kb = smem_u32(my_ring + slot * KV_STAGE);
-            block_mma<NH, EMIT>(kb, kb + KV_STAGE / 2, j, b, qa, qscale, st, take,
+            block_mma<NH, EMIT>(kb, kb + KV_STAGE / 2, j, b, qa, qscale, st, take_of(is_mid),
                                 [&](int h, float v) { s_bm[(u - u0) * NH + h] = v; });
             __syncwarp();
             if (u + 2 * ATT_WARPS < u1) {  // refill this slot with the block after next
@@ -923,9 +930,29 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
                 issue(slot, u + 2 * ATT_WARPS);
             }
         }
+        ATT_TRACE(3);
+        merge_mma_to_smem<NH>(st, sm_att, cpart);
+    } else {
+        const int sub = lane & 15;
+        float qf[NH][8];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(P.q + ((int64_t)s * P.n_q_heads + h0 + h) * HD + sub * 8));
+            bf16x8_to_f32(u, qf[h]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) qf[h][i] *= qscale;
+        }
+        WarpState<NH, true> st;
+        st.init();
+        for (int u = u0 + warp; u < u1; u += ATT_WARPS) {
+            bool is_mid;
+            const int64_t j = block_of(u, is_mid);
+            process_block<NH, true, EMIT>(kh, v_of(u, j, is_mid), j, b, qf, st, take_of(is_mid),
+                                          [&](int h, float v) { if (lane == 0) s_bm[(u - u0) * NH + h] = v; });
+        }
+        ATT_TRACE(3);
+        merge_warps_to_smem<NH>(st, sm_att, cpart);
     }
-    ATT_TRACE(3);
-    merge_mma_to_smem<NH>(st, sm_att, cpart);
     __syncthreads();
     ATT_TRACE(4);
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1015,7 +1042,7 @@ template <int NH, bool EMIT, int CL>
 static int launch_cluster(const AttnParams& P, cudaStream_t st) {
     const int units_max = (P.sel.sink + P.block - 1) / P.block + P.sel.local / P.block + 2 + P.sel.k_mid;
     const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * NH) * sizeof(float) +
-                      1024 + (size_t)ATT_WARPS * 2 * KV_STAGE;  // + the per-warp K/V staging rings (128 KB)
+                      (NH >= 2 ? 1024 + (size_t)ATT_WARPS * 2 * KV_STAGE : 0);  // + the K/V staging rings (128 KB)
     auto k = sparse_cluster_kernel<NH, EMIT, CL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (CL > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
