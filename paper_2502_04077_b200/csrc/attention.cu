@@ -809,12 +809,16 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
         for (int64_t j = z0 + threadIdx.x; j < z1; j += ATT_THREADS) dst[j] = 0.f;
         if (split == 0 && threadIdx.x == 0) P.sel.slot_xmax[(int64_t)map * Hh + slot] = 0.f;  // atomicMax'd later
     }
+    // block id of each of this CTA's units (sink | local | middle), gathered once into shared memory
+    int* s_blk = reinterpret_cast<int*>(s_bm + per * NH);
+    for (int i = threadIdx.x; i < u1 - u0; i += ATT_THREADS) {
+        const int u = u0 + i;
+        s_blk[i] = u < sb ? u : (u < sb + n_local ? (int)(lb + (u - sb)) : mid[u - sb - n_local]);
+    }
+    __syncthreads();
     auto block_of = [&](int u, bool& is_mid) -> int64_t {
-        is_mid = false;
-        if (u < sb) return u;
-        if (u < sb + n_local) return lb + (u - sb);
-        is_mid = true;
-        return mid[u - sb - n_local];
+        is_mid = u >= sb + n_local;
+        return s_blk[u - u0];
     };
     auto v_of = [&](int u, int64_t j, bool is_mid) -> const __nv_bfloat16* {
         if (!P.paged) return vh;
@@ -836,7 +840,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
     // busy) with the blocks prefetched into L2 and no staging, so the kernel's small shared-memory
     // footprint lets the next projection's CTAs start on the same SMs.
     constexpr bool TC = NH >= 2;
-    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_bm + per * NH) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_blk + per) + 1023) & ~uintptr_t(1023));
     uint8_t* my_ring = ring + warp * 2 * KV_STAGE;
     __shared__ __align__(8) uint64_t s_kvbar[ATT_WARPS][2];
     if (TC && lane == 0) {
@@ -1041,7 +1045,7 @@ static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream
 template <int NH, bool EMIT, int CL>
 static int launch_cluster(const AttnParams& P, cudaStream_t st) {
     const int units_max = (P.sel.sink + P.block - 1) / P.block + P.sel.local / P.block + 2 + P.sel.k_mid;
-    const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * NH) * sizeof(float) +
+    const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * (NH + 1)) * sizeof(float) +
                       (NH >= 2 ? 1024 + (size_t)ATT_WARPS * 2 * KV_STAGE : 0);  // + the K/V staging rings (128 KB)
     auto k = sparse_cluster_kernel<NH, EMIT, CL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
