@@ -37,6 +37,12 @@ def sparse_splits(n_maps: int, sm_count: int) -> int:
     return cl
 
 
+def dense_splits(n_units: int, sm_count: int, t_max: int) -> int:
+    """Flash-decoding splits of the dense pass for n_units (sequence, KV head) pairs per launch: one
+    wave of the tensor-core kernel (one CTA per SM), at most one split per 1024 positions."""
+    return max(1, min(t_max // 1024, sm_count // max(1, n_units)))
+
+
 class DecodeAttention:
     """Workspaces + launchers for one layer shape (reused by every layer of a model).
 

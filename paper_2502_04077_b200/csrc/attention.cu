@@ -726,6 +726,98 @@ __device__ void merge_mma_to_smem(const MmaState& st, float* scratch, float (*cp
     }
 }
 
+// Dense pass on tensor cores (output path, NH >= 2): grid (n_splits, Hkv, S) as dense_partial_kernel,
+// each warp streaming its blocks through a 2-slot TMA ring (K/V boxes as in the sparse cluster
+// kernel) into block_mma; partials combined by the last split (combine_heads).
+template <int NH, bool EMIT>
+__global__ void __launch_bounds__(ATT_THREADS, 1) dense_tc_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                               const __grid_constant__ CUtensorMap vmap,
+                                                               AttnParams P) {
+    extern __shared__ float sm_att[];  // [warps][NH][HD+2] merge scratch, then the staging rings
+    __shared__ float cpart[NH][HD + 2];
+    __shared__ __align__(8) uint64_t s_kvbar[ATT_WARPS][2];
+    const int split = blockIdx.x, kvh = blockIdx.y, s = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t t = P.seq_len[s];
+    const int b = P.block;
+    const int64_t nblk = (t + b - 1) / b;
+    const int64_t blk_per_split = (((int64_t)P.t_max + b - 1) / b + P.n_splits - 1) / P.n_splits;
+    const int64_t j0 = split * blk_per_split, j1 = min(nblk, j0 + blk_per_split);
+    const int h0 = kvh * NH;
+    uint8_t* ring = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(sm_att + ATT_WARPS * NH * (HD + 2)) + 1023) & ~uintptr_t(1023));
+    uint8_t* my_ring = ring + warp * 2 * KV_STAGE;
+    if (lane == 0) {
+        mbar_init(&s_kvbar[warp][0], 1);
+        mbar_init(&s_kvbar[warp][1], 1);
+    }
+    __syncwarp();
+    pdl_trigger();
+    const int row0 = (int)(((int64_t)s * P.n_kv_heads + kvh) * P.t_max);
+    auto issue = [&](int slot, int64_t j) {
+        if (lane == 0) {
+            uint8_t* d = my_ring + slot * KV_STAGE;
+            const int row = row0 + (int)(j * b);
+            mbar_arrive_tx(&s_kvbar[warp][slot], KV_STAGE);
+            tma_load_2d(d, &kmap, 0, row, &s_kvbar[warp][slot]);
+            tma_load_2d(d + 2048, &kmap, 64, row, &s_kvbar[warp][slot]);
+            tma_load_2d(d + 4096, &vmap, 0, row, &s_kvbar[warp][slot]);
+            tma_load_2d(d + 6144, &vmap, 64, row, &s_kvbar[warp][slot]);
+        }
+    };
+    // the first two blocks of each warp before the programmatic-dependent-launch wait, unless they
+    // hold the newest token (written by the kernel just before)
+    bool issued[2] = {false, false};
+    for (int i = 0; i < 2; ++i) {
+        const int64_t j = j0 + warp + i * ATT_WARPS;
+        if (j < j1 && j != nblk - 1) {
+            issue(i, j);
+            issued[i] = true;
+        }
+    }
+    pdl_wait();
+    const float qscale = LOG2E * rsqrtf((float)HD);
+    uint32_t qa[8][2];
+    {
+        const int g = lane >> 2, t4 = lane & 3;
+        const uint32_t* qrow =
+            reinterpret_cast<const uint32_t*>(P.q + ((int64_t)s * P.n_q_heads + h0 + (g < NH ? g : 0)) * HD);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            qa[kk][0] = g < NH ? qrow[kk * 8 + t4] : 0u;
+            qa[kk][1] = g < NH ? qrow[kk * 8 + 4 + t4] : 0u;
+        }
+    }
+    for (int i = 0; i < 2; ++i) {
+        const int64_t j = j0 + warp + i * ATT_WARPS;
+        if (j < j1 && !issued[i]) issue(i, j);
+    }
+    MmaState st;
+    st.init();
+    float* bm = P.bmax + ((int64_t)s * P.n_q_heads + h0) * P.w_max;
+    int i = 0;
+    for (int64_t j = j0 + warp; j < j1; j += ATT_WARPS, ++i) {
+        const int slot = i & 1;
+        mbar_wait(&s_kvbar[warp][slot], (uint32_t)((i >> 1) & 1));
+        const uint32_t kb = smem_u32(my_ring + slot * KV_STAGE);
+        block_mma<NH, EMIT>(kb, kb + KV_STAGE / 2, j, b, qa, qscale, st, [&](int64_t p) { return p < t; },
+                            [&](int h, float v) { bm[h * (int64_t)P.w_max + j] = v; });
+        __syncwarp();
+        if (j + 2 * ATT_WARPS < j1) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(slot, j + 2 * ATT_WARPS);
+        }
+    }
+    merge_mma_to_smem<NH>(st, sm_att, cpart);
+    __syncthreads();
+    float* part = P.partial + (((int64_t)s * P.n_q_heads + h0) * P.n_splits + split) * (HD + 2);
+    for (int idx = threadIdx.x; idx < NH * (HD + 2); idx += ATT_THREADS) {
+        const int h = idx / (HD + 2), e = idx % (HD + 2);
+        part[h * (int64_t)P.n_splits * (HD + 2) + e] = cpart[h][e];
+    }
+    if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) combine_heads(P, s, h0, NH);
+}
+
 // DSMEM push helpers: 32-bit shared::cluster address of a local variable in CTA `rank`, and
 // register -> remote shared memory stores that complete_tx on the receiver's mbarrier.
 __device__ __forceinline__ uint32_t mapa_u32(const void* p, int rank) {
@@ -1037,6 +1129,19 @@ template <int NH>
 static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream_t st) {
     dim3 grid(P.n_splits, P.n_kv_heads, P.n_seq);
     const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
+    if constexpr (NH >= 2) {
+        if (with_v) {  // tensor-core output path
+            CUtensorMap kmap, vmap;
+            const uint64_t rows = (uint64_t)P.n_seq * P.n_kv_heads * P.t_max;
+            if (make_tmap_bf16_sw128(&kmap, P.k, rows, HD, 16) && make_tmap_bf16_sw128(&vmap, P.v, rows, HD, 16)) {
+                const size_t smtc = sm + 1024 + (size_t)ATT_WARPS * 2 * KV_STAGE;
+                auto k = emit ? dense_tc_kernel<NH, true> : dense_tc_kernel<NH, false>;
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smtc);
+                launch_ex(k, grid, dim3(ATT_THREADS), smtc, st, 1, kmap, vmap, P);
+                return;
+            }
+        }
+    }
     if (with_v && emit) launch_ex(dense_partial_kernel<NH, true, true>, grid, dim3(ATT_THREADS), sm, st, 1, P);
     else if (with_v) launch_ex(dense_partial_kernel<NH, true, false>, grid, dim3(ATT_THREADS), sm, st, 1, P);
     else launch_ex(dense_partial_kernel<NH, false, true>, grid, dim3(ATT_THREADS), sm, st, 1, P);

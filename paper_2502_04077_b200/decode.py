@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 from . import _device as D
 from . import _lib
-from .attention import DecodeAttention, sparse_splits
+from .attention import DecodeAttention, dense_splits, sparse_splits
 from .batched import BatchedSelector
 from .errors import ConfigError
 from .predictor import PredictorWeights, init_weights, install_weights
@@ -161,7 +161,8 @@ class DecodeEngine:
         self.logits = torch.zeros(S, V, dtype=bf, device=dev)
         self.seq_len = torch.full((S,), ctx_len, dtype=torch.int32, device=dev)
         self.maps_per_layer = Hq // group
-        self.att = DecodeAttention(S, Hq, Hkv, self.t_max, n_splits_dense=min(64, self.t_max // 1024),
+        self.att = DecodeAttention(S, Hq, Hkv, self.t_max,
+                                   n_splits_dense=dense_splits(S * Hkv, _lib.fn("ap_device_sm_count")(), self.t_max),
                                    n_splits_sparse=sparse_splits(S * self.maps_per_layer,
                                                                  _lib.fn("ap_device_sm_count")()), device=dev)
         self.sel = None

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--splits", type=int, default=8)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--dense-splits", type=int, default=0, help="0: attention.dense_splits rule")
     args = ap.parse_args()
     S, Hq, Hkv, L = args.batch, 32, 8, args.layers
     t_max = -(-(args.t + 16) // 1024) * 1024
@@ -53,7 +54,10 @@ def main():
         st[m]["mid_clip"] = args.t - 1
         sel.mid_blocks[m, : len(blk)] = torch.tensor(blk, dtype=torch.int32)
     sel.state.copy_(torch.from_numpy(st.view(np.uint8).copy()))
-    att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_dense=min(64, t_max // 1024), n_splits_sparse=args.splits)
+    from paper_2502_04077_b200 import _lib
+    from paper_2502_04077_b200.attention import dense_splits
+    nsd = args.dense_splits or dense_splits(S * Hkv, _lib.fn("ap_device_sm_count")(), t_max)
+    att = DecodeAttention(S, Hq, Hkv, t_max, n_splits_dense=nsd, n_splits_sparse=args.splits)
 
     def timeit(fn):
         """GPU time per launch: the L launches (one per layer) captured in a CUDA graph, replayed."""
@@ -88,7 +92,7 @@ def main():
     res["calib_us"] = timeit(lambda l: att.dense(q, k[l], k[l], seq_len, None, with_v=False, emit=True, selector=sel,
                                                  map_base=l * maps, maps_per_seq=L * maps, group=G))
     res["calib_GBps"] = dense_bytes / 2 / (res["calib_us"] * 1e-6) / 1e9
-    res.update(batch=S, t=args.t, group=args.group, sparse_bytes=sparse_bytes, dense_bytes=dense_bytes)
+    res.update(batch=S, dense_splits=nsd, t=args.t, group=args.group, sparse_bytes=sparse_bytes, dense_bytes=dense_bytes)
     print(json.dumps({k_: (round(v_, 2) if isinstance(v_, float) else v_) for k_, v_ in res.items()}))
 
 
