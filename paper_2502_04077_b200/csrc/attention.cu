@@ -391,17 +391,20 @@ __device__ void combine_heads(const AttnParams& P, int s, int h0, int nh) {
 }
 
 // Count this CTA's split as done; the last one (returns true) runs the combine.
+// The counting atomic is acq_rel at gpu scope: after the CTA barrier it releases every thread's
+// partial stores (release is cumulative over what the barrier ordered before it) and, for the last
+// CTA, acquires the other splits' (read back with ld.cg, past L1).  No sequentially-consistent
+// fences: under load they cost microseconds.
 __device__ __forceinline__ bool last_split(int32_t* counter, int n_splits) {
     __shared__ int s_last;
-    __threadfence();  // partials / block maxima visible device-wide before counting
     __syncthreads();
     if (threadIdx.x == 0) {
-        const int prev = atomicAdd(counter, 1);
+        int prev;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
         s_last = (prev == n_splits - 1);
         if (s_last) *counter = 0;  // ready for the next launch (stream-ordered)
     }
     __syncthreads();
-    if (s_last) __threadfence();
     return s_last;
 }
 
@@ -1438,9 +1441,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_c
             const int map = s * P.maps_per_seq + P.map_base + (h0 + threadIdx.x * P.group) / P.group;
             P.sel.slot_xmax[(int64_t)map * Hh + (int)((epoch - 1) % Hh)] = 0.f;
         }
-        __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) atomicExch((int32_t*)ready, (int32_t)epoch);
+        if (threadIdx.x == 0)  // release: the LSE and the xmax resets above, ordered by the barrier
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(ready), "r"((int32_t)epoch) : "memory");
         ATT_TRACE(9);
         for (int g0 = 0; g0 < NH; g0 += P.group) {  // zero the ring row beyond W (rarely any)
             const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;
@@ -1451,10 +1454,15 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_c
         }
     }
     // ---- every split emits the compressed-row values of its own blocks once the LSE is out
-    if (threadIdx.x == 0)
-        while (*ready != (int32_t)epoch) __nanosleep(64);
+    if (threadIdx.x == 0) {
+        int32_t v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
+            if (v == (int32_t)epoch) break;
+            __nanosleep(32);
+        }
+    }
     __syncthreads();
-    __threadfence();
     ATT_TRACE(4);
     if (threadIdx.x < NH)
         s_lse[threadIdx.x] = __ldcg(P.partial + ((int64_t)s * P.n_q_heads + h0 + threadIdx.x) * P.n_splits * (HD + 2) + 2);
