@@ -1132,7 +1132,7 @@ template <int NH>
 static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream_t st) {
     dim3 grid(P.n_splits, P.n_kv_heads, P.n_seq);
     const size_t sm = (size_t)ATT_WARPS * NH * (HD + 2) * sizeof(float);
-    if constexpr (NH >= 2) {
+    {
         if (with_v) {  // tensor-core output path
             CUtensorMap kmap, vmap;
             const uint64_t rows = (uint64_t)P.n_seq * P.n_kv_heads * P.t_max;

@@ -41,11 +41,11 @@ def _selector(n_maps, w_max, budget=1024):
     return BatchedSelector(SelectorConfig(budget=budget), n_maps, w_max)
 
 
-@pytest.mark.parametrize("group", [1, 4])
-def test_dense_attention_and_calibration_row(group):
+@pytest.mark.parametrize("Hq,Hkv,group", [(8, 2, 1), (8, 2, 4), (4, 4, 1)])  # (4, 4): MHA, one q-head per KV head
+def test_dense_attention_and_calibration_row(Hq, Hkv, group):
     import torch
     from paper_2502_04077_b200.attention import DecodeAttention
-    S, Hq, Hkv, t_max = 2, 8, 2, 1024
+    S, t_max = 2, 1024
     q, k, v = _setup(S, Hq, Hkv, t_max)
     lens = [700, 1013]
     seq_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
