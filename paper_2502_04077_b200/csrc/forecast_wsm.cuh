@@ -16,11 +16,17 @@
 namespace ap {
 namespace wsm {
 
-constexpr int NCONV = 10;                   // conv1 warps (16 measured slower: shared-memory port)
+#ifndef AP_WSM_NCONV
+#define AP_WSM_NCONV 10
+#endif
+#ifndef AP_WSM_NX
+#define AP_WSM_NX 4
+#endif
+constexpr int NCONV = AP_WSM_NCONV;         // conv1 warps (16 measured slower: shared-memory port)
 constexpr int MO = 5;                       // output rows per band
 constexpr int MA = MO + 4;                  // a1 tile rows per band (2 segments x (n + 2))
 constexpr int MX = MO + 8;                  // x tile rows per band (2 segments x (n + 4))
-constexpr int NX = 4;                       // x tile stages
+constexpr int NX = AP_WSM_NX;               // x tile stages
 constexpr int NA = 2;                       // a1 tile / accumulator stages
 constexpr int WARP_PROD = 0, WARP_MMA = 1, EPI0 = 2, NEPI = 4, CONV0 = 6;
 constexpr int NT = (CONV0 + NCONV) * 32;
@@ -31,6 +37,15 @@ constexpr int PLANE_M = MA * A1C * 16;      // one 8-channel fp16 plane of the a
 static_assert(NA * ACC_COLS <= TMEM, "TMEM budget");
 
 __device__ long long g_trace[64 * 8];  // debug bit 16: CTA 0 timeline of its first 64 bands
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// debug bit 32: per-CTA globaltimer stamps in ws::g_prof[cta * 8 + e] (entry, setup done, producer's last
+// band issued, exit) and the CTA's band count
+#define WSM_CTA(e, v) \
+    if ((dbg & 32) && (threadIdx.x & 31) == 0 && blockIdx.x < 320) ws::g_prof[blockIdx.x * 8 + (e)] = (v);
 #define WSM_TRACE(b, e) \
     if ((dbg & 16) && blockIdx.x == 0 && (b) < 64) g_trace[(b) * 8 + (e)] = clock64();
 
@@ -108,6 +123,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
     const int H = P.H;
     const bool sel = P.state != nullptr;
     const int dbg = P.debug;  // profiling only: 1 no conv1 arithmetic, 2 no MMAs, 4 no epilogue arithmetic
+    if (tid == 0) WSM_CTA(0, gtimer());
 
     {  // B operands once per persistent CTA; barriers; TMEM
         const uint4* src = g_bpack96;
@@ -133,6 +149,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
         tc_fence_after();
     }
     const uint32_t tmem_base = *tmem_slot;
+    if (tid == 0) WSM_CTA(1, gtimer());
 
     if (warp == WARP_PROD) {
         // ------------------------------------------------------------------ producer (whole warp)
@@ -250,6 +267,10 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                 cb = nb_;
             }
             if (task0 + 32 * G >= n_tasks) break;
+        }
+        if (lane == 0) {
+            WSM_CTA(2, gtimer());
+            WSM_CTA(4, b);
         }
         {  // end of work: an invalid band tells the consumers to stop
             const int s = b % NX;
@@ -472,24 +493,30 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
             if (b >= NA) mbar_wait(&a1_empty[a], ((b / NA) & 1) ^ 1);
             if (ct == 0) WSM_TRACE(b, 2);
             uint8_t* a1t = smem + Smem::off_a1 + a * Smem::kA1;
-            // Two adjacent a1 pixels per thread (packed FFMA2, shared x window), real a1 rows only
-            constexpr int PAIRS = A1C / 2;
-            const int n_items = (dbg & 1) ? 0 : m.n_a1 * PAIRS;
+            // Two a1 pixels per thread, HALF apart (packed FFMA2), real a1 rows only: consecutive lanes own
+            // consecutive pixels, so every 16-byte tile store of a warp is one contiguous 512-byte run and
+            // every x load one contiguous 128-byte run (adjacent pixel pairs per thread cost twice the
+            // shared-memory wavefronts, and the port is what this kernel is bound by alongside the MMAs)
+            constexpr int HALF = A1C / 2;
+            const int n_items = (dbg & 1) ? 0 : m.n_a1 * HALF;
             for (int i = ct; i < n_items; i += NCONV_T) {
-                const int rr = i / PAIRS, ac = 2 * (i - rr * PAIRS);
+                const int rr = i / HALF, ac = i - rr * HALF;
                 const int ar = m.a1_r[rr], xb = m.a1_x[rr];
-                const int c = w0 - 1 + ac;  // pixel columns c, c + 1
-                float xw[3][4];
+                const int c = w0 - 1 + ac;  // pixel columns c, c + HALF
+                float xw[3][3], xv[3][3];
 #pragma unroll
                 for (int di = 0; di < 3; ++di) {
                     const int lim = m.x_lim[xb + di];
                     const float* xr = xs + (xb + di) * XC4 + ac + 2;
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) xw[di][e] = ((unsigned)(c - 1 + e) < (unsigned)lim) ? xr[e] : 0.f;
+                    for (int e = 0; e < 3; ++e) {
+                        xw[di][e] = ((unsigned)(c - 1 + e) < (unsigned)lim) ? xr[e] : 0.f;
+                        xv[di][e] = ((unsigned)(c + HALF - 1 + e) < (unsigned)lim) ? xr[HALF + e] : 0.f;
+                    }
                 }
                 // pixels outside [0, W) are conv2's zero padding: a zero scale clears them
                 const float sc0 = (unsigned)c < (unsigned)W ? ascale : 0.f;
-                const float sc1 = (unsigned)(c + 1) < (unsigned)W ? ascale : 0.f;
+                const float sc1 = (unsigned)(c + HALF) < (unsigned)W ? ascale : 0.f;
                 const int px = ar * A1C + ac;
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
@@ -500,7 +527,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                         float s0 = c_w[OFF_B1 + ch], s1 = s0;
 #pragma unroll
                         for (int k = 0; k < 9; ++k)
-                            ffma2(s0, s1, xw[k / 3][k % 3], xw[k / 3][k % 3 + 1], c_w[OFF_W1 + ch * 9 + k]);
+                            ffma2(s0, s1, xw[k / 3][k % 3], xv[k / 3][k % 3], c_w[OFF_W1 + ch * 9 + k]);
                         v0[q] = fmaxf(s0 * sc0, 0.f);  // relu(s) * 2^aexp (scale > 0, exact)
                         v1[q] = fmaxf(s1 * sc1, 0.f);
                     }
@@ -517,10 +544,10 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                                         pack_f16x2(v1[6], v1[7]));
                     }
                     *reinterpret_cast<uint4*>(a1t + g * PLANE_M + px * 16) = h0;
-                    *reinterpret_cast<uint4*>(a1t + g * PLANE_M + px * 16 + 16) = h1;
+                    *reinterpret_cast<uint4*>(a1t + g * PLANE_M + (px + HALF) * 16) = h1;
                     if constexpr (PREC == AP_PREC_F16X3) {
                         *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE_M + px * 16) = l0;
-                        *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE_M + px * 16 + 16) = l1;
+                        *reinterpret_cast<uint4*>(a1t + (2 + g) * PLANE_M + (px + HALF) * 16) = l1;
                     }
                 }
             }
@@ -559,6 +586,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
 
     tc_fence_before();
     __syncthreads();
+    if (tid == 0) WSM_CTA(3, gtimer());
     if (warp == WARP_PROD) tmem_dealloc(tmem_base, TMEM);
 }
 
