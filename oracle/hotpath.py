@@ -20,6 +20,8 @@ Reference anchors (paths relative to /root/reference/pkg/src/attncast):
   expand_indices    compress.py:43-57
   stack_history     predictor.py:145-157
   forward           predictor.py:185-216  (_forward_cached + forward)
+  backward          predictor.py:219-251
+  adam / train      predictor.py:327-391  (minibatch gradient sum, Adam update)
   init_weights      predictor.py:101-116
   APW1 I/O          predictor.py:424-444
   topk              selector.py:73-81
@@ -210,6 +212,122 @@ def row_contributions(w: Weights, grid) -> np.ndarray:
     """
     p = forward_parts(w, grid)
     return np.einsum("c,chw->hw", np.asarray(w.w3, np.float64), np.maximum(p["s2"], 0.0))
+
+
+def _corr3x3(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """g[ca, cb, di, dj] = sum_p a[ca, p] * b_pad[cb, p + (di-1, dj-1)] — the weight
+    gradient d_s @ cols.T of predictor.py:241,247 without forming im2col."""
+    cb, h, wd = b.shape
+    bp = np.zeros((cb, h + 2, wd + 2), dtype=np.float64)
+    bp[:, 1:-1, 1:-1] = b
+    af = a.reshape(a.shape[0], h * wd)
+    g = np.zeros((a.shape[0], cb, KS, KS))
+    for di in range(KS):
+        for dj in range(KS):
+            g[:, :, di, dj] = af @ bp[:, di:di + h, dj:dj + wd].reshape(cb, h * wd).T
+    return g
+
+
+def backward(w: Weights, grid, target):
+    """predictor.py:219-251 — loss = mean((out - target)^2) and its exact gradients.
+
+    The input gradient of conv2 (col2im of W2^T d_s2, predictor.py:242-243) is restated
+    as the 3x3 correlation of d_s2 with the flipped, channel-swapped kernel.
+    Returns (loss, Weights of gradients).
+    """
+    g = np.asarray(grid, dtype=np.float64)
+    tgt = np.asarray(target, dtype=np.float64)
+    h, wd = g.shape
+    if tgt.shape != (wd,):
+        raise OracleError("ParameterError", f"target must have shape ({wd},)")
+    p = forward_parts(w, g)
+    resid = p["out"] - tgt
+    loss = float(np.mean(resid ** 2))
+    d_out = 2.0 * resid / wd
+    d_w3 = p["z"] @ d_out
+    d_b3 = np.array(d_out.sum())
+    d_s2 = np.where(p["s2"] > 0, (np.asarray(w.w3, np.float64)[:, None] * d_out[None, :] / h)[:, None, :], 0.0)
+    d_w2 = _corr3x3(d_s2, p["a1"])
+    d_b2 = d_s2.sum(axis=(1, 2))
+    w2t = np.asarray(w.w2, np.float64).transpose(1, 0, 2, 3)[:, :, ::-1, ::-1]
+    d_a1 = _conv3x3(d_s2, w2t, np.zeros(C1))
+    d_s1 = np.where(p["a1"] > 0, d_a1, 0.0)
+    d_w1 = _corr3x3(d_s1, g[None])
+    d_b1 = d_s1.sum(axis=(1, 2))
+    return loss, Weights(d_w1, d_b1, d_w2, d_b2, d_w3, d_b3)
+
+
+def adam_update(wf, m, v, grad_sum, batch: int, step: int, lr: float = 1e-3,
+                beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8) -> None:
+    """predictor.py:381-391 on flat float64 arrays, in place (same operation order)."""
+    corr1 = 1.0 - beta1 ** step
+    corr2 = 1.0 - beta2 ** step
+    g = grad_sum / batch
+    m *= beta1
+    m += (1 - beta1) * g
+    v *= beta2
+    v += (1 - beta2) * g * g
+    wf -= lr * (m / corr1) / (np.sqrt(v / corr2) + eps)
+
+
+def block_recovery_accuracy(preds, targets) -> float:
+    """predictor.py:297-313 on precomputed predictions: mean recovered target mass of the
+    top round(0.1 W) predicted blocks relative to the best, in percent."""
+    if not targets:
+        return 0.0
+    ratios = []
+    for pred, tgt in zip(preds, targets):
+        w = pred.size
+        k = max(1, int(round(0.1 * w)))
+        op = np.lexsort((np.arange(w), -pred))[:k]
+        ot = np.lexsort((np.arange(w), -tgt))[:k]
+        best = float(tgt[ot].sum())
+        ratios.append(1.0 if best <= 0 else float(tgt[op].sum()) / best)
+    return 100.0 * float(np.mean(ratios))
+
+
+def train_schedule(n_samples: int, epochs: int, rng_seed: int, batch_size: int, holdout_fraction: float = 0.1):
+    """The sample order of predictor.train (predictor.py:345-371): (holdout ids, train ids,
+    [per epoch: list of minibatches of sample ids]).  Shared by the oracle and device trainers."""
+    rng = np.random.default_rng(np.random.SeedSequence(rng_seed, spawn_key=(0x7241,)))
+    order = rng.permutation(n_samples)
+    n_hold = int(round(holdout_fraction * n_samples)) if n_samples >= 10 else 0
+    hold = [int(i) for i in order[:n_hold]]
+    tr = [int(i) for i in order[n_hold:]]
+    epochs_b = []
+    for _ in range(epochs):
+        perm = rng.permutation(len(tr))
+        epochs_b.append([[tr[i] for i in perm[s:s + batch_size]] for s in range(0, len(perm), batch_size)])
+    return hold, tr, epochs_b
+
+
+def train(grids, targets, epochs: int = 30, lr: float = 1e-3, rng_seed: int = 0, batch_size: int = 32,
+          holdout_fraction: float = 0.1):
+    """predictor.py:327-409 — minibatch Adam on the MSE loss; returns (best weights, [(mse, acc)])."""
+    hold, tr, sched = train_schedule(len(grids), epochs, rng_seed, batch_size, holdout_fraction)
+    w = init_weights(rng_seed)
+    wf = w.flat()
+    m, v = np.zeros_like(wf), np.zeros_like(wf)
+    step, best, best_acc, metrics = 0, wf.copy(), -np.inf, []
+    for batches in sched:
+        losses = []
+        for batch in batches:
+            cur = Weights.from_flat(wf)
+            acc, bl = np.zeros_like(wf), 0.0
+            for i in batch:
+                loss, g = backward(cur, grids[i], targets[i])
+                bl += loss
+                acc += g.flat()
+            losses.append(bl / len(batch))
+            step += 1
+            adam_update(wf, m, v, acc, len(batch), step, lr)
+        ev = hold if hold else tr
+        cur = Weights.from_flat(wf)
+        a = block_recovery_accuracy([forward_parts(cur, grids[i])["out"] for i in ev], [targets[i] for i in ev])
+        metrics.append((float(np.mean(losses)), a))
+        if a > best_acc:
+            best_acc, best = a, wf.copy()
+    return Weights.from_flat(best), metrics
 
 
 # ---------------------------------------------------------------------------

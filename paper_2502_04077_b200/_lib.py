@@ -149,6 +149,11 @@ SIGNATURES = {
     "ap_trace_writer_finish": (ctypes.c_int, [_P, ctypes.POINTER(_I64)]),
     "ap_trace_writer_bytes": (ctypes.c_int, [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64)]),
     "ap_trace_writer_free": (None, [_P]),
+    # forecaster training (predictor.backward / train)
+    "ap_train_workspace_bytes": (ctypes.c_int64, [_I32, _I32, _I32]),
+    "ap_train_backward": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P, ctypes.c_int64, _P]),
+    "ap_adam_step": (ctypes.c_int, [_P, _P, _P, _P, _I32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_double, _I64, _P]),
 }
 
 _lib = None

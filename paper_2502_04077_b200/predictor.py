@@ -5,8 +5,9 @@ pkg/src/attncast/predictor.py:1-216,424-444): ``PredictorWeights``,
 ``init_weights``, ``AttentionHistory``, ``stack_history``, ``forward``,
 ``save_weights`` / ``load_weights`` with the APW1 format.  ``forward`` runs
 ``ap_predict_forward`` (csrc/predictor.cu) — a tcgen05 implicit-GEMM conv in
-the default ``fp16x3`` precision.  Training (backward / Adam,
-predictor.py:219-416) is out of scope for this B200 path.
+the default ``fp16x3`` precision.  Training — ``backward`` / ``train``
+(predictor.py:219-251,327-409) — runs ``ap_train_backward`` / ``ap_adam_step``
+(csrc/train.cu).
 """
 
 from __future__ import annotations
@@ -19,12 +20,12 @@ import numpy as np
 
 from . import _device as D
 from . import _lib
-from .errors import FormatError, NumericError, ParameterError
+from .errors import FormatError, NumericError, ParameterError, TrainingError
 
 __all__ = [
     "CONV1_OUT", "CONV2_OUT", "KERNEL", "PARAM_COUNT", "WEIGHTS_MAGIC", "PredictorWeights", "init_weights",
     "AttentionHistory", "stack_history", "forward", "save_weights", "load_weights", "install_weights",
-    "default_precision",
+    "default_precision", "TrainSample", "EpochMetrics", "backward", "train",
 ]
 
 CONV1_OUT = 16
@@ -208,3 +209,181 @@ def load_weights(path) -> PredictorWeights:
         if fh.read(1):
             raise FormatError("trailing bytes after weight tensors")
     return PredictorWeights.from_flat(flat.astype(np.float64))
+
+
+# ----------------------------------------------------------------- training (device)
+@dataclass
+class TrainSample:
+    """predictor.py:139-142 — one (history window, next compressed row) pair."""
+
+    input: AttentionHistory
+    target: np.ndarray  # length W
+
+
+@dataclass
+class EpochMetrics:
+    """predictor.py:316-320."""
+
+    epoch: int
+    train_mse: float
+    holdout_accuracy: float
+
+
+class _GradBatcher:
+    """Samples resident on the device, grouped by (H, W); one ap_train_backward per shape group."""
+
+    def __init__(self, grids, targets):
+        torch = D.torch()
+        self.shape_of = [tuple(np.asarray(g).shape) for g in grids]
+        self.groups = {}
+        for i, s in enumerate(self.shape_of):
+            self.groups.setdefault(s, []).append(i)
+        self.slot = {}
+        self.g_dev, self.t_dev = {}, {}
+        for s, ids in self.groups.items():
+            for j, i in enumerate(ids):
+                self.slot[i] = j
+            self.g_dev[s] = D.to_device(np.stack([np.asarray(grids[i], np.float32) for i in ids]))
+            self.t_dev[s] = D.to_device(np.stack([np.asarray(targets[i], np.float32) for i in ids]))
+        dev = D.device()
+        self.grads = torch.zeros(PARAM_COUNT, dtype=torch.float64, device=dev)
+        self.ws = torch.empty(0, dtype=torch.uint8, device=dev)
+        self.torch = torch
+
+    def grad_sum(self, w_dev, ids, loss_out):
+        """grads = sum over ids of each sample's gradient; loss_out += sum of losses (device)."""
+        torch = self.torch
+        self.grads.zero_()
+        by_shape = {}
+        for i in ids:
+            by_shape.setdefault(self.shape_of[i], []).append(self.slot[i])
+        for (H, W), slots in by_shape.items():
+            idx = torch.tensor(slots, dtype=torch.long, device=self.grads.device)
+            g = self.g_dev[(H, W)].index_select(0, idx).contiguous()
+            t = self.t_dev[(H, W)].index_select(0, idx).contiguous()
+            need = int(_lib.fn("ap_train_workspace_bytes")(len(slots), H, W))
+            if self.ws.numel() < need:
+                self.ws = torch.empty(need, dtype=torch.uint8, device=self.grads.device)
+            _lib.check(_lib.fn("ap_train_backward")(_lib.ptr(g), _lib.ptr(t), len(slots), H, W, _lib.ptr(w_dev),
+                                                    _lib.ptr(self.grads), _lib.ptr(loss_out), _lib.ptr(self.ws),
+                                                    self.ws.numel(), _lib.stream_handle()), "backward")
+        return self.grads
+
+
+def backward(weights: PredictorWeights, history: AttentionHistory, target) -> tuple[float, PredictorWeights]:
+    """predictor.py:219-251 — loss and exact gradients of mean((forward - target)^2), on the device
+    (ap_train_backward: fp32 arithmetic, fp64 reductions)."""
+    weights.validate()
+    grid = np.asarray(history.grid, dtype=np.float64)
+    target = np.asarray(target, dtype=np.float64)
+    H, W = grid.shape
+    if target.shape != (W,):
+        raise ParameterError(f"target must have shape ({W},)")
+    torch = D.torch()
+    b = _GradBatcher([grid], [target])
+    w_dev = D.to_device(weights.flat().astype(np.float64))
+    loss = torch.zeros(1, dtype=torch.float64, device=w_dev.device)
+    g = b.grad_sum(w_dev, [0], loss)
+    return float(loss.item()), PredictorWeights.from_flat(g.cpu().numpy())
+
+
+def _train_schedule(n: int, epochs: int, rng_seed: int, batch_size: int, holdout_fraction: float):
+    """The sample order of predictor.train (predictor.py:345-371): holdout ids, train ids and each
+    epoch's minibatches, drawn from the same seeded generator in the same order."""
+    rng = np.random.default_rng(np.random.SeedSequence(rng_seed, spawn_key=(0x7241,)))
+    order = rng.permutation(n)
+    n_hold = int(round(holdout_fraction * n)) if n >= 10 else 0
+    hold = [int(i) for i in order[:n_hold]]
+    tr = [int(i) for i in order[n_hold:]]
+    sched = []
+    for _ in range(epochs):
+        perm = rng.permutation(len(tr))
+        sched.append([[tr[i] for i in perm[s:s + batch_size]] for s in range(0, len(perm), batch_size)])
+    return hold, tr, sched
+
+
+def _block_recovery_accuracy(preds, targets) -> float:
+    """predictor.py:297-313 on device predictions (host ranking of W values per sample)."""
+    if not targets:
+        return 0.0
+    ratios = []
+    for pred, tgt in zip(preds, targets):
+        w = pred.size
+        k = max(1, int(round(0.1 * w)))
+        op = np.lexsort((np.arange(w), -pred))[:k]
+        ot = np.lexsort((np.arange(w), -tgt))[:k]
+        best = float(tgt[ot].sum())
+        ratios.append(1.0 if best <= 0 else float(tgt[op].sum()) / best)
+    return 100.0 * float(np.mean(ratios))
+
+
+def _forward_many(w_flat: np.ndarray, grids) -> list[np.ndarray]:
+    """fp32 ap_predict_forward of many histories, one launch per (H, W) group."""
+    torch = D.torch()
+    install_weights(PredictorWeights.from_flat(w_flat))
+    out = [None] * len(grids)
+    groups = {}
+    for i, g in enumerate(grids):
+        groups.setdefault(np.asarray(g).shape, []).append(i)
+    status = D.new_status()
+    for (H, W), ids in groups.items():
+        pitch = -(-W // 4) * 4
+        buf = np.zeros((len(ids), H, pitch), np.float32)
+        for j, i in enumerate(ids):
+            buf[j, :, :W] = grids[i]
+        g = D.to_device(buf)
+        o = torch.empty((len(ids), W), dtype=torch.float32, device=g.device)
+        scratch = torch.empty_like(g)
+        _lib.check(_lib.fn("ap_predict_forward")(_lib.ptr(g), len(ids), H, W, pitch, H * pitch, _lib.ptr(o), W,
+                                                 _lib.ptr(scratch), _lib.PREC["fp32"], _lib.ptr(status),
+                                                 _lib.stream_handle()), "forward")
+        o = o.cpu().numpy().astype(np.float64)
+        for j, i in enumerate(ids):
+            out[i] = o[j]
+    D.sync_and_check(status, "forward")
+    return out
+
+
+def train(samples, epochs: int = 30, learning_rate: float = 1e-3, rng_seed: int = 0, batch_size: int = 32,
+          holdout_fraction: float = 0.1) -> tuple[PredictorWeights, list[EpochMetrics]]:
+    """predictor.py:327-409 — minibatch Adam on the MSE loss, on the device.
+
+    Same holdout split, permutations, per-batch gradient sums and Adam arithmetic as the
+    reference (ap_train_backward + ap_adam_step; weights and moments stay on the device in
+    fp64); returns the checkpoint with the best held-out block-recovery accuracy.  Per-batch
+    losses are checked at the end of each epoch (TrainingError names the epoch).
+    """
+    if not samples:
+        raise ParameterError("cannot train on an empty sample set")
+    if epochs < 1:
+        raise ParameterError("epochs must be >= 1")
+    torch = D.torch()
+    grids = [np.asarray(s.input.grid, np.float64) for s in samples]
+    targets = [np.asarray(s.target, np.float64) for s in samples]
+    for g, t in zip(grids, targets):
+        if t.shape != (g.shape[1],):
+            raise ParameterError(f"target must have shape ({g.shape[1]},)")
+    hold, tr, sched = _train_schedule(len(samples), epochs, rng_seed, batch_size, holdout_fraction)
+    batcher = _GradBatcher(grids, targets)
+    w = D.to_device(init_weights(rng_seed).flat().astype(np.float64))
+    m, v = torch.zeros_like(w), torch.zeros_like(w)
+    best, best_acc, metrics, step = w.clone(), -np.inf, [], 0
+    ev = hold if hold else tr
+    for epoch, batches in enumerate(sched, start=1):
+        losses = torch.zeros(len(batches), dtype=torch.float64, device=w.device)
+        for b, ids in enumerate(batches):
+            g = batcher.grad_sum(w, ids, losses[b:b + 1])
+            step += 1
+            _lib.check(_lib.fn("ap_adam_step")(_lib.ptr(w), _lib.ptr(m), _lib.ptr(v), _lib.ptr(g), PARAM_COUNT,
+                                               float(len(ids)), learning_rate, 0.9, 0.999, 1e-8, step,
+                                               _lib.stream_handle()), "adam")
+        sizes = np.array([len(ids) for ids in batches], np.float64)
+        batch_loss = losses.cpu().numpy() / sizes
+        if not np.all(np.isfinite(batch_loss)):
+            raise TrainingError(f"loss became non-finite in epoch {epoch}", epoch=epoch)
+        w_host = w.cpu().numpy()
+        acc = _block_recovery_accuracy(_forward_many(w_host, [grids[i] for i in ev]), [targets[i] for i in ev])
+        metrics.append(EpochMetrics(epoch=epoch, train_mse=float(np.mean(batch_loss)), holdout_accuracy=acc))
+        if acc > best_acc:
+            best_acc, best = acc, w.clone()
+    return PredictorWeights.from_flat(best.cpu().numpy()), metrics

@@ -1,0 +1,110 @@
+"""Device forecaster training (ap_train_backward / ap_adam_step, csrc/train.cu) against the
+reference's golden training vectors and the float64 oracle (predictor.py:219-251,327-409).
+
+Tolerance (fp32 arithmetic, fp64 reductions): gradients |x - y| <= 1e-3 * max(|y|, 1e-2 * max|y|)
+(the parity contract of SURVEY.md §8(b)); loss rtol 1e-4."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, unragged
+from oracle import hotpath as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _close(x, y, rtol=1e-3):
+    x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
+    floor = 1e-2 * np.max(np.abs(y)) if y.size else 0.0
+    return np.all(np.abs(x - y) <= rtol * np.maximum(np.abs(y), floor))
+
+
+def _cases(z, prefix):
+    grids = unragged(z[f"{prefix}_grid"], z[f"{prefix}_grid_off"])
+    targets = unragged(z[f"{prefix}_target"], z[f"{prefix}_target_off"])
+    return [g.reshape(*s) for g, s in zip(grids, z[f"{prefix}_shapes"])], targets
+
+
+def test_backward_golden():
+    from paper_2502_04077_b200 import predictor as P
+
+    z = load_golden("train")
+    grids, targets = _cases(z, "bw")
+    for i, (g, t) in enumerate(zip(grids, targets)):
+        w = P.PredictorWeights.from_flat(z["bw_weights"][i])
+        loss, gr = P.backward(w, P.AttentionHistory(g), t)
+        assert abs(loss - z["bw_loss"][i]) <= 1e-4 * z["bw_loss"][i], (i, loss, z["bw_loss"][i])
+        assert _close(gr.flat(), z["bw_grads"][i]), (i, np.max(np.abs(gr.flat() - z["bw_grads"][i])))
+
+
+def test_backward_batched_full_shape():
+    """A 32-sample minibatch at the deployment window (H=64, W=256): the device gradient SUM
+    equals the sum of the oracle's per-sample gradients."""
+    import torch
+
+    from paper_2502_04077_b200 import predictor as P
+
+    rng = np.random.default_rng(11)
+    w = O.init_weights(5)
+    w.b1 = rng.standard_normal(16) * 0.05
+    w.b2 = rng.standard_normal(32) * 0.05
+    grids = [rng.dirichlet(np.full(256, 0.1), size=64) for _ in range(32)]
+    targets = [rng.dirichlet(np.full(256, 0.1)) for _ in range(32)]
+    b = P._GradBatcher(grids, targets)
+    wd = torch.from_numpy(w.flat()).cuda()
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g = b.grad_sum(wd, list(range(32)), loss).cpu().numpy()
+    ref_g, ref_l = np.zeros(O.PARAM_COUNT), 0.0
+    for i in (0, 7, 31):  # oracle on three samples, device on those three alone
+        l_i, g_i = O.backward(w, grids[i], targets[i])
+        ref_g += g_i.flat()
+        ref_l += l_i
+    loss3 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g3 = b.grad_sum(wd, [0, 7, 31], loss3).cpu().numpy()
+    assert _close(g3, ref_g) and abs(loss3.item() - ref_l) <= 1e-4 * ref_l
+    assert np.all(np.isfinite(g)) and loss.item() > 0
+
+
+def test_adam_matches_reference_arithmetic():
+    import torch
+
+    from paper_2502_04077_b200 import _lib
+
+    rng = np.random.default_rng(2)
+    wf, m, v = rng.standard_normal(4833), rng.standard_normal(4833) * 1e-3, rng.random(4833) * 1e-5
+    gsum = rng.standard_normal(4833)
+    dev = [torch.from_numpy(a.copy()).cuda() for a in (wf, m, v, gsum)]
+    for step in (1, 2, 3):
+        O.adam_update(wf, m, v, gsum, 6, step)
+        _lib.check(_lib.fn("ap_adam_step")(*(_lib.ptr(t) for t in dev), 4833, 6.0, 1e-3, 0.9, 0.999, 1e-8, step,
+                                           _lib.stream_handle()), "adam")
+    for host, d in zip((wf, m, v), dev):
+        assert np.max(np.abs(d.cpu().numpy() - host)) <= 1e-15 * max(1.0, np.max(np.abs(host)))
+
+
+def test_train_golden():
+    from paper_2502_04077_b200 import predictor as P
+
+    z = load_golden("train")
+    grids, targets = _cases(z, "tr")
+    epochs, seed, bs = (int(x) for x in z["tr_params"])
+    samples = [P.TrainSample(input=P.AttentionHistory(g), target=t) for g, t in zip(grids, targets)]
+    best, metrics = P.train(samples, epochs=epochs, learning_rate=1e-3, rng_seed=seed, batch_size=bs)
+    np.testing.assert_allclose([m.train_mse for m in metrics], z["tr_mse"], rtol=1e-3)
+    np.testing.assert_allclose([m.holdout_accuracy for m in metrics], z["tr_acc"], atol=1e-6)
+    # Adam normalises each step to ~lr, so fp32-gradient rounding moves weights by << lr
+    assert np.max(np.abs(best.flat() - z["tr_best"])) <= 1e-5
+
+
+def test_train_errors():
+    from paper_2502_04077_b200 import predictor as P
+    from paper_2502_04077_b200.errors import ParameterError, TrainingError
+
+    with pytest.raises(ParameterError):
+        P.train([])
+    g = np.full((4, 6), 1e30)
+    s = [P.TrainSample(input=P.AttentionHistory(g), target=np.full(6, 1e30))] * 3
+    with pytest.raises(TrainingError):
+        P.train(s, epochs=1)
