@@ -25,17 +25,20 @@ struct TrainWs {
     float* dout;  // [n][W] d loss / d out
     float* ds2;   // [n][32][H][W]
     float* ds1;   // [n][16][H][W]
+    double* part; // [CORR_CTAS][CORR_OUT] per-CTA d_w2 / d_b2 partials
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t carve(TrainWs* ws, void* base, int64_t n, int64_t H, int64_t W) {
     const int64_t px = n * H * W;
-    const size_t sizes[7] = {AP_PARAM_COUNT * 4, 16 * 32 * 9 * 4, (size_t)(C1 * px) * 4, (size_t)(C2 * px) * 4,
-                             (size_t)(n * W) * 4, (size_t)(C2 * px) * 4, (size_t)(C1 * px) * 4};
-    float** dst[7] = {&ws->wf, &ws->w2t, &ws->a1, &ws->s2, &ws->dout, &ws->ds2, &ws->ds1};
+    const size_t sizes[8] = {AP_PARAM_COUNT * 4, 16 * 32 * 9 * 4, (size_t)(C1 * px) * 4, (size_t)(C2 * px) * 4,
+                             (size_t)(n * W) * 4, (size_t)(C2 * px) * 4, (size_t)(C1 * px) * 4,
+                             (size_t)296 * (32 * 16 * 9 + 32) * 8};
+    float** dst[8] = {&ws->wf, &ws->w2t, &ws->a1, &ws->s2, &ws->dout, &ws->ds2, &ws->ds1,
+                      reinterpret_cast<float**>(&ws->part)};
     size_t off = 0;
-    for (int i = 0; i < 7; ++i) {
+    for (int i = 0; i < 8; ++i) {
         if (ws) *dst[i] = reinterpret_cast<float*>(static_cast<char*>(base) + off);
         off += align_up(sizes[i]);
     }
@@ -96,38 +99,51 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// One thread per (sample, column): z = mean_h relu(s2), out = w3.z + b3, the loss and d out,
-// d w3 = sum z * d out, d b3 = sum d out (predictor.py:196-199,230-238).
-__global__ void __launch_bounds__(128) head_kernel(const float* __restrict__ s2, const float* __restrict__ wf,
+// z = mean_h relu(s2), out = w3.z + b3, the loss and d out, d w3 = sum z * d out, d b3 = sum d out
+// (predictor.py:196-199,230-238).  CTA = 32 columns x 8 channel groups of 4: each thread sums its
+// 4 channel planes down one column, z goes through shared memory to the group-0 warp, which forms
+// out / resid / d out; then every thread reduces z * d out for its channels.
+__global__ void __launch_bounds__(256) head_kernel(const float* __restrict__ s2, const float* __restrict__ wf,
                                                    const float* __restrict__ target, float* __restrict__ dout,
                                                    double* __restrict__ grads, double* __restrict__ loss_sum,
                                                    int H, int W) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x, n = blockIdx.y;
+    __shared__ float zs[C2][33];
+    __shared__ float ds[32];
+    const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const int x = blockIdx.x * 32 + lane, n = blockIdx.y;
     const bool live = x < W;
     const int64_t plane = (int64_t)H * W;
-    float z[C2];
-    float out = wf[OFF_B3];
 #pragma unroll
-    for (int c = 0; c < C2; ++c) {
+    for (int j = 0; j < 4; ++j) {
+        const int c = grp * 4 + j;
         float s = 0.f;
         if (live) {
             const float* src = s2 + ((int64_t)n * C2 + c) * plane + x;
             for (int y = 0; y < H; ++y) s += fmaxf(src[(int64_t)y * W], 0.f);
         }
-        z[c] = s / (float)H;
-        out = fmaf(wf[OFF_W3 + c], z[c], out);
+        zs[c][lane] = s / (float)H;
     }
-    float resid = live ? out - target[(int64_t)n * W + x] : 0.f;
-    const float d = 2.f * resid / (float)W;
-    if (live) dout[(int64_t)n * W + x] = d;
-    const int lane = threadIdx.x & 31;
-    double l = warp_sum((double)resid * resid / W);
-    if (lane == 0) atomicAdd(loss_sum, l);
-    double db3 = warp_sum((double)d);
-    if (lane == 0) atomicAdd(grads + OFF_B3, db3);
+    __syncthreads();
+    if (grp == 0) {
+        float out = wf[OFF_B3];
 #pragma unroll
-    for (int c = 0; c < C2; ++c) {
-        double g = warp_sum((double)z[c] * d);
+        for (int c = 0; c < C2; ++c) out = fmaf(wf[OFF_W3 + c], zs[c][lane], out);
+        const float resid = live ? out - target[(int64_t)n * W + x] : 0.f;
+        const float d = 2.f * resid / (float)W;
+        ds[lane] = d;
+        if (live) dout[(int64_t)n * W + x] = d;
+        const double l = warp_sum((double)resid * resid / W);
+        const double db3 = warp_sum((double)d);
+        if (lane == 0) {
+            atomicAdd(loss_sum, l);
+            atomicAdd(grads + OFF_B3, db3);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = grp * 4 + j;
+        const double g = warp_sum((double)zs[c][lane] * ds[lane]);
         if (lane == 0) atomicAdd(grads + OFF_W3 + c, g);
     }
 }
@@ -193,6 +209,100 @@ __global__ void __launch_bounds__(256) corr_kernel(const float* __restrict__ A, 
     }
 }
 
+// d w2 / d b2 as a shared-memory tiled reduction: the 4608 outputs d_w2[a][b][tap] =
+// sum_p d_s2[a][p] * a1_pad[b][p + off(tap)] form a 32 x 144 GEMM over pixels.  A persistent
+// CTA walks 64-column row tiles (d_s2 rows [32][64], a1 rows y-1..y+1 with halo [16][3][66] in
+// shared memory); thread t owns a-pair t/16 and b = t%16 (2 x 9 taps = 18 fp32 accumulators),
+// sliding a 3-wide register window along the row so each pixel costs 2 + 3 shared loads for
+// 18 FMAs.  Each tile's fp32 sums are folded into fp64 registers; per-CTA partials go to a
+// [grid][4640] fp64 buffer and are summed in a fixed order (run-to-run deterministic).
+constexpr int CT = 64;        // tile columns
+constexpr int CORR_CTAS = 296;
+constexpr int CORR_OUT = C2 * C1 * 9 + C2;  // d_w2 then d_b2
+
+__global__ void __launch_bounds__(256) corr2_tiled_kernel(const float* __restrict__ ds2, const float* __restrict__ a1,
+                                                          double* __restrict__ partial, int n_samples, int H, int W) {
+    __shared__ float As[C2][CT + 1];
+    __shared__ float Bs[C1][3][CT + 2];
+    const int tid = threadIdx.x, b = tid % 16, a0 = (tid / 16) * 2;
+    double tot[2][10];  // per-tile fp32 sums folded into fp64 (tiles are 64 pixels)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int t = 0; t < 10; ++t) tot[i][t] = 0.0;
+    const int xt = (W + CT - 1) / CT;
+    const int64_t n_tiles = (int64_t)n_samples * H * xt, plane = (int64_t)H * W;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int x0 = (int)(tile % xt) * CT;
+        const int y = (int)((tile / xt) % H);
+        const int64_t n = tile / ((int64_t)xt * H);
+        __syncthreads();
+        for (int i = tid; i < C2 * CT; i += 256) {
+            const int c = i / CT, x = x0 + i % CT;
+            As[c][i % CT] = x < W ? ds2[(n * C2 + c) * plane + (int64_t)y * W + x] : 0.f;
+        }
+        for (int i = tid; i < C1 * 3 * (CT + 2); i += 256) {
+            const int c = i / (3 * (CT + 2)), r = (i / (CT + 2)) % 3, xx = x0 - 1 + i % (CT + 2), yy = y - 1 + r;
+            Bs[c][r][i % (CT + 2)] =
+                (yy >= 0 && yy < H && xx >= 0 && xx < W) ? a1[(n * C1 + c) * plane + (int64_t)yy * W + xx] : 0.f;
+        }
+        __syncthreads();
+        float acc[2][9], bias[2] = {0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int t = 0; t < 9; ++t) acc[i][t] = 0.f;
+        float win[3][3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            win[r][0] = Bs[b][r][0];
+            win[r][1] = Bs[b][r][1];
+        }
+#pragma unroll 4
+        for (int p = 0; p < CT; ++p) {
+#pragma unroll
+            for (int r = 0; r < 3; ++r) win[r][2] = Bs[b][r][p + 2];
+            const float g0 = As[a0][p], g1 = As[a0 + 1][p];
+            bias[0] += g0;
+            bias[1] += g1;
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    acc[0][r * 3 + c] = fmaf(g0, win[r][c], acc[0][r * 3 + c]);
+                    acc[1][r * 3 + c] = fmaf(g1, win[r][c], acc[1][r * 3 + c]);
+                }
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                win[r][0] = win[r][1];
+                win[r][1] = win[r][2];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+#pragma unroll
+            for (int t = 0; t < 9; ++t) tot[i][t] += acc[i][t];
+            tot[i][9] += bias[i];
+        }
+    }
+    double* out = partial + (int64_t)blockIdx.x * CORR_OUT;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+#pragma unroll
+        for (int t = 0; t < 9; ++t) out[((a0 + i) * C1 + b) * 9 + t] = tot[i][t];
+        if (b == 0) out[C2 * C1 * 9 + a0 + i] = tot[i][9];
+    }
+}
+
+// grads[OFF_W2 + j] += sum over CTAs of partial[cta][j] (j < 4608), then d_b2; fixed order.
+__global__ void corr2_finish_kernel(const double* __restrict__ partial, int n_parts, double* __restrict__ grads) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= CORR_OUT) return;
+    double s = 0.0;
+    for (int k = 0; k < n_parts; ++k) s += partial[(int64_t)k * CORR_OUT + j];
+    grads[(j < C2 * C1 * 9 ? OFF_W2 + j : OFF_B2 + (j - C2 * C1 * 9))] += s;
+}
+
 // Adam (predictor.py:381-391), fp64, no FMA contraction so it rounds like numpy.
 __global__ void adam_kernel(double* __restrict__ w, double* __restrict__ m, double* __restrict__ v,
                             const double* __restrict__ gsum, int n, double batch, double lr, double beta1,
@@ -240,11 +350,11 @@ int ap_train_backward(const float* grids, const float* targets, int32_t n_sample
     const dim3 cblk(128), cgrid((W + 127) / 128, H, n_samples);
     conv3x3_kernel<1, C1, true><<<cgrid, cblk, 0, st>>>(grids, ws.wf + OFF_W1, ws.wf + OFF_B1, nullptr, ws.a1, H, W);
     conv3x3_kernel<C1, C2, false><<<cgrid, cblk, 0, st>>>(ws.a1, ws.wf + OFF_W2, ws.wf + OFF_B2, nullptr, ws.s2, H, W);
-    head_kernel<<<dim3((W + 127) / 128, n_samples), 128, 0, st>>>(ws.s2, ws.wf, targets, ws.dout, grads, loss_sum, H, W);
+    head_kernel<<<dim3((W + 31) / 32, n_samples), 256, 0, st>>>(ws.s2, ws.wf, targets, ws.dout, grads, loss_sum, H, W);
     ds2_kernel<<<grid_for(C2 * px, 256), 256, 0, st>>>(ws.s2, ws.wf, ws.dout, ws.ds2, H, W, C2 * px);
     const int chunks = grid_for(px, 256) / 4 + 1;
-    corr_kernel<C2, C1, 4><<<dim3(chunks, C2 * C1 / 4), 256, 0, st>>>(ws.ds2, ws.a1, grads + OFF_W2, grads + OFF_B2,
-                                                                      n_samples, H, W);
+    corr2_tiled_kernel<<<CORR_CTAS, 256, 0, st>>>(ws.ds2, ws.a1, ws.part, n_samples, H, W);
+    corr2_finish_kernel<<<(CORR_OUT + 255) / 256, 256, 0, st>>>(ws.part, CORR_CTAS, grads);
     // d a1 = conv2^T(d s2); d s1 = [a1 > 0] * d a1  (predictor.py:243-245; a1 > 0 <=> s1 > 0)
     conv3x3_kernel<C2, C1, false><<<cgrid, cblk, 0, st>>>(ws.ds2, ws.w2t, nullptr, ws.a1, ws.ds1, H, W);
     corr_kernel<C1, 1, 1><<<dim3(chunks, C1), 256, 0, st>>>(ws.ds1, grids, grads + OFF_W1, grads + OFF_B1, n_samples,
