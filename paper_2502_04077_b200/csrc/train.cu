@@ -57,40 +57,65 @@ __global__ void prep_weights_kernel(const double* __restrict__ w, float* __restr
 
 // out[n][co][p] = bias[co] + sum_{ci, tap} w[co][ci][tap] * in[n][ci][p + off(tap)]  (zero pad 1)
 // RELU: out = max(out, 0).  mask != nullptr: out = mask[n][co][p] > 0 ? out : 0.
-template <int CI, int CO, bool RELU>
-__global__ void __launch_bounds__(128) conv3x3_kernel(const float* __restrict__ in, const float* __restrict__ w,
-                                                      const float* __restrict__ bias, const float* __restrict__ mask,
-                                                      float* __restrict__ out, int H, int W) {
+// Each thread computes PX consecutive columns of one row, so every weight read from shared
+// memory (a warp-wide broadcast) feeds PX FMAs and each input row segment of PX+2 values
+// feeds 3·PX taps.
+template <int CI, int CO, int PX, bool RELU>
+__global__ void __launch_bounds__(64) conv3x3_kernel(const float* __restrict__ in, const float* __restrict__ w,
+                                                     const float* __restrict__ bias, const float* __restrict__ mask,
+                                                     float* __restrict__ out, int H, int W) {
     __shared__ float sw[CO * CI * 9];
     for (int i = threadIdx.x; i < CO * CI * 9; i += blockDim.x) sw[i] = w[i];
     __syncthreads();
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * PX;
     const int y = blockIdx.y, n = blockIdx.z;
-    if (x >= W) return;
+    if (x0 >= W) return;
     const int64_t plane = (int64_t)H * W;
-    float acc[CO];
+    float acc[CO][PX];
 #pragma unroll
-    for (int co = 0; co < CO; ++co) acc[co] = bias ? bias[co] : 0.f;
+    for (int co = 0; co < CO; ++co)
+#pragma unroll
+        for (int q = 0; q < PX; ++q) acc[co][q] = bias ? bias[co] : 0.f;
+#pragma unroll 1
     for (int ci = 0; ci < CI; ++ci) {
         const float* src = in + ((int64_t)n * CI + ci) * plane;
-        float v[9];
+        float v[3][PX + 2];
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-            const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
-            v[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? src[(int64_t)yy * W + xx] : 0.f;
+        for (int r = 0; r < 3; ++r) {
+            const int yy = y + r - 1;
+#pragma unroll
+            for (int j = 0; j < PX + 2; ++j) {
+                const int xx = x0 + j - 1;
+                v[r][j] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? src[(int64_t)yy * W + xx] : 0.f;
+            }
         }
 #pragma unroll
         for (int co = 0; co < CO; ++co)
 #pragma unroll
-            for (int t = 0; t < 9; ++t) acc[co] = fmaf(sw[(co * CI + ci) * 9 + t], v[t], acc[co]);
-    }
-    const int64_t p = (int64_t)y * W + x;
+            for (int t = 0; t < 9; ++t) {
+                const float wt = sw[(co * CI + ci) * 9 + t];
 #pragma unroll
-    for (int co = 0; co < CO; ++co) {
-        float r = RELU ? fmaxf(acc[co], 0.f) : acc[co];
-        if (mask && !(mask[((int64_t)n * CO + co) * plane + p] > 0.f)) r = 0.f;
-        out[((int64_t)n * CO + co) * plane + p] = r;
+                for (int q = 0; q < PX; ++q) acc[co][q] = fmaf(wt, v[t / 3][q + t % 3], acc[co][q]);
+            }
     }
+#pragma unroll
+    for (int co = 0; co < CO; ++co)
+#pragma unroll
+        for (int q = 0; q < PX; ++q) {
+            const int x = x0 + q;
+            if (x >= W) continue;
+            const int64_t o = ((int64_t)n * CO + co) * plane + (int64_t)y * W + x;
+            float r = RELU ? fmaxf(acc[co][q], 0.f) : acc[co][q];
+            if (mask && !(mask[o] > 0.f)) r = 0.f;
+            out[o] = r;
+        }
+}
+
+template <int CI, int CO, int PX, bool RELU>
+void launch_conv(const float* in, const float* w, const float* bias, const float* mask, float* out, int n, int H,
+                 int W, cudaStream_t st) {
+    const dim3 grid((W + 64 * PX - 1) / (64 * PX), H, n);
+    conv3x3_kernel<CI, CO, PX, RELU><<<grid, 64, 0, st>>>(in, w, bias, mask, out, H, W);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -347,16 +372,15 @@ int ap_train_backward(const float* grids, const float* targets, int32_t n_sample
     carve(&ws, workspace, n_samples, H, W);
     const int64_t px = (int64_t)n_samples * H * W;
     prep_weights_kernel<<<8, 512, 0, st>>>(weights, ws.wf, ws.w2t);
-    const dim3 cblk(128), cgrid((W + 127) / 128, H, n_samples);
-    conv3x3_kernel<1, C1, true><<<cgrid, cblk, 0, st>>>(grids, ws.wf + OFF_W1, ws.wf + OFF_B1, nullptr, ws.a1, H, W);
-    conv3x3_kernel<C1, C2, false><<<cgrid, cblk, 0, st>>>(ws.a1, ws.wf + OFF_W2, ws.wf + OFF_B2, nullptr, ws.s2, H, W);
+    launch_conv<1, C1, 4, true>(grids, ws.wf + OFF_W1, ws.wf + OFF_B1, nullptr, ws.a1, n_samples, H, W, st);
+    launch_conv<C1, C2, 2, false>(ws.a1, ws.wf + OFF_W2, ws.wf + OFF_B2, nullptr, ws.s2, n_samples, H, W, st);
     head_kernel<<<dim3((W + 31) / 32, n_samples), 256, 0, st>>>(ws.s2, ws.wf, targets, ws.dout, grads, loss_sum, H, W);
     ds2_kernel<<<grid_for(C2 * px, 256), 256, 0, st>>>(ws.s2, ws.wf, ws.dout, ws.ds2, H, W, C2 * px);
     const int chunks = grid_for(px, 256) / 4 + 1;
     corr2_tiled_kernel<<<CORR_CTAS, 256, 0, st>>>(ws.ds2, ws.a1, ws.part, n_samples, H, W);
     corr2_finish_kernel<<<(CORR_OUT + 255) / 256, 256, 0, st>>>(ws.part, CORR_CTAS, grads);
     // d a1 = conv2^T(d s2); d s1 = [a1 > 0] * d a1  (predictor.py:243-245; a1 > 0 <=> s1 > 0)
-    conv3x3_kernel<C2, C1, false><<<cgrid, cblk, 0, st>>>(ws.ds2, ws.w2t, nullptr, ws.a1, ws.ds1, H, W);
+    launch_conv<C2, C1, 4, false>(ws.ds2, ws.w2t, nullptr, ws.a1, ws.ds1, n_samples, H, W, st);
     corr_kernel<C1, 1, 1><<<dim3(chunks, C1), 256, 0, st>>>(ws.ds1, grids, grads + OFF_W1, grads + OFF_B1, n_samples,
                                                             H, W);
     return launch_status("ap_train_backward");

@@ -382,6 +382,8 @@ def train(samples, epochs: int = 30, learning_rate: float = 1e-3, rng_seed: int 
         if not np.all(np.isfinite(batch_loss)):
             raise TrainingError(f"loss became non-finite in epoch {epoch}", epoch=epoch)
         w_host = w.cpu().numpy()
+        if not np.all(np.isfinite(w_host)):
+            raise TrainingError(f"weights became non-finite in epoch {epoch}", epoch=epoch)
         acc = _block_recovery_accuracy(_forward_many(w_host, [grids[i] for i in ev]), [targets[i] for i in ev])
         metrics.append(EpochMetrics(epoch=epoch, train_mse=float(np.mean(batch_loss)), holdout_accuracy=acc))
         if acc > best_acc:

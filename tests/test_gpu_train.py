@@ -104,7 +104,7 @@ def test_train_errors():
 
     with pytest.raises(ParameterError):
         P.train([])
-    g = np.full((4, 6), 1e30)
-    s = [P.TrainSample(input=P.AttentionHistory(g), target=np.full(6, 1e30))] * 3
+    g = np.random.default_rng(0).random((4, 6))
+    s = [P.TrainSample(input=P.AttentionHistory(g), target=np.full(6, np.nan))] * 3  # non-finite loss
     with pytest.raises(TrainingError):
         P.train(s, epochs=1)
