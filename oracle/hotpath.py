@@ -22,6 +22,7 @@ Reference anchors (paths relative to /root/reference/pkg/src/attncast):
   forward           predictor.py:185-216  (_forward_cached + forward)
   backward          predictor.py:219-251
   adam / train      predictor.py:327-391  (minibatch gradient sum, Adam update)
+  build_dataset     predictor.py:254-300
   init_weights      predictor.py:101-116
   APW1 I/O          predictor.py:424-444
   topk              selector.py:73-81
@@ -268,6 +269,28 @@ def adam_update(wf, m, v, grad_sum, batch: int, step: int, lr: float = 1e-3,
     v *= beta2
     v += (1 - beta2) * g * g
     wf -= lr * (m / corr1) / (np.sqrt(v / corr2) + eps)
+
+
+def build_dataset(trace, history_steps: int, block_size: int, sample_ratio: float, rng_seed: int = 0,
+                  max_step=None):
+    """predictor.py:254-300 — [(grid, target)] from any object with the reference trace API
+    (``header.num_layers/num_heads/num_decode_steps/first_step_offset/row_len``, ``row``)."""
+    h = trace.header
+    last_t = h.num_decode_steps - 1 if max_step is None else min(max_step - 1, h.num_decode_steps - 1)
+    cands = [(la, he, t) for la in range(h.num_layers) for he in range(h.num_heads) for t in range(1, last_t + 1)]
+    rng = np.random.default_rng(np.random.SeedSequence(rng_seed, spawn_key=(0xDA7A,)))
+    keep = max(1, int(round(sample_ratio * len(cands))))
+    chosen = sorted(rng.choice(len(cands), size=min(keep, len(cands)), replace=False).tolist())
+    out = []
+    for idx in chosen:
+        la, he, t = cands[idx]
+        t_len = h.row_len(t)
+        width = -(-t_len // block_size)
+        rows = [max_pool(trace.row(la, he, s), block_size) for s in range(t - history_steps + 1, t + 1)
+                if s >= h.first_step_offset]
+        out.append((stack_history(rows, history_steps, width),
+                    max_pool(np.asarray(trace.row(la, he, t + 1))[:t_len], block_size)))
+    return out
 
 
 def block_recovery_accuracy(preds, targets) -> float:

@@ -26,6 +26,7 @@ __all__ = [
     "CONV1_OUT", "CONV2_OUT", "KERNEL", "PARAM_COUNT", "WEIGHTS_MAGIC", "PredictorWeights", "init_weights",
     "AttentionHistory", "stack_history", "forward", "save_weights", "load_weights", "install_weights",
     "default_precision", "TrainSample", "EpochMetrics", "backward", "train",
+    "build_dataset",
 ]
 
 CONV1_OUT = 16
@@ -389,3 +390,66 @@ def train(samples, epochs: int = 30, learning_rate: float = 1e-3, rng_seed: int 
         if acc > best_acc:
             best_acc, best = acc, w.clone()
     return PredictorWeights.from_flat(best.cpu().numpy()), metrics
+
+
+def build_dataset(trace, history_steps: int, block_size: int, sample_ratio: float, rng_seed: int = 0,
+                  max_step: int | None = None) -> list[TrainSample]:
+    """predictor.py:254-300 — (history window, next compressed row) pairs from an attention trace.
+
+    Same candidate enumeration, seeded subsample, window and target definitions as the
+    reference.  The compression runs on the device: per (layer, head), every stored row (zero
+    padded to the trace's final length; zero padding is what max_pool pads with, so the leading
+    blocks are unchanged) and every truncated next-step target row go through ONE ``ap_max_pool``.
+    """
+    if history_steps < 1:
+        raise ParameterError("history_steps must be >= 1")
+    if block_size < 1:
+        raise ParameterError("block size must be >= 1")
+    if not (0.0 < sample_ratio <= 1.0):
+        raise ParameterError("sample_ratio must lie in (0, 1]")
+    h = trace.header
+    if h.num_decode_steps < 1:
+        raise ParameterError("trace has no decode steps to learn from")
+    last_t = h.num_decode_steps - 1 if max_step is None else min(max_step - 1, h.num_decode_steps - 1)
+    candidates = [(layer, head, t) for layer in range(h.num_layers) for head in range(h.num_heads)
+                  for t in range(1, last_t + 1)]
+    rng = np.random.default_rng(np.random.SeedSequence(rng_seed, spawn_key=(0xDA7A,)))
+    keep = max(1, int(round(sample_ratio * len(candidates))))
+    chosen = sorted(rng.choice(len(candidates), size=min(keep, len(candidates)), replace=False).tolist())
+    if not chosen:
+        return []
+    torch = D.torch()
+    steps = list(h.steps)
+    L = h.total_len
+    W_all = -(-L // block_size)
+    n_rows = len(steps)
+    compressed = {}
+
+    def pool(layer, head):
+        if (layer, head) not in compressed:
+            # rows [0, n_rows): stored rows; rows [n_rows, 2 n_rows): row s truncated to row_len(s - 1)
+            buf = np.zeros((2 * n_rows, L), np.float32)
+            for k, s in enumerate(steps):
+                r = np.asarray(trace.row(layer, head, s), np.float32)
+                buf[k, :r.size] = r
+                if s >= 1:
+                    n = min(h.row_len(s - 1), r.size)
+                    buf[n_rows + k, :n] = r[:n]
+            x = D.to_device(buf)
+            out = torch.empty((2 * n_rows, W_all), dtype=torch.float64, device=x.device)
+            _lib.check(_lib.fn("ap_max_pool")(_lib.ptr(x), _lib.AP_F32, 2 * n_rows, L, L, block_size, _lib.ptr(out),
+                                              _lib.AP_F64, W_all, _lib.stream_handle()), "max_pool")
+            compressed[(layer, head)] = out.cpu().numpy()
+        return compressed[(layer, head)]
+
+    samples = []
+    for idx in chosen:
+        layer, head, t = candidates[idx]
+        cm = pool(layer, head)
+        width = -(-h.row_len(t) // block_size)
+        window = [cm[s - h.first_step_offset, :-(-h.row_len(s) // block_size)]
+                  for s in range(t - history_steps + 1, t + 1) if s >= h.first_step_offset]
+        history = stack_history(window, history_steps, width)
+        target = cm[n_rows + (t + 1 - h.first_step_offset), :width].copy()
+        samples.append(TrainSample(input=history, target=target))
+    return samples

@@ -8,7 +8,8 @@ Writes ``tests/golden/train.npz``: inputs and outputs of attncast.predictor.back
 (predictor.py:219-251) on several history shapes with biased weights, and one short
 attncast.predictor.train run (predictor.py:327-409: seeded holdout split, per-epoch
 permutations, per-sample gradient sums, Adam) on a mixed-width sample set — its best
-weights and per-epoch metrics.  Ragged arrays are (flat, offsets) pairs.
+weights and per-epoch metrics; and attncast.predictor.build_dataset (predictor.py:254-300) on
+the committed trace_tiny.att1 for three (history, block, ratio, seed, max_step) settings.  Ragged arrays are (flat, offsets) pairs.
 """
 
 from __future__ import annotations
@@ -85,6 +86,18 @@ def main():
     out["tr_best"] = best.flat()
     out["tr_mse"] = np.array([m.train_mse for m in metrics])
     out["tr_acc"] = np.array([m.holdout_accuracy for m in metrics])
+    # predictor.build_dataset (predictor.py:254-300) on the committed golden trace
+    from attncast.trace import read_trace_file
+
+    tr = read_trace_file(OUT / "trace_tiny.att1")
+    ds_cases = [(8, 16, 1.0, 0, None), (4, 8, 0.5, 3, None), (16, 4, 0.7, 1, 5)]
+    for k, (hs, bs_, ratio, seed, max_step) in enumerate(ds_cases):
+        ds = predictor.build_dataset(tr, hs, bs_, ratio, rng_seed=seed, max_step=max_step)
+        out[f"ds{k}_params"] = np.array([hs, bs_, seed, -1 if max_step is None else max_step], np.int64)
+        out[f"ds{k}_ratio"] = np.array(ratio)
+        out[f"ds{k}_shapes"] = np.array([s.input.grid.shape for s in ds], np.int64)
+        out[f"ds{k}_grid"], out[f"ds{k}_grid_off"] = ragged([s.input.grid for s in ds])
+        out[f"ds{k}_target"], out[f"ds{k}_target_off"] = ragged([s.target for s in ds])
     np.savez_compressed(OUT / "train.npz", **out)
     print("wrote", OUT / "train.npz", {k: v.shape for k, v in out.items()})
 

@@ -108,3 +108,37 @@ def test_train_errors():
     s = [P.TrainSample(input=P.AttentionHistory(g), target=np.full(6, np.nan))] * 3  # non-finite loss
     with pytest.raises(TrainingError):
         P.train(s, epochs=1)
+
+
+def test_build_dataset_golden_exact():
+    """Device build_dataset (ap_max_pool batched per head) = the reference's samples, bit for bit."""
+    from conftest import GOLDEN
+
+    from paper_2502_04077_b200 import predictor as P
+    from paper_2502_04077_b200.trace import read_trace_file
+
+    z = load_golden("train")
+    tr = read_trace_file(GOLDEN / "trace_tiny.att1")
+    for k in range(3):
+        grids, targets = _cases(z, f"ds{k}")
+        hs, bs, seed, max_step = (int(x) for x in z[f"ds{k}_params"])
+        got = P.build_dataset(tr, hs, bs, float(z[f"ds{k}_ratio"]), rng_seed=seed,
+                              max_step=None if max_step < 0 else max_step)
+        assert len(got) == len(grids)
+        for s, rg, rt in zip(got, grids, targets):
+            assert np.array_equal(s.input.grid, rg) and np.array_equal(s.target, rt)
+
+
+def test_build_then_train_end_to_end():
+    """The reference's training pipeline (build_dataset -> train) on the device, against the oracle."""
+    from conftest import GOLDEN
+
+    from paper_2502_04077_b200 import predictor as P
+    from paper_2502_04077_b200.trace import read_trace_file
+
+    tr = read_trace_file(GOLDEN / "trace_tiny.att1")
+    ds = P.build_dataset(tr, 8, 16, 1.0, rng_seed=0)
+    best, metrics = P.train(ds, epochs=2, rng_seed=1, batch_size=16)
+    ob, om = O.train([s.input.grid for s in ds], [s.target for s in ds], epochs=2, lr=1e-3, rng_seed=1, batch_size=16)
+    np.testing.assert_allclose([m.train_mse for m in metrics], [m[0] for m in om], rtol=1e-3)
+    assert np.max(np.abs(best.flat() - ob.flat())) <= 1e-5

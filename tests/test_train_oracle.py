@@ -52,3 +52,23 @@ def test_train_golden():
     assert np.max(np.abs(best.flat() - z["tr_best"])) <= 1e-12
     np.testing.assert_allclose([m[0] for m in metrics], z["tr_mse"], rtol=1e-12)
     np.testing.assert_allclose([m[1] for m in metrics], z["tr_acc"], rtol=1e-12)
+
+
+def _golden_dataset(z, k):
+    grids, targets = _cases(z, f"ds{k}")
+    hs, bs, seed, max_step = (int(x) for x in z[f"ds{k}_params"])
+    return grids, targets, hs, bs, float(z[f"ds{k}_ratio"]), seed, None if max_step < 0 else max_step
+
+
+def test_build_dataset_golden():
+    from paper_2502_04077_b200.trace import read_trace_file  # host C++ reader, no GPU
+    from conftest import GOLDEN
+
+    z = load_golden("train")
+    tr = read_trace_file(GOLDEN / "trace_tiny.att1")
+    for k in range(3):
+        grids, targets, hs, bs, ratio, seed, max_step = _golden_dataset(z, k)
+        got = O.build_dataset(tr, hs, bs, ratio, rng_seed=seed, max_step=max_step)
+        assert len(got) == len(grids)
+        for (g, t), rg, rt in zip(got, grids, targets):
+            assert np.array_equal(g, rg) and np.array_equal(t, rt)
