@@ -360,13 +360,14 @@ int ap_gemm_tc(const void* W, const void* x, void* y, int32_t N, int32_t K, int3
 /* ---------------------------------------------------------------------------
  * Forecaster training (not on the decode path).
  * ------------------------------------------------------------------------- */
-/* predictor.backward (predictor.py:219-251) for n_samples equal-shape samples: grids [n][H][W] fp32 and
- * targets [n][W] fp32, contiguous; weights: 4833 fp64 in the APW1 order.  Accumulates (+=) the SUM over
- * samples of each sample's gradient into grads[4833] (fp64) and of its loss into *loss_sum (the
- * reference's per-batch accumulation, predictor.py:371-377).  Arithmetic fp32, reductions fp64.
- * workspace: ap_train_workspace_bytes(n, H, W) bytes (activations and gradients, 384 B per pixel). */
+/* predictor.backward (predictor.py:219-251) for n_samples equal-shape samples: grids [n][H][W] and
+ * targets [n][W] fp64, contiguous; weights: 4833 fp64 in the APW1 order.  Accumulates (+=) the SUM over
+ * samples of each sample's gradient into grads[4833] and of its loss into *loss_sum (the reference's
+ * per-batch accumulation, predictor.py:371-377).  fp64 arithmetic like the reference; every reduction
+ * runs in a fixed order, so results are run-to-run deterministic.
+ * workspace: ap_train_workspace_bytes(n, H, W) bytes (activations and gradients, 768 B per pixel). */
 int64_t ap_train_workspace_bytes(int32_t n_samples, int32_t H, int32_t W);
-int ap_train_backward(const float* grids, const float* targets, int32_t n_samples, int32_t H, int32_t W,
+int ap_train_backward(const double* grids, const double* targets, int32_t n_samples, int32_t H, int32_t W,
                       const double* weights, double* grads, double* loss_sum, void* workspace,
                       int64_t workspace_bytes, void* stream);
 /* Adam of predictor.train (predictor.py:381-391) in fp64 with numpy's rounding: g = grad_sum / batch,

@@ -244,8 +244,8 @@ class _GradBatcher:
         for s, ids in self.groups.items():
             for j, i in enumerate(ids):
                 self.slot[i] = j
-            self.g_dev[s] = D.to_device(np.stack([np.asarray(grids[i], np.float32) for i in ids]))
-            self.t_dev[s] = D.to_device(np.stack([np.asarray(targets[i], np.float32) for i in ids]))
+            self.g_dev[s] = D.to_device(np.stack([np.asarray(grids[i], np.float64) for i in ids]))
+            self.t_dev[s] = D.to_device(np.stack([np.asarray(targets[i], np.float64) for i in ids]))
         dev = D.device()
         self.grads = torch.zeros(PARAM_COUNT, dtype=torch.float64, device=dev)
         self.ws = torch.empty(0, dtype=torch.uint8, device=dev)
@@ -273,7 +273,7 @@ class _GradBatcher:
 
 def backward(weights: PredictorWeights, history: AttentionHistory, target) -> tuple[float, PredictorWeights]:
     """predictor.py:219-251 — loss and exact gradients of mean((forward - target)^2), on the device
-    (ap_train_backward: fp32 arithmetic, fp64 reductions)."""
+    (ap_train_backward: fp64 arithmetic like the reference, deterministic reductions)."""
     weights.validate()
     grid = np.asarray(history.grid, dtype=np.float64)
     target = np.asarray(target, dtype=np.float64)
