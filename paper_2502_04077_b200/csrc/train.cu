@@ -71,9 +71,9 @@ __global__ void prep_weights_kernel(const real* __restrict__ w, real* __restrict
 // RELU: out = max(out, 0).  mask != nullptr: out = mask[n][co][p] > 0 ? out : 0.
 // Each thread computes PX consecutive columns of one row, so every weight read from shared
 // memory (a warp-wide broadcast) feeds PX FMAs and each input row segment of PX+2 values
-// feeds 3·PX taps.
-template <int CI, int CO, int PX, bool RELU>
-__global__ void __launch_bounds__(64) conv3x3_kernel(const real* __restrict__ in, const real* __restrict__ w,
+// feeds 3·PX taps.  NT threads per CTA (measured: 64 for conv2, 128 for the others).
+template <int CI, int CO, int PX, bool RELU, int NT>
+__global__ void __launch_bounds__(NT) conv3x3_kernel(const real* __restrict__ in, const real* __restrict__ w,
                                                      const real* __restrict__ bias, const real* __restrict__ mask,
                                                      real* __restrict__ out, int H, int W) {
     __shared__ real sw[CO * CI * 9];
@@ -123,11 +123,11 @@ __global__ void __launch_bounds__(64) conv3x3_kernel(const real* __restrict__ in
         }
 }
 
-template <int CI, int CO, int PX, bool RELU>
+template <int CI, int CO, int PX, bool RELU, int NT>
 void launch_conv(const real* in, const real* w, const real* bias, const real* mask, real* out, int n, int H, int W,
                  cudaStream_t st) {
-    const dim3 grid((W + 64 * PX - 1) / (64 * PX), H, n);
-    conv3x3_kernel<CI, CO, PX, RELU><<<grid, 64, 0, st>>>(in, w, bias, mask, out, H, W);
+    const dim3 grid((W + NT * PX - 1) / (NT * PX), H, n);
+    conv3x3_kernel<CI, CO, PX, RELU, NT><<<grid, NT, 0, st>>>(in, w, bias, mask, out, H, W);
 }
 
 // z = mean_h relu(s2), out = w3.z + b3, the loss and d out; per-CTA partials of the loss,
@@ -180,20 +180,20 @@ __global__ void __launch_bounds__(256) head_kernel(const real* __restrict__ s2, 
     }
 }
 
-// loss_sum += sum of per-sample losses; grads[b3], grads[w3] += column sums (fixed order)
+// loss_sum += sum of per-sample losses; grads[b3], grads[w3] += column sums.  One warp per
+// output: lane-strided partial sums then a fixed shuffle tree (deterministic).
 __global__ void head_finish_kernel(const real* __restrict__ parth, int n_samples, int xblocks,
                                    real* __restrict__ grads, real* __restrict__ loss_sum) {
-    const int j = threadIdx.x;
-    if (j >= HEAD_OUT) return;
-    real tot = 0.0;
-    for (int n = 0; n < n_samples; ++n) {
-        real s = 0.0;  // one sample's sum (its loss is the mean over its W columns)
-        for (int b = 0; b < xblocks; ++b) s += parth[((int64_t)n * xblocks + b) * HEAD_OUT + j];
-        tot += s;
+    const int j = blockIdx.x, lane = threadIdx.x;
+    const int64_t total = (int64_t)n_samples * xblocks;
+    real s = 0.0;
+    for (int64_t k = lane; k < total; k += 32) s += parth[k * HEAD_OUT + j];
+    s = warp_sum(s);
+    if (lane == 0) {
+        if (j == 0) *loss_sum += s;
+        else if (j == 1) grads[OFF_B3] += s;
+        else grads[OFF_W3 + j - 2] += s;
     }
-    if (j == 0) *loss_sum += tot;
-    else if (j == 1) grads[OFF_B3] += tot;
-    else grads[OFF_W3 + j - 2] += tot;
 }
 
 // d s2 = [s2 > 0] * w3[c] * d out[x] / H  (predictor.py:239-240)
@@ -378,16 +378,16 @@ int ap_train_backward(const double* grids, const double* targets, int32_t n_samp
     carve(&ws, workspace, n_samples, H, W);
     const int64_t px = (int64_t)n_samples * H * W;
     prep_weights_kernel<<<8, 512, 0, st>>>(weights, ws.w2t);
-    launch_conv<1, C1, 2, true>(grids, weights + OFF_W1, weights + OFF_B1, nullptr, ws.a1, n_samples, H, W, st);
-    launch_conv<C1, C2, 1, false>(ws.a1, weights + OFF_W2, weights + OFF_B2, nullptr, ws.s2, n_samples, H, W, st);
+    launch_conv<1, C1, 2, true, 128>(grids, weights + OFF_W1, weights + OFF_B1, nullptr, ws.a1, n_samples, H, W, st);
+    launch_conv<C1, C2, 1, false, 64>(ws.a1, weights + OFF_W2, weights + OFF_B2, nullptr, ws.s2, n_samples, H, W, st);
     const int xblocks = (W + 31) / 32;
     head_kernel<<<dim3(xblocks, n_samples), 256, 0, st>>>(ws.s2, weights, targets, ws.dout, ws.parth, H, W);
-    head_finish_kernel<<<1, 64, 0, st>>>(ws.parth, n_samples, xblocks, grads, loss_sum);
+    head_finish_kernel<<<HEAD_OUT, 32, 0, st>>>(ws.parth, n_samples, xblocks, grads, loss_sum);
     ds2_kernel<<<grid_for(C2 * px, 256), 256, 0, st>>>(ws.s2, weights, ws.dout, ws.ds2, H, W, C2 * px);
     corr2_tiled_kernel<<<CORR_CTAS, 256, 0, st>>>(ws.ds2, ws.a1, ws.part2, n_samples, H, W);
     corr2_finish_kernel<<<(CORR_OUT + 255) / 256, 256, 0, st>>>(ws.part2, CORR_CTAS, grads);
     // d a1 = conv2^T(d s2); d s1 = [a1 > 0] * d a1  (predictor.py:243-245; a1 > 0 <=> s1 > 0)
-    launch_conv<C2, C1, 2, false>(ws.ds2, ws.w2t, nullptr, ws.a1, ws.ds1, n_samples, H, W, st);
+    launch_conv<C2, C1, 2, false, 128>(ws.ds2, ws.w2t, nullptr, ws.a1, ws.ds1, n_samples, H, W, st);
     corr1_kernel<<<dim3(C1_CHUNKS, C1), 256, 0, st>>>(ws.ds1, grids, ws.part1, n_samples, H, W);
     corr1_finish_kernel<<<1, 192, 0, st>>>(ws.part1, C1_CHUNKS, grads);
     return launch_status("ap_train_backward");
