@@ -63,7 +63,11 @@ def parse():
                     help="N>1: independent sequences per GPU (weak) or one sequence with KV heads split (strong)")
     ap.add_argument("--offload", action="store_true",
                     help="cfg4: V in pinned host memory + cross-token prefetch of the predicted blocks")
-    ap.add_argument("--cpu-sample", type=int, default=48, help="oracle map-steps timed for cpu_baseline")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="reference map-steps timed for cpu_baseline")
+    ap.add_argument("--total-seqs", type=int, default=0,
+                    help="cfg5: this many sequences in total, sharded over the ranks by seq_shard (0: --batch per GPU)")
+    ap.add_argument("--parity-maps", type=int, default=8, help="maps re-checked against the CPU oracle after the run")
+    ap.add_argument("--parity-steps", type=int, default=3, help="decode steps of the in-run parity check")
     ap.add_argument("--dense-layers", type=int, default=0,
                     help="layer-skip policy: the first N layers always run full attention (the paper uses 2)")
     return ap.parse_args()
@@ -197,24 +201,77 @@ def profiled_traffic():
         return {}
 
 
-# ---------------------------------------------------------------- CPU oracle baseline
-def cpu_oracle_rate(ctx: int, budget: int, n_map_steps: int, seed: int = 0):
-    """Time the oracle's selector.step (selector.py:91-154: max_pool + forward + mask + topk) for one
-    (layer, head) map at context ctx, H=64, b=16 on this host.  Returns (seconds per map-step, cores)."""
+# ---------------------------------------------------------------- CPU reference baseline
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def _reference_modules():
+    """The UNMODIFIED reference package (attncast: pure Python + numpy) from baseline/_ref
+    (scripts/install_reference.sh).  None if it is not installed (then the pinned oracle port is timed)."""
+    if not (REF_DIR / "attncast" / "selector.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    try:
+        from attncast import predictor, selector
+    except Exception:
+        return None
+    return predictor, selector
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_map_steps(ctx: int, budget: int, n: int, seed: int = 0, threads: int | None = None):
+    """Time the reference's own selector.step (selector.py:91-154: max_pool + stack_history + forward +
+    mask + topk + expand) driven like evaluation._iter_selections (evaluation.py:90-115: observed row =
+    dense row at the previous selection) on one (layer, head) map at context ctx, H=64, b=16.
+    Returns (list of per-map-step seconds, kind, BLAS threads used)."""
     import numpy as np
-    from oracle import hotpath as O
+    from threadpoolctl import threadpool_info, threadpool_limits
+    ref = _reference_modules()
     rng = np.random.default_rng(seed)
-    cfg = O.Config(budget=budget)
-    w = O.init_weights(0)
-    prefill = [rng.dirichlet(np.full(ctx - 63 + i, 0.05)).astype(np.float32) for i in range(63)]
-    st = O.init_state(cfg, prefill)
-    rows = [rng.dirichlet(np.full(ctx + 1 + i, 0.05)).astype(np.float32) for i in range(n_map_steps)]
-    t0 = time.perf_counter()
-    for r in rows:
-        O.step(st, cfg, w, r, full_row=r)
-    dt = (time.perf_counter() - t0) / n_map_steps
-    cores = len(os.sched_getaffinity(0))
-    return dt, cores
+    prefill = [rng.dirichlet(np.full(ctx - 63 + i, 0.05)) for i in range(63)]
+    rows = [rng.dirichlet(np.full(ctx + i, 0.05)) for i in range(n)]
+    if ref is not None:
+        predictor, selector = ref
+        cfg = selector.SelectorConfig(budget=budget)
+        w = predictor.init_weights(0)
+        st = selector.init_state(cfg, prefill)
+        kind = "reference"
+
+        def step(st, obs, row):
+            return selector.step(st, cfg, w, obs, full_row=row)
+    else:
+        from oracle import hotpath as O
+        cfg = O.Config(budget=budget)
+        w = O.init_weights(0)
+        st = O.init_state(cfg, prefill)
+        kind = "port"
+
+        def step(st, obs, row):
+            return O.step(st, cfg, w, obs, full_row=row)
+    times, sel = [], None
+    with threadpool_limits(limits=threads):
+        used = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+        for r in rows:
+            t0 = time.perf_counter()
+            if sel is None:
+                obs = r
+            else:
+                obs = np.zeros_like(r)
+                idx = np.fromiter(sel, dtype=np.intp)
+                obs[idx] = r[idx]
+            st, sel = step(st, obs, r)
+            times.append(time.perf_counter() - t0)
+    return times, kind, used
 
 
 # ---------------------------------------------------------------- whole-step HBM accounting
@@ -329,6 +386,48 @@ def measure_selector(eng, reps=20):
     return us, W
 
 
+def inrun_parity(eng, n_maps: int, n_steps: int):
+    """After the timed run: for n_steps more decode steps, copy n_maps sampled maps' history windows
+    (the rows the engine's attention kernels emitted) to the host and re-run the CPU oracle on them
+    (forward predictor.py:185-216 + sink/local mask + topk selector.py:126-145, float64) with the
+    weights as the device holds them (fp32 image of the APW1 weights); the device's middle block ids
+    must equal the oracle's.  Returns {maps, steps, mismatches, exemptions, worst forecast err/bound}."""
+    import numpy as np
+    from oracle import hotpath as O
+    sel = eng.sel
+    cfg = eng.cfg
+    ocfg = O.Config(budget=cfg.budget, block_size=cfg.block_size, history=cfg.history,
+                    calibration_period=cfg.calibration_period, sink_tokens=cfg.sink_tokens,
+                    local_tokens=cfg.local_tokens, update_interval=cfg.update_interval)
+    w = O.Weights.from_flat(eng.pweights.flat().astype(np.float32).astype(np.float64))
+    rng = np.random.default_rng(7)
+    picks = sorted(rng.choice(sel.n_maps, size=min(n_maps, sel.n_maps), replace=False).tolist())
+    mism, checked, worst = 0, 0, 0.0
+    for _ in range(n_steps):
+        eng.step()
+        import torch
+        torch.cuda.synchronize()
+        st = sel.states()
+        scores = sel.scores.cpu().numpy()
+        for m in picks:
+            rows = sel.history_rows(m)
+            t = int(st[m]["row_len"])
+            W = int(st[m]["width"])
+            pred = O.forward(w, O.stack_history(rows, ocfg.history, W))
+            masked = O.masked_scores(ocfg, pred, t)
+            avail = int(np.count_nonzero(masked > -np.inf))
+            want = sorted(O.topk(masked, min(ocfg.middle_blocks, avail)))
+            got = sel.middle(m)
+            mism += got != want
+            floor = np.abs(pred).max() * 1e-2
+            worst = max(worst, float(np.max(np.abs(scores[m, :W] - pred) / (1e-3 * np.maximum(np.abs(pred), floor)))))
+            checked += 1
+    return {"maps": len(picks), "steps": n_steps, "map_steps": checked, "mismatches": int(mism), "exemptions": 0,
+            "worst_forecast_err_over_bound": round(worst, 4),
+            "what": "engine-emitted history windows (sparse_renorm rows, calibration rows) -> CPU oracle "
+                    "forward + mask + topk vs the device's middle blocks"}
+
+
 def roofline_for(eng, args, us, W, key):
     cfg = eng.cfg
     n_maps = eng.sel.n_maps
@@ -342,9 +441,14 @@ def roofline_for(eng, args, us, W, key):
     f_inc = n_maps * W * (5 * 9216 + 7 * 288)
     tf_peak = measured_tensor_peak()
     tflops = f_inc / (us * 1e-6) / 1e12
+    traffic = profiled_traffic().get(key)
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": profiled_traffic().get(key), "peak_kind": peak_kind,
-            "kernel": "ap_sel_step (conv_forecast_ws_kernel + sel_topk_kernel)", "maps": n_maps,
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_source": "ncu dram__bytes_read+write of the forecaster launch, profiles/roofline_traffic.json "
+                              "(not measured in this run)" if traffic is not None else None,
+            "peak_kind": peak_kind,
+            "kernel": "ap_sel_step (conv_forecast_wsm_kernel + sel_topk_reg_kernel + tie refine_kernel)",
+            "maps": n_maps,
             "us_per_launch": round(us, 2), "us_per_layer": round(us / eng.shape.n_layers, 3),
             "algorithmic_bytes_per_launch": b_alg,
             "tensor": {"algorithmic_flops_per_launch": f_inc, "achieved": round(tflops, 1), "peak": tf_peak,
@@ -360,6 +464,11 @@ def run_ours(args, rank, world):
     shape = SHAPES[args.model]
     G = shape.n_q_heads // shape.n_kv_heads
     group = 1 if args.group == "head" else G
+    if args.total_seqs:  # cfg5: the sequences of the whole job, sharded over the ranks (no collective)
+        from paper_2502_04077_b200.distributed import seq_shard
+        if args.total_seqs % world:
+            raise SystemExit("--total-seqs must be divisible by the number of GPUs")
+        _, args.batch = seq_shard(args.total_seqs, rank, world)
     cfg = SelectorConfig(budget=args.budget)
     total_steps = args.warmup + args.steps
     if args.offload:
@@ -401,6 +510,8 @@ def run_ours(args, rank, world):
                 "note": "algorithmic bytes of the whole decode step (weights once, selected KV, calibration K "
                         "share, history window) over the device-timed step"}
     e2e = measure_e2e(eng, args.steps, args.batch, world, units)
+    tie_run = eng.sel.tie_stats()
+    parity = inrun_parity(eng, args.parity_maps, args.parity_steps) if (rank == 0 and args.parity_maps > 0) else None
     us, W = measure_selector(eng)
     roofline = roofline_for(eng, args, us, W, f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
 
@@ -428,14 +539,27 @@ def run_ours(args, rank, world):
 
     cpu = None
     if rank == 0 and world == 1:
-        dt, cores = cpu_oracle_rate(args.ctx, args.budget, args.cpu_sample)
+        R = measure_reference(args.ctx, args.budget, 1, args.cpu_sample)
         maps_head = args.batch * shape.n_layers * shape.n_q_heads  # the reference's per-head semantics
-        per_token = dt * maps_head
-        cpu = {"value": round(args.batch / per_token, 6), "unit": "tok/s", "cores": cores, "kind": "port",
-               "sample": f"{args.cpu_sample} oracle selector.step map-steps (max_pool+forward+mask+topk, "
-                         f"H=64, W={-(-args.ctx // 16)}) timed, x {maps_head} (layer, head) maps per token; "
-                         f"OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}",
-               "s_per_map_step": round(dt, 4)}
+        rate = max(R["rate_par"], R["rate_all"])  # map-steps per second on this host
+        dt = 1.0 / rate
+        par = R["best"] == "process-parallel"
+        cpu = {"value": round(args.batch * rate / maps_head, 6), "unit": "tok/s",
+               "cores": R["cores"] if par else R["blas_threads"], "kind": R["kind"],
+               "sample": f"{args.cpu_sample} map-steps of the reference's selector.step "
+                         f"({'unmodified attncast from baseline/_ref' if R['kind'] == 'reference' else 'oracle port'}; "
+                         f"max_pool+forward+mask+topk+expand, H=64, W={-(-args.ctx // 16)}) "
+                         f"{'per process, ' + str(R['cores']) + ' processes x 1 BLAS thread' if par else 'in one process, all BLAS threads'}"
+                         f", extrapolated x {maps_head} (layer, q-head) maps per token",
+               "cpu_model": cpu_model(), "s_per_map_step_1_thread": round(R["dt_1"], 4),
+               "s_per_map_step_all_blas_threads": round(R["dt_all"], 4)}
+        if alt is not None or args.group == "head":  # same work on the GPU: ap_sel_step over the 1024 per-head maps
+            us_head = (alt["roofline"]["us_per_launch"] if args.group == "kv" else roofline["us_per_launch"])
+            cpu["selector_same_work"] = {
+                "gpu_us_per_token": us_head, "cpu_s_per_token": round(dt * maps_head, 2),
+                "ratio": round(dt * maps_head / (us_head * 1e-6), 1),
+                "note": "per-q-head selection (the reference's semantics), 1024 maps: ap_sel_step (forecast + top-k + "
+                        "guard) vs the reference's selector.step per map"}
 
     plain = sum(1 for v in variants if v == "plain")
     out = {
@@ -446,13 +570,17 @@ def run_ours(args, rank, world):
         "config": {"workload": f"{shape.name} decode, ctx {args.ctx}, budget {args.budget}, batch {args.batch}/GPU",
                    "model_shape": shape.name, "ctx": args.ctx, "budget": args.budget, "block": 16, "history": 64,
                    "calibration_period": 5, "batch_per_gpu": args.batch,
+                   "total_seqs": args.batch * (world if split is None else 1),
                    "selection": {"kv": f"per KV head ({G} q-heads share a map)", "head": "per q-head"}[args.group],
                    "forecaster_precision": args.precision, "dense_layers": args.dense_layers,
                    "parallelism": f"replicas x{world}" if split is None else f"kv-head split x{world} + all-gather",
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "step_hbm": step_hbm, "cpu_baseline": cpu,
-        "alt_selection": alt, "prefetch": prefetch,
+        "alt_selection": alt, "prefetch": prefetch, "parity": parity,
+        "tie_guard": dict(tie_run, steps=2 * args.steps + args.warmup + 1,
+                          note="cumulative over warm-up, timed and e2e steps: maps whose top-k boundary was "
+                               "ambiguous within the guard band and was re-scored in fp64"),
         "dense_tok_s": None if dense is None else round(dense, 2),
         "sparse_over_dense": None if dense is None else round(value / dense, 4),
         "clocks": clk.summary(),
@@ -463,30 +591,91 @@ def run_ours(args, rank, world):
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
+    """The reference's own CPU implementation of the path, as shipped: attncast.selector.step from
+    baseline/_ref (pure Python + numpy/OpenBLAS), per (layer, q-head) map — the reference has no GQA
+    and no batching.  One bench step = ONE map-step (a bounded sample: a token is 32 layers x 32 q-heads
+    = 1024 map-steps at 32K, ~2-3 min of CPU), so ms_per_step is the measured time of that sample and
+    value extrapolates it to tok/s.  Also timed at one BLAS thread."""
     if rank != 0:
         return
+    import multiprocessing as mp
+
+    import numpy as np
     from paper_2502_04077_b200.decode import SHAPES
     shape = SHAPES[args.model]
-    maps = args.batch * shape.n_layers * shape.n_q_heads  # the reference's semantics: one selector per (layer, head)
-    # warm-up then K steps; each step = one oracle map-step (a bounded sample of one token's 1024 map-steps)
-    cpu_oracle_rate(args.ctx, args.budget, max(1, args.warmup))
-    dt, cores = cpu_oracle_rate(args.ctx, args.budget, args.steps, seed=1)
-    value = args.batch / (dt * maps)
+    maps = args.batch * shape.n_layers * shape.n_q_heads
+    R = measure_reference(args.ctx, args.budget, args.warmup, args.steps)
+    kind, thr, cores, best = R["kind"], R["blas_threads"], R["cores"], R["best"]
+    dt_1, dt_all, rate_par, rate_all = R["dt_1"], R["dt_all"], R["rate_par"], R["rate_all"]
+    value = args.batch * max(rate_par, rate_all) / maps
+    ms_step = (dt_1 if best == "process-parallel" else dt_all) * 1e3  # one bench step = one map-step per process
+    model = cpu_model()
+    sample = (f"{args.steps} timed map-steps (after {args.warmup} warm-up) of attncast.selector.step at t={args.ctx} "
+              f"{'in each of ' + str(cores) + ' processes (1 BLAS thread each, independent maps)' if best == 'process-parallel' else 'in one process with all BLAS threads'}; "
+              f"{'unmodified reference from baseline/_ref' if kind == 'reference' else 'oracle port'}")
     out = {"metric": METRIC, "value": round(value, 6), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(dt * maps * 1e3, 1), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic Dirichlet attention rows",
-           "impl": "reference",
+           "warmup": args.warmup, "ms_per_step": round(ms_step, 2), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic Dirichlet(0.05) attention rows, init_weights(0)", "impl": "reference",
            "config": {"workload": f"{shape.name} decode, ctx {args.ctx}, budget {args.budget}, batch {args.batch}",
-                      "selection": "per (layer, head) map — the reference's semantics", "maps_per_token": maps},
-           "cpu_baseline": {"value": round(value, 6), "unit": "tok/s", "cores": cores, "kind": "port",
-                            "sample": f"{args.steps} oracle selector.step map-steps per run, x{maps} maps/token"},
+                      "selection": "per (layer, q-head) map - the reference's semantics", "maps_per_token": maps,
+                      "step": "one bench step = one map-step of selector.step per process (1/1024 of a token "
+                              "each); value = map-steps/s over all processes / 1024"},
+           "extrapolated_from": f"map-step samples x {maps} maps per token",
+           "cpu_baseline": {"value": round(value, 6), "unit": "tok/s", "cores": cores if best == "process-parallel" else thr,
+                            "kind": kind, "sample": sample, "cpu_model": model, "host_threads": cores},
+           "variants": {"process_parallel_1_blas_thread": {"tok_s": round(args.batch * rate_par / maps, 6),
+                                                           "s_per_map_step": round(dt_1, 4), "processes": cores},
+                        "one_process_all_blas_threads": {"tok_s": round(args.batch * rate_all / maps, 6),
+                                                         "s_per_map_step": round(dt_all, 4), "blas_threads": thr}},
            "e2e": {"value": round(value, 6), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
+def measure_reference(ctx, budget, warmup, steps):
+    """The reference's selector.step throughput on this host: (a) one process with all BLAS threads,
+    (b) one process per host core with one BLAS thread each, each advancing its own independent map
+    ((layer, head) states advance independently) - the best CPU throughput of the reference."""
+    import multiprocessing as mp
+
+    import numpy as np
+    n = warmup + steps
+    ts, kind, thr = reference_map_steps(ctx, budget, n, seed=1)
+    dt_all = float(np.mean(ts[warmup:]))
+    cores = len(os.sched_getaffinity(0))
+    with mp.get_context("spawn").Pool(cores) as pool:
+        per = pool.map(_ref_worker, [(ctx, budget, n, 10 + i) for i in range(cores)])
+    dt_1 = float(np.mean([np.mean(t[warmup:]) for t in per]))
+    rate_par, rate_all = cores / dt_1, 1.0 / dt_all
+    return {"kind": kind, "blas_threads": thr, "cores": cores, "dt_1": dt_1, "dt_all": dt_all, "rate_par": rate_par,
+            "rate_all": rate_all, "best": "process-parallel" if rate_par >= rate_all else "blas-threads"}
+
+
+def _ref_worker(a):
+    ctx, budget, n, seed = a
+    ts, _, _ = reference_map_steps(ctx, budget, n, seed=seed, threads=1)
+    return ts
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` without a launcher: re-exec under torchrun with N ranks (one per GPU)."""
+    if "WORLD_SIZE" in os.environ or args.gpus <= 1:
+        return
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    self_launch(args)
     rank, world = dist_init()
+    if world != args.gpus and int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit(f"--gpus {args.gpus} disagrees with WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

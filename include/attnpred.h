@@ -114,6 +114,9 @@ typedef struct ap_map_state {
     int32_t width;     /* W of the newest row = ceil(row_len / b) */
     int32_t r_width;   /* W when the r-map was last brought up to date */
     int32_t n_mid;     /* number of middle blocks currently selected */
+    int32_t r_wgen;    /* forecaster weight generation the r-map was built with (ap_set_weights bumps it) */
+    int32_t tie_n;     /* exact-boundary guard at the last update: 0 = no ambiguity, n > 0 = n near-tie
+                        * candidates re-scored in fp64, -n = n candidates exceeded the guard capacity */
     int32_t pad_;
 } ap_map_state;
 
@@ -138,6 +141,8 @@ typedef struct ap_selector {
     int32_t* mid_blocks;      /* [n_maps][k_mid] middle block ids, ascending        */
     uint32_t* mid_mask;       /* [n_maps][ceil(w_max/32)] bitmask of middle blocks  */
     int32_t* status;          /* [1] device status word                             */
+    int32_t* tie_ws;          /* exact-boundary guard workspace, ap_sel_tie_ws_bytes(n_maps) bytes, zeroed
+                               * once before first use; NULL disables the guard                         */
 } ap_selector;
 
 /* Zero the state of every map (selector.init_state with no prefill rows). */
@@ -167,8 +172,23 @@ int ap_sel_push_compressed(const ap_selector* s, const float* comp, int64_t comp
  * (incrementally: only the history rows whose 3x3 receptive field changed),
  * forecast the next compressed row, mask the sink/local covering blocks
  * (selector.py:134-142), take top-min(K, available) (selector.py:143-145)
- * into mid_blocks / mid_mask; then counter += 1. */
+ * into mid_blocks / mid_mask; then counter += 1.
+ * Exact-boundary guard (s->tie_ws != NULL, precisions FP32 / F16X3): blocks
+ * within band = rel * max(|tau|, floor * max|score|) of the k-th forecast tau
+ * are, when the boundary among them is ambiguous, re-scored in fp64 from the
+ * history window and ordered like selector.py:80, so the ids equal the
+ * float64 reference's (per-map outcome in ap_map_state.tie_n). */
 int ap_sel_step(const ap_selector* s, int precision, void* stream);
+
+/* Bytes of the guard workspace for n_maps maps (zero it once before first use). */
+int64_t ap_sel_tie_ws_bytes(int32_t n_maps);
+/* [host] cumulative guard counters of a workspace: [maps over capacity, maps re-scored,
+ * candidates re-scored].  Synchronous copy. */
+int ap_sel_tie_stats(const int32_t* tie_ws, int32_t* host_out3);
+/* [host] guard switch and band (defaults: on, rel 2^-13, floor 2^-6; env ATTNPRED_TIE_GUARD /
+ * ATTNPRED_TIE_REL / ATTNPRED_TIE_FLOOR).  Applies to later ap_sel_step calls (graphs keep the
+ * values they were captured with). */
+int ap_sel_set_tie_guard(int enabled, float rel, float floor_frac);
 
 /* Number of persistent CTAs the predictor kernels use (for reporting). */
 int ap_sel_grid_ctas(int precision);
@@ -374,6 +394,14 @@ int ap_train_backward(const double* grids, const double* targets, int32_t n_samp
  * m = b1 m + (1-b1) g, v = b2 v + (1-b2) g g, w -= lr (m / (1-b1^step)) / (sqrt(v / (1-b2^step)) + eps). */
 int ap_adam_step(double* weights, double* m, double* v, const double* grad_sum, int32_t n_params, double batch,
                  double lr, double beta1, double beta2, double eps, int64_t step, void* stream);
+/* predictor.forward (predictor.py:185-216) in fp64 — the reference's arithmetic type — for n_grids
+ * equal-shape grids [n][H][W] (contiguous fp64) with fp64 weights (4833, APW1 order): out[n*out_stride + w].
+ * The default of the reference-compatible `predictor.forward`; uses the conv/head kernels of
+ * ap_train_backward, so a forward used as a training target gives an exactly zero residual
+ * (reference test_predictor.py:64-70).  workspace: ap_forward_f64_workspace_bytes(n, H, W). */
+int64_t ap_forward_f64_workspace_bytes(int32_t n_grids, int32_t H, int32_t W);
+int ap_predict_forward_f64(const double* grids, int32_t n_grids, int32_t H, int32_t W, const double* weights,
+                           double* out, int64_t out_stride, void* workspace, int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

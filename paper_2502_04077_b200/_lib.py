@@ -41,7 +41,8 @@ class MapState(ctypes.Structure):
     _fields_ = [
         ("n_pushed", ctypes.c_int64), ("r_pushed", ctypes.c_int64), ("row_len", ctypes.c_int64),
         ("counter", ctypes.c_int64), ("mid_clip", ctypes.c_int64), ("width", ctypes.c_int32),
-        ("r_width", ctypes.c_int32), ("n_mid", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("r_width", ctypes.c_int32), ("n_mid", ctypes.c_int32), ("r_wgen", ctypes.c_int32),
+        ("tie_n", ctypes.c_int32), ("pad_", ctypes.c_int32),
     ]
 
 
@@ -54,7 +55,7 @@ class Selector(ctypes.Structure):
         ("ring", ctypes.c_void_p), ("rmap", ctypes.c_void_p), ("rsum", ctypes.c_void_p),
         ("slot_width", ctypes.c_void_p), ("slot_xmax", ctypes.c_void_p),
         ("state", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("mid_blocks", ctypes.c_void_p),
-        ("mid_mask", ctypes.c_void_p), ("status", ctypes.c_void_p),
+        ("mid_mask", ctypes.c_void_p), ("status", ctypes.c_void_p), ("tie_ws", ctypes.c_void_p),
     ]
 
 
@@ -83,7 +84,7 @@ class VPages(ctypes.Structure):
     ]
 
 
-MAP_STATE_BYTES = ctypes.sizeof(MapState)  # 56
+MAP_STATE_BYTES = ctypes.sizeof(MapState)  # 64
 
 
 class TraceHeaderC(ctypes.Structure):
@@ -110,6 +111,9 @@ SIGNATURES = {
     "ap_sel_push_compressed": (ctypes.c_int, [ctypes.POINTER(Selector), _P, _I64, _I64, ctypes.c_int, _P]),
     "ap_sel_step": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.c_int, _P]),
     "ap_sel_grid_ctas": (ctypes.c_int, [ctypes.c_int]),
+    "ap_sel_tie_ws_bytes": (ctypes.c_int64, [_I32]),
+    "ap_sel_tie_stats": (ctypes.c_int, [_P, _P]),
+    "ap_sel_set_tie_guard": (ctypes.c_int, [ctypes.c_int, ctypes.c_float, ctypes.c_float]),
     "ap_attn_dense": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.c_int, ctypes.POINTER(Selector),
                                      _I32, _I32, _I32, ctypes.c_int, _P]),
     "ap_attn_set_calib_kernel": (ctypes.c_int, [ctypes.c_int]),
@@ -154,6 +158,8 @@ SIGNATURES = {
     "ap_train_backward": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P, _P, _P, _P, ctypes.c_int64, _P]),
     "ap_adam_step": (ctypes.c_int, [_P, _P, _P, _P, _I32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_double, _I64, _P]),
+    "ap_forward_f64_workspace_bytes": (ctypes.c_int64, [_I32, _I32, _I32]),
+    "ap_predict_forward_f64": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _I64, _P, ctypes.c_int64, _P]),
 }
 
 _lib = None

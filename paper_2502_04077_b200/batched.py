@@ -22,13 +22,14 @@ import numpy as np
 
 from . import _device as D
 from . import _lib
-from .errors import ConfigError, ParameterError
+from .errors import ParameterError
 
 PUSH_PREFILL, PUSH_DENSE, PUSH_OBSERVED = 0, 1, 2
 
 _STATE_DTYPE = np.dtype([
     ("n_pushed", "<i8"), ("r_pushed", "<i8"), ("row_len", "<i8"), ("counter", "<i8"), ("mid_clip", "<i8"),
-    ("width", "<i4"), ("r_width", "<i4"), ("n_mid", "<i4"), ("pad_", "<i4"),
+    ("width", "<i4"), ("r_width", "<i4"), ("n_mid", "<i4"), ("r_wgen", "<i4"),
+    ("tie_n", "<i4"), ("pad_", "<i4"),
 ])
 assert _STATE_DTYPE.itemsize == _lib.MAP_STATE_BYTES
 
@@ -41,7 +42,7 @@ class BatchedSelector:
     w_max: the largest compressed width any map will reach (ceil(t_max/b)).
     """
 
-    def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "fp16x3", device=None):
+    def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "fp16x3", device=None, tie_guard: bool = True):
         cfg.validate()
         if n_maps < 1 or w_max < 1:
             raise ParameterError("n_maps and w_max must be >= 1")
@@ -66,6 +67,12 @@ class BatchedSelector:
         self.mid_blocks = torch.zeros(n_maps, max(self.k_mid, 1), dtype=i32, device=dev)
         self.mid_mask = torch.zeros(n_maps, words, dtype=i32, device=dev)
         self.status = torch.zeros(1, dtype=i32, device=dev)
+        # exact-boundary guard workspace (csrc/tieguard.cuh): near-tie candidates of the top-k boundary
+        # are re-scored in fp64 so the block ids equal the float64 reference's
+        self.tie_ws = None
+        if tie_guard:
+            nb = int(_lib.fn("ap_sel_tie_ws_bytes")(self.n_maps))
+            self.tie_ws = torch.zeros(-(-nb // 4), dtype=i32, device=dev)
         self._desc = _lib.Selector(
             n_maps=n_maps, history=H, block=cfg.block_size, w_max=w_max, k_mid=self.k_mid,
             sink=cfg.sink_tokens, local=cfg.local_tokens, calib_period=cfg.calibration_period,
@@ -74,6 +81,7 @@ class BatchedSelector:
             slot_width=self.slot_width.data_ptr(), slot_xmax=self.slot_xmax.data_ptr(),
             state=self.state.data_ptr(), scores=self.scores.data_ptr(), mid_blocks=self.mid_blocks.data_ptr(),
             mid_mask=self.mid_mask.data_ptr(), status=self.status.data_ptr(),
+            tie_ws=None if self.tie_ws is None else self.tie_ws.data_ptr(),
         )
         self.reset()
 
@@ -114,6 +122,17 @@ class BatchedSelector:
         st = self.states()[i]
         return self.mid_blocks[i, : int(st["n_mid"])].cpu().tolist()
 
+    def tie_stats(self) -> dict:
+        """Cumulative exact-boundary guard counters: maps whose boundary was ambiguous and re-scored in
+        fp64 (``refined_maps``, ``candidates``) and maps whose ambiguity exceeded the guard's capacity
+        (``overflow``: those kept the fp32 order)."""
+        if self.tie_ws is None:
+            return {"enabled": False}
+        out = (ctypes.c_int32 * 3)()
+        D.torch().cuda.synchronize()
+        _lib.check(_lib.fn("ap_sel_tie_stats")(_lib.ptr(self.tie_ws), ctypes.cast(out, ctypes.c_void_p)), "tie")
+        return {"enabled": True, "overflow": int(out[0]), "refined_maps": int(out[1]), "candidates": int(out[2])}
+
     def check_status(self) -> None:
         D.sync_and_check(self.status, "selector")
 
@@ -130,9 +149,3 @@ class BatchedSelector:
             out.append(ring[s, : widths[s]].astype(np.float64))
         return out
 
-
-def check_config(cfg) -> None:
-    try:
-        cfg.validate()
-    except ConfigError:
-        raise

@@ -1203,6 +1203,13 @@ static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t m
     P.seq_len = a->seq_len; P.out = (__nv_bfloat16*)a->out; P.lse = a->lse; P.partial = a->partial;
     P.bmax = a->bmax; P.w_max = a->w_max; P.counters = a->counters;
     AP_REQUIRE(a->counters != nullptr, AP_EPARAM, "counters workspace is required");
+    // the kernels use P.block for the sink/local/middle units and the emitted width, the selector masks in
+    // sel->block units and its ring rows are w_max wide: both must agree with the attention descriptor
+    AP_REQUIRE(!sel || sel->block == a->block, AP_ECONFIG, "selector block size %d != attention block size %d",
+               sel ? sel->block : 0, a->block);
+    AP_REQUIRE(!sel || sel->w_max >= (a->t_max + a->block - 1) / a->block, AP_ECONFIG,
+               "selector w_max %d < ceil(t_max / block) = %d", sel ? sel->w_max : 0,
+               (a->t_max + a->block - 1) / a->block);
     if (sel) P.sel = *sel; else memset(&P.sel, 0, sizeof(P.sel));
     memset(&P.vp, 0, sizeof(P.vp));
     P.sparse_units = 0;

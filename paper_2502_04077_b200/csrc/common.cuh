@@ -157,6 +157,16 @@ __device__ __forceinline__ unsigned long long order_key(double v) {
     return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// Exact-boundary guard parameters of the selector top-k (tieguard.cuh; set by ap_sel_step).
+namespace tie {
+struct Params {
+    int enabled;
+    float rel, floor;   // band = rel * max(|tau|, floor * max|score|) around the k-th score tau
+    const float* w;     // the installed 4833 fp32 weights (c_w)
+    const int* wgen;    // the installed weight generation (g_wgen)
+};
+}  // namespace tie
+
 __host__ __device__ __forceinline__ int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ------------------------------------------------------------ block reduce/scan

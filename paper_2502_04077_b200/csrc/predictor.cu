@@ -45,6 +45,8 @@ __device__ __align__(16) uint4 g_bpack[2 * 9 * BTILE_BYTES / 16];
 constexpr int B96_BYTES = 96 * 16 * 2;
 __device__ __align__(16) uint4 g_bpack96[2 * 3 * B96_BYTES / 16];
 __device__ int g_wexp;            // power-of-2 exponent applied to w2
+__device__ int g_wgen;            // weight generation: bumped by every ap_set_weights; a map whose r-map was
+                                  // built under another generation is recomputed in full (plan_task)
 __device__ float g_w1abs[16];     // sum_t |w1[c][t]|  (a1 magnitude bound)
 __device__ float g_b1abs[16];     // |b1[c]|
 
@@ -86,7 +88,10 @@ __global__ void pack_weights_kernel() {
     atomicMax(reinterpret_cast<int*>(&s_max), __float_as_int(m));  // non-negative floats order as ints
     __syncthreads();
     const int e = f16_scale_exp(s_max);
-    if (threadIdx.x == 0) g_wexp = e;
+    if (threadIdx.x == 0) {
+        g_wexp = e;
+        g_wgen = g_wgen + 1;
+    }
     if (threadIdx.x == 0) {  // a1 <= max_c |b1_c| + max_c sum_t |w1_ct| * max|x|  (slot 0 holds the maxima)
         float wm = 0.f, bm = 0.f;
         for (int c = 0; c < 16; ++c) {
@@ -160,7 +165,8 @@ __device__ __forceinline__ Task plan_task(const ConvParams& P, const ap_map_stat
         return T;
     }
     const int64_t s = st.n_pushed - st.r_pushed;
-    bool full = st.r_pushed < 0 || (int64_t)H - s - 2 <= 2;
+    // r-map rows stay valid only under the weights they were computed with (ap_set_weights)
+    bool full = st.r_pushed < 0 || (int64_t)H - s - 2 <= 2 || st.r_wgen != g_wgen;
     if (!full && st.r_width != st.width) {  // columns from min(W_old, W_new)-1 changed in every row
         int lo = (st.r_width < st.width ? st.r_width : st.width) - 1;
         if (lo < 0) lo = 0;
@@ -733,7 +739,43 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
     return launch_status("conv_forecast_kernel");
 }
 
-void launch_sel_topk(const ap_selector& s, cudaStream_t stream);
+void launch_sel_topk(const ap_selector& s, const tie::Params& tp, cudaStream_t stream);
+
+// Exact-boundary guard (tieguard.cuh): on for the fp32-class precisions unless ATTNPRED_TIE_GUARD=0.
+// The band must cover twice the forecaster's worst error (measured in
+// tests/test_gpu_parity_32k.py); ATTNPRED_TIE_REL / ATTNPRED_TIE_FLOOR override it.
+static int g_tie_on = -1;
+static float g_tie_rel = 0.f, g_tie_floor = 0.f;
+
+static void tie_init() {
+    if (g_tie_on >= 0) return;
+    const char* e = getenv("ATTNPRED_TIE_GUARD");
+    g_tie_on = !(e && strcmp(e, "0") == 0);
+    const char* r = getenv("ATTNPRED_TIE_REL");
+    const char* f = getenv("ATTNPRED_TIE_FLOOR");
+    g_tie_rel = r ? (float)atof(r) : 1.220703125e-4f;  // 2^-13
+    g_tie_floor = f ? (float)atof(f) : 1.5625e-2f;     // 2^-6
+}
+
+static tie::Params tie_params(int precision) {
+    static const float* w = nullptr;
+    static const int* gen = nullptr;
+    tie_init();
+    if (!w) {
+        void* p = nullptr;
+        if (cudaGetSymbolAddress(&p, c_w) == cudaSuccess) w = static_cast<const float*>(p);
+        if (cudaGetSymbolAddress(&p, g_wgen) == cudaSuccess) gen = static_cast<const int*>(p);
+    }
+    const int env_on = g_tie_on;
+    const float rel = g_tie_rel, flo = g_tie_floor;
+    tie::Params tp;
+    tp.enabled = env_on && precision != AP_PREC_F16 && w != nullptr;
+    tp.rel = rel;
+    tp.floor = flo;
+    tp.w = w;
+    tp.wgen = gen;
+    return tp;
+}
 
 }  // namespace ap
 
@@ -808,7 +850,7 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream) {
         int rc = launch_conv(P, precision, st);
         if (rc != AP_OK) return rc;
     }
-    launch_sel_topk(*s, st);
+    launch_sel_topk(*s, tie_params(precision), st);
     return launch_status("sel_topk_kernel");
 }
 
@@ -824,6 +866,15 @@ int ap_debug_trace(long long* host_out) {
                           : k == 3 ? cudaMemcpyFromSymbol(host_out, wsm::g_trace, sizeof(long long) * 64 * 8)
                                    : cudaMemcpyFromSymbol(host_out, ws::g_trace, sizeof(long long) * 64 * 8);
     return e == cudaSuccess ? AP_OK : AP_ECUDA;
+}
+
+int ap_sel_set_tie_guard(int enabled, float rel, float floor_frac) {
+    AP_REQUIRE(rel >= 0.f && floor_frac >= 0.f, AP_EPARAM, "tie band parameters must be non-negative");
+    tie_init();
+    g_tie_on = enabled != 0;
+    g_tie_rel = rel;
+    g_tie_floor = floor_frac;
+    return AP_OK;
 }
 
 int ap_sel_grid_ctas(int precision) {

@@ -10,6 +10,7 @@
 // the lowest-index keys == T until k are taken.  Output ids are ascending,
 // which is the set the reference returns.  Bit-exact on identical inputs.
 #include "common.cuh"
+#include "tieguard.cuh"
 
 namespace ap {
 
@@ -132,19 +133,23 @@ struct MaskedScoreKey {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s) {
+__global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s, tie::Params tp) {
     __shared__ int hist[256];
     __shared__ int scan_tmp[NT / 32 + 2];
-    __shared__ int s_nan;
+    __shared__ int s_nan, s_amax, s_bcast;
     const int m = blockIdx.x;
     ap_map_state st = s.state[m];
     const bool update = (st.counter % s.update_interval) == 0;
     const int words = (s.w_max + 31) / 32;
     uint32_t* mask = s.mid_mask + (int64_t)m * words;
     int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
-    if (threadIdx.x == 0) s_nan = 0;
+    if (threadIdx.x == 0) {
+        s_nan = 0;
+        s_amax = 0;
+    }
     __syncthreads();
     int count = st.n_mid;
+    int tie_n = 0;
     if (update && s.k_mid > 0 && st.width > 0) {
         const int W = st.width;
         const int b = s.block;
@@ -163,12 +168,15 @@ __global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s) {
         if (kf.local_hi > W) kf.local_hi = W;
         // available = #finite after masking (selector.py:143)
         int n_masked_local = 0;
+        float amax = 0.f;
         for (int i = threadIdx.x; i < W; i += NT) {
             bool masked = (i >= kf.sink_lo && i < kf.sink_hi) || (i >= kf.local_lo && i < kf.local_hi);
             float v = kf.scores[i];
             if (v != v) s_nan = 1;
             n_masked_local += masked || (v == -INFINITY);
+            if (!masked && fabsf(v) <= 3.402823466e38f) amax = fmaxf(amax, fabsf(v));
         }
+        atomicMax(&s_amax, __float_as_int(amax));  // non-negative floats order as ints
         int n_masked = 0;
         block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
         if (s_nan) raise_status(s.status, AP_ENUMERIC);
@@ -184,6 +192,9 @@ __global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s) {
                 mid[pos] = i;
                 atomicOr(&mask[i >> 5], 1u << (i & 31));
             });
+            if (tp.enabled && s.tie_ws)
+                tie_n = tie::detect<NT>(s, tp, m, kf, W, k, T, __int_as_float(s_amax), kf.sink_hi, kf.local_lo,
+                                        kf.local_hi, scan_tmp, &s_bcast);
         } else {
             count = 0;
         }
@@ -192,6 +203,8 @@ __global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s) {
             st.mid_clip = t;
             st.r_pushed = st.n_pushed;
             st.r_width = st.width;
+            st.r_wgen = tp.wgen ? *tp.wgen : 0;
+            st.tie_n = tie_n;
         }
     } else if (update && s.k_mid <= 0) {
         for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
@@ -208,19 +221,23 @@ __global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s) {
 // t owns blocks [t * IPT, t * IPT + IPT), loaded once; the radix passes and the ordered emission run
 // on registers (the generic kernel re-reads the row from global memory on every pass).
 template <int NT, int IPT>
-__global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s) {
+__global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Params tp) {
     __shared__ int hist[256];
     __shared__ int scan_tmp[NT / 32 + 2];
-    __shared__ int s_nan;
+    __shared__ int s_nan, s_amax, s_bcast;
     const int m = blockIdx.x;
     ap_map_state st = s.state[m];
     const bool update = (st.counter % s.update_interval) == 0;
     const int words = (s.w_max + 31) / 32;
     uint32_t* mask = s.mid_mask + (int64_t)m * words;
     int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
-    if (threadIdx.x == 0) s_nan = 0;
+    if (threadIdx.x == 0) {
+        s_nan = 0;
+        s_amax = 0;
+    }
     __syncthreads();
     int count = st.n_mid;
+    int tie_n = 0;
     if (update && s.k_mid > 0 && st.width > 0) {
         const int W = st.width;
         const int b = s.block;
@@ -239,6 +256,7 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s) {
         uint32_t key[IPT];
         int n_masked_local = 0;
         bool nan = false;
+        float amax = 0.f;
 #pragma unroll
         for (int q = 0; q < IPT; ++q) {
             const int i = i0 + q;
@@ -247,8 +265,10 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s) {
             const bool masked = i >= W || (i < sink_hi) || (i >= local_lo && i < local_hi);
             key[q] = masked ? 0u : order_key(v);  // 0 sorts below every real key (and is never taken)
             n_masked_local += i < W && (masked || v == -INFINITY);
+            if (!masked && fabsf(v) <= 3.402823466e38f) amax = fmaxf(amax, fabsf(v));
         }
         if (nan) s_nan = 1;
+        atomicMax(&s_amax, __float_as_int(amax));  // non-negative floats order as ints
         int n_masked = 0;
         block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
         if (s_nan) raise_status(s.status, AP_ENUMERIC);
@@ -315,6 +335,14 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s) {
             for (int wq = 0; wq < (IPT + 31) / 32 + 1; ++wq)
                 if (bits[wq]) atomicOr(&mask[(i0 >> 5) + wq], bits[wq]);
             count = total;
+            if (tp.enabled && s.tie_ws) {
+                auto kf = [&](int i) -> uint32_t {
+                    const bool masked = (i < sink_hi) || (i >= local_lo && i < local_hi);
+                    return masked ? 0u : order_key(sc[i]);
+                };
+                tie_n = tie::detect<NT>(s, tp, m, kf, W, k, T, __int_as_float(s_amax), sink_hi, local_lo, local_hi,
+                                        scan_tmp, &s_bcast);
+            }
         } else {
             count = 0;
         }
@@ -323,6 +351,8 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s) {
             st.mid_clip = t;
             st.r_pushed = st.n_pushed;
             st.r_width = st.width;
+            st.r_wgen = tp.wgen ? *tp.wgen : 0;
+            st.tie_n = tie_n;
         }
     } else if (update && s.k_mid <= 0) {
         for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
@@ -334,15 +364,34 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s) {
     }
 }
 
-void launch_sel_topk(const ap_selector& s, cudaStream_t stream) {
-    if (s.w_max <= 256 * 8) sel_topk_reg_kernel<256, 8><<<s.n_maps, 256, 0, stream>>>(s);
-    else if (s.w_max <= 256 * 16) sel_topk_reg_kernel<256, 16><<<s.n_maps, 256, 0, stream>>>(s);
-    else sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s);
+void launch_sel_topk(const ap_selector& s, const tie::Params& tp, cudaStream_t stream) {
+    if (s.w_max <= 256 * 8) sel_topk_reg_kernel<256, 8><<<s.n_maps, 256, 0, stream>>>(s, tp);
+    else if (s.w_max <= 256 * 16) sel_topk_reg_kernel<256, 16><<<s.n_maps, 256, 0, stream>>>(s, tp);
+    else sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s, tp);
+    if (tp.enabled && s.tie_ws) {
+        static int grid = 0;
+        if (!grid) {
+            cudaFuncSetAttribute(tie::refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tie::SMEM_BYTES);
+            grid = 2 * ap_device_sm_count();
+        }
+        tie::refine_kernel<<<grid, tie::NT, tie::SMEM_BYTES, stream>>>(s, tp);
+    }
 }
 
 }  // namespace ap
 
 using namespace ap;
+
+extern "C" int64_t ap_sel_tie_ws_bytes(int32_t n_maps) {
+    return n_maps < 1 ? 0 : 4 * tie::ws_words(n_maps);
+}
+
+extern "C" int ap_sel_tie_stats(const int32_t* tie_ws, int32_t* host_out3) {
+    // cumulative [overflow maps, refined maps, re-scored candidates] since the workspace was zeroed
+    AP_REQUIRE(tie_ws && host_out3, AP_EPARAM, "null pointer");
+    return cudaMemcpy(host_out3, tie_ws + tie::H_OVERFLOW, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost) ==
+                   cudaSuccess ? AP_OK : AP_ECUDA;
+}
 
 extern "C" int ap_topk(const void* values, int dtype, int64_t n_rows, int64_t row_stride, int32_t n, int32_t k,
                        int32_t* out_ids, int64_t out_stride, int32_t* out_count, int32_t* status, void* stream) {

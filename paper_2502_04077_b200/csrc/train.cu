@@ -130,6 +130,43 @@ void launch_conv(const real* in, const real* w, const real* bias, const real* ma
     conv3x3_kernel<CI, CO, PX, RELU, NT><<<grid, NT, 0, st>>>(in, w, bias, mask, out, H, W);
 }
 
+// z[c][lane] = mean_h relu(s2) of one column (predictor.py:196-198); shared by the training head and
+// the inference-only fp64 forward so both form `out` with the same operations in the same order.
+__device__ __forceinline__ void head_z(const real* __restrict__ s2, real (*zs)[33], int n, int x, bool live,
+                                       int H, int W) {
+    const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    const int64_t plane = (int64_t)H * W;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int c = grp * 4 + j;
+        real s = 0.0;
+        if (live) {
+            const real* src = s2 + ((int64_t)n * C2 + c) * plane + x;
+            for (int y = 0; y < H; ++y) s += fmax(src[(int64_t)y * W], 0.0);
+        }
+        zs[c][lane] = s / H;
+    }
+}
+
+// out = w3 . z + b3 (predictor.py:199)
+__device__ __forceinline__ real head_out(const real* __restrict__ w, const real (*zs)[33], int lane) {
+    real out = 0.0;
+#pragma unroll
+    for (int c = 0; c < C2; ++c) out = fma(w[OFF_W3 + c], zs[c][lane], out);
+    return out + w[OFF_B3];
+}
+
+// Inference only: out[n][x] of predictor.forward in fp64 (one warp group per 32 columns).
+__global__ void __launch_bounds__(256) head_fwd_kernel(const real* __restrict__ s2, const real* __restrict__ w,
+                                                       real* __restrict__ out, int64_t out_stride, int H, int W) {
+    __shared__ real zs[C2][33];
+    const int lane = threadIdx.x & 31;
+    const int x = blockIdx.x * 32 + lane, n = blockIdx.y;
+    head_z(s2, zs, n, x, x < W, H, W);
+    __syncthreads();
+    if (threadIdx.x < 32 && x < W) out[(int64_t)n * out_stride + x] = head_out(w, zs, lane);
+}
+
 // z = mean_h relu(s2), out = w3.z + b3, the loss and d out; per-CTA partials of the loss,
 // d b3 = sum d out and d w3 = sum z * d out (predictor.py:196-199,230-238).  CTA = 32 columns x
 // 8 channel groups of 4: each thread sums its 4 channel planes down one column, z goes through
@@ -142,24 +179,11 @@ __global__ void __launch_bounds__(256) head_kernel(const real* __restrict__ s2, 
     const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
     const int x = blockIdx.x * 32 + lane, n = blockIdx.y;
     const bool live = x < W;
-    const int64_t plane = (int64_t)H * W;
     real* part = parth + ((int64_t)n * gridDim.x + blockIdx.x) * HEAD_OUT;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const int c = grp * 4 + j;
-        real s = 0.0;
-        if (live) {
-            const real* src = s2 + ((int64_t)n * C2 + c) * plane + x;
-            for (int y = 0; y < H; ++y) s += fmax(src[(int64_t)y * W], 0.0);
-        }
-        zs[c][lane] = s / H;
-    }
+    head_z(s2, zs, n, x, live, H, W);
     __syncthreads();
     if (grp == 0) {
-        real out = 0.0;
-#pragma unroll
-        for (int c = 0; c < C2; ++c) out = fma(w[OFF_W3 + c], zs[c][lane], out);
-        out += w[OFF_B3];
+        const real out = head_out(w, zs, lane);
         const real resid = live ? out - target[(int64_t)n * W + x] : 0.0;
         const real d = 2.0 * resid / W;
         ds[lane] = d;
@@ -391,6 +415,29 @@ int ap_train_backward(const double* grids, const double* targets, int32_t n_samp
     corr1_kernel<<<dim3(C1_CHUNKS, C1), 256, 0, st>>>(ws.ds1, grids, ws.part1, n_samples, H, W);
     corr1_finish_kernel<<<1, 192, 0, st>>>(ws.part1, C1_CHUNKS, grads);
     return launch_status("ap_train_backward");
+}
+
+int64_t ap_forward_f64_workspace_bytes(int32_t n_grids, int32_t H, int32_t W) {
+    if (n_grids < 1 || H < 1 || W < 1) return 0;
+    return (int64_t)align_up(sizeof(real) * (size_t)(C1 + C2) * n_grids * H * W);
+}
+
+int ap_predict_forward_f64(const double* grids, int32_t n_grids, int32_t H, int32_t W, const double* weights,
+                           double* out, int64_t out_stride, void* workspace, int64_t workspace_bytes, void* stream) {
+    AP_REQUIRE(n_grids >= 0 && H >= 1 && W >= 1, AP_EPARAM, "bad grid shape");
+    AP_REQUIRE(H <= 65535 && n_grids <= 65535 && out_stride >= W, AP_EPARAM, "bad sizes");
+    if (n_grids == 0) return AP_OK;
+    AP_REQUIRE(grids && weights && out && workspace, AP_EPARAM, "null pointer");
+    AP_REQUIRE(workspace_bytes >= ap_forward_f64_workspace_bytes(n_grids, H, W), AP_EPARAM, "workspace too small");
+    cudaStream_t st = as_stream(stream);
+    real* a1 = static_cast<real*>(workspace);
+    real* s2 = a1 + (int64_t)C1 * n_grids * H * W;
+    // the same conv kernels and head arithmetic as ap_train_backward, so `out` here equals the
+    // forward that backward differentiates bit for bit
+    launch_conv<1, C1, 2, true, 128>(grids, weights + OFF_W1, weights + OFF_B1, nullptr, a1, n_grids, H, W, st);
+    launch_conv<C1, C2, 1, false, 64>(a1, weights + OFF_W2, weights + OFF_B2, nullptr, s2, n_grids, H, W, st);
+    head_fwd_kernel<<<dim3((W + 31) / 32, n_grids), 256, 0, st>>>(s2, weights, out, out_stride, H, W);
+    return launch_status("ap_predict_forward_f64");
 }
 
 int ap_adam_step(double* weights, double* m, double* v, const double* grad_sum, int32_t n_params, double batch,

@@ -23,8 +23,9 @@ from . import _device as D
 from . import _lib
 from .attention import DecodeAttention, dense_splits, sparse_splits
 from .batched import BatchedSelector
+from .distributed import gather_heads_into
 from .errors import ConfigError
-from .predictor import PredictorWeights, init_weights, install_weights
+from .predictor import PredictorWeights, init_weights, install_weights, installed_digest, weights_digest
 
 
 @dataclass(frozen=True)
@@ -168,8 +169,13 @@ class DecodeEngine:
         self.sel = None
         from .selector import SelectorConfig
         self.cfg = cfg or SelectorConfig(budget=1024)
+        self.cfg.validate()
+        if self.cfg.block_size != 16:
+            raise ConfigError("the decode attention kernels use 16-token KV blocks: block_size must be 16")
+        self.pweights = weights or init_weights(0)
+        self._wdigest = weights_digest(self.pweights)
         if mode == "sparse":
-            install_weights(weights or init_weights(0))
+            install_weights(self.pweights)
             self.sel = BatchedSelector(self.cfg, S * self.sel_layers * self.maps_per_layer, self.t_max // 16,
                                        precision=precision, device=dev)
         self.voff = None
@@ -278,11 +284,7 @@ class DecodeEngine:
             self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=True, vpages=self.voff,
                             layer=l, **kw)
         if self.split is not None:  # one collective per layer: the heads' outputs over NVLink
-            import torch.distributed as dist
-            parts = torch.empty(self.split.world, S, sh.n_q_heads, 128, dtype=self.att_out.dtype,
-                                device=self.att_out.device)
-            dist.all_gather_into_tensor(parts, self.att_out.contiguous())
-            self.att_full.copy_(parts.permute(1, 0, 2, 3).reshape(S, -1, 128))
+            gather_heads_into(self.att_full, self.att_out, self.split)
         if self.fused:
             self._gemv(self.wo[l], self.att_full.view(S, -1), self.o, 0)
             self._gemv(self.wgu[l], self.o, self.act, GEMV_RMS | GEMV_SILU, residual=self.r, residual_out=self.r2,
@@ -357,8 +359,11 @@ class DecodeEngine:
 
     def step(self, use_graph: bool = True):
         """One decode token for every sequence."""
-        torch = D.torch()
         v = self.variant_for_next()
+        if self.sel is not None and installed_digest() != self._wdigest:
+            # another caller installed other forecaster weights (the library holds one set): put ours
+            # back; the generation bump makes every map recompute its r-map rows under them
+            install_weights(self.pweights)
         if use_graph and v != "first":
             g = self.graphs.get(v)
             if g is None:

@@ -87,6 +87,23 @@ def gather_heads(local_out, split: HeadSplit, group=None):
     return torch.cat(parts, dim=1)
 
 
+def gather_heads_into(out_full, local_out, split: HeadSplit, group=None):
+    """The engine's per-layer exchange (decode.py, KV-head split): every rank's [S, q_per_rank, D]
+    attention output -> ``out_full`` [S, n_q_heads, D] in head order.  One
+    ``all_gather_into_tensor`` (a single NCCL collective over NVLink, capturable in the step's CUDA
+    graph) into a rank-major buffer, then a head-major copy."""
+    import torch
+    import torch.distributed as dist
+    if split.world == 1:
+        out_full.copy_(local_out)
+        return out_full
+    S, hq, D = local_out.shape
+    parts = torch.empty(split.world * S, hq, D, dtype=local_out.dtype, device=local_out.device)  # rank-major
+    dist.all_gather_into_tensor(parts, local_out.contiguous(), group=group)
+    out_full.copy_(parts.view(split.world, S, hq, D).permute(1, 0, 2, 3).reshape(S, split.world * hq, D))
+    return out_full
+
+
 def max_over_ranks(x: float, device=None) -> float:
     """Max of a per-rank scalar (timing) over the default process group."""
     import torch

@@ -25,7 +25,7 @@ from .errors import FormatError, NumericError, ParameterError, TrainingError
 __all__ = [
     "CONV1_OUT", "CONV2_OUT", "KERNEL", "PARAM_COUNT", "WEIGHTS_MAGIC", "PredictorWeights", "init_weights",
     "AttentionHistory", "stack_history", "forward", "save_weights", "load_weights", "install_weights",
-    "default_precision", "TrainSample", "EpochMetrics", "backward", "train",
+    "default_precision", "forward_precision", "TrainSample", "EpochMetrics", "backward", "train",
     "build_dataset",
 ]
 
@@ -149,11 +149,22 @@ def stack_history(rows, depth: int, width: int) -> AttentionHistory:
 _installed = {"digest": None, "tensor": None}
 
 
+def weights_digest(weights: PredictorWeights) -> str:
+    """Identity of a weight set as the device sees it (its fp32 image)."""
+    return hashlib.sha1(weights.flat().astype(np.float32).tobytes()).hexdigest()
+
+
+def installed_digest() -> str | None:
+    return _installed["digest"]
+
+
 def install_weights(weights: PredictorWeights, stream=None):
     """Upload the weights as 4833 fp32 and install them (ap_set_weights) if they changed.
 
     Returns the device tensor.  The native library keeps one installed weight
     set, as the reference shares one forecaster across every (layer, head).
+    Installing a different set bumps the device weight generation, so every
+    selector map recomputes its forecaster rows in full at its next update.
     """
     weights.validate()
     flat32 = weights.flat().astype(np.float32)
@@ -165,12 +176,39 @@ def install_weights(weights: PredictorWeights, stream=None):
     return _installed["tensor"]
 
 
+def forward_precision() -> str:
+    """Arithmetic of the reference-compatible ``forward``: ATTNPRED_FORWARD_PRECISION in {fp64 (default:
+    the reference's own type, ap_predict_forward_f64), fp16x3, fp32, fp16 (the selector's kernels)}."""
+    p = os.environ.get("ATTNPRED_FORWARD_PRECISION", "fp64")
+    if p != "fp64" and p not in _lib.PREC:
+        raise ParameterError(f"unknown precision {p!r}")
+    return p
+
+
+def _forward_f64(weights: PredictorWeights, grid: np.ndarray) -> np.ndarray:
+    torch = D.torch()
+    H, W = grid.shape
+    g = D.to_device(np.ascontiguousarray(grid, dtype=np.float64))
+    w = D.to_device(weights.flat().astype(np.float64))
+    out = torch.empty(W, dtype=torch.float64, device=g.device)
+    ws = torch.empty(int(_lib.fn("ap_forward_f64_workspace_bytes")(1, H, W)), dtype=torch.uint8, device=g.device)
+    _lib.check(_lib.fn("ap_predict_forward_f64")(_lib.ptr(g), 1, H, W, _lib.ptr(w), _lib.ptr(out), W, _lib.ptr(ws),
+                                                 ws.numel(), _lib.stream_handle()), "forward")
+    return out.cpu().numpy()
+
+
 def forward(weights: PredictorWeights, history: AttentionHistory, precision: str | None = None) -> np.ndarray:
-    """predictor.py:211-216: predict the next compressed row (length = history width)."""
+    """predictor.py:211-216: predict the next compressed row (length = history width).
+
+    Default arithmetic is fp64 (``forward_precision``), like the reference; the selector's
+    tensor-core precisions (fp16x3 / fp32 / fp16) are available by name."""
     weights.validate()
     grid = np.asarray(history.grid, dtype=np.float64)
     if not np.all(np.isfinite(grid)):
         raise NumericError("history contains non-finite values")
+    precision = precision or forward_precision()
+    if precision == "fp64":
+        return _forward_f64(weights, grid)
     H, W = grid.shape
     torch = D.torch()
     install_weights(weights)
@@ -181,7 +219,7 @@ def forward(weights: PredictorWeights, history: AttentionHistory, precision: str
     out = torch.empty(W, dtype=torch.float32, device=g.device)
     scratch = torch.empty(H * pitch, dtype=torch.float32, device=g.device)
     status = D.new_status()
-    prec = _lib.PREC[precision or default_precision()]
+    prec = _lib.PREC[precision]
     _lib.check(_lib.fn("ap_predict_forward")(_lib.ptr(g), 1, H, W, pitch, H * pitch, _lib.ptr(out), W,
                                              _lib.ptr(scratch), prec, _lib.ptr(status), _lib.stream_handle()),
                "forward")
@@ -319,29 +357,24 @@ def _block_recovery_accuracy(preds, targets) -> float:
 
 
 def _forward_many(w_flat: np.ndarray, grids) -> list[np.ndarray]:
-    """fp32 ap_predict_forward of many histories, one launch per (H, W) group."""
+    """fp64 ap_predict_forward_f64 of many histories (the reference's arithmetic), one launch per
+    (H, W) group."""
     torch = D.torch()
-    install_weights(PredictorWeights.from_flat(w_flat))
     out = [None] * len(grids)
     groups = {}
     for i, g in enumerate(grids):
         groups.setdefault(np.asarray(g).shape, []).append(i)
-    status = D.new_status()
+    w = D.to_device(np.asarray(w_flat, np.float64))
     for (H, W), ids in groups.items():
-        pitch = -(-W // 4) * 4
-        buf = np.zeros((len(ids), H, pitch), np.float32)
-        for j, i in enumerate(ids):
-            buf[j, :, :W] = grids[i]
-        g = D.to_device(buf)
-        o = torch.empty((len(ids), W), dtype=torch.float32, device=g.device)
-        scratch = torch.empty_like(g)
-        _lib.check(_lib.fn("ap_predict_forward")(_lib.ptr(g), len(ids), H, W, pitch, H * pitch, _lib.ptr(o), W,
-                                                 _lib.ptr(scratch), _lib.PREC["fp32"], _lib.ptr(status),
-                                                 _lib.stream_handle()), "forward")
-        o = o.cpu().numpy().astype(np.float64)
+        g = D.to_device(np.stack([np.asarray(grids[i], np.float64) for i in ids]))
+        o = torch.empty((len(ids), W), dtype=torch.float64, device=g.device)
+        ws = torch.empty(int(_lib.fn("ap_forward_f64_workspace_bytes")(len(ids), H, W)), dtype=torch.uint8,
+                         device=g.device)
+        _lib.check(_lib.fn("ap_predict_forward_f64")(_lib.ptr(g), len(ids), H, W, _lib.ptr(w), _lib.ptr(o), W,
+                                                     _lib.ptr(ws), ws.numel(), _lib.stream_handle()), "forward")
+        o = o.cpu().numpy()
         for j, i in enumerate(ids):
             out[i] = o[j]
-    D.sync_and_check(status, "forward")
     return out
 
 

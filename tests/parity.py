@@ -8,8 +8,8 @@ import numpy as np
 #   |x - y| <= rtol * max(|y|, floor * max|y_row|)
 # fp32-class modes (SIMT fp32, fp16x3 tensor cores): rtol 1e-3, floor 1e-2;
 # the single-MMA fp16 mode: rtol 2e-2 (the north_star's bf16 bound), floor 1e-1.
-RTOL = {"fp32": 1e-3, "fp16x3": 1e-3, "fp16": 2e-2}
-FLOOR = {"fp32": 1e-2, "fp16x3": 1e-2, "fp16": 1e-1}
+RTOL = {"fp64": 1e-12, "fp32": 1e-3, "fp16x3": 1e-3, "fp16": 2e-2}
+FLOOR = {"fp64": 1e-2, "fp32": 1e-2, "fp16x3": 1e-2, "fp16": 1e-1}
 
 
 def scores_close(got, want, precision: str) -> tuple[bool, float]:

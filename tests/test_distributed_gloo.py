@@ -3,8 +3,9 @@
 * sequence sharding covers every sequence exactly once;
 * KV-head split: each rank computes decode attention for its KV heads (the
   float64 oracle math stands in for the CUDA kernel, which is tested on the
-  GPU), the outputs are all-gathered, and the result equals the unsplit
-  computation; the fused-QKV row slice selects exactly the rank's heads;
+  GPU), the outputs are all-gathered — by ``gather_heads`` and by the engine's
+  own ``gather_heads_into`` (all_gather_into_tensor + head-major permute) — and
+  the result equals the unsplit computation; the fused-QKV row slice selects exactly the rank's heads;
 * max-over-ranks timing takes the slowest rank.
 """
 
@@ -32,7 +33,8 @@ def _worker(rank, world, port, q, ret):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2502_04077_b200.distributed import HeadSplit, gather_heads, max_over_ranks, seq_shard
+        from paper_2502_04077_b200.distributed import (HeadSplit, gather_heads, gather_heads_into, max_over_ranks,
+                                                       seq_shard)
         rng = np.random.default_rng(0)  # same data on every rank
         S, Hq, Hkv, D, t = 2, 8, 4, 16, 50
         qv = rng.standard_normal((S, Hq, D))
@@ -49,6 +51,9 @@ def _worker(rank, world, port, q, ret):
         want = np.stack([[A.dense_decode(qv[s, h], K[s, h // G], V[s, h // G])[0] for h in range(Hq)]
                          for s in range(S)])
         ok_heads = bool(np.allclose(full, want))
+        # the decode engine's exchange (DecodeEngine._layer, KV-head split): all_gather_into_tensor + permute
+        eng_full = gather_heads_into(torch.empty(S, Hq, D, dtype=torch.float64), torch.from_numpy(local), split)
+        ok_heads = ok_heads and bool(np.allclose(eng_full.numpy(), want))
         rows = split.qkv_rows(D)
         ok_rows = len(rows) == (split.q_per_rank + 2 * split.kv_per_rank) * D and rows[0] == rank * split.q_per_rank * D
         starts = [seq_shard(7, r, world) for r in range(world)]
