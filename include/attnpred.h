@@ -185,7 +185,7 @@ int64_t ap_sel_tie_ws_bytes(int32_t n_maps);
 /* [host] cumulative guard counters of a workspace: [maps over capacity, maps re-scored,
  * candidates re-scored].  Synchronous copy. */
 int ap_sel_tie_stats(const int32_t* tie_ws, int32_t* host_out3);
-/* [host] guard switch and band (defaults: on, rel 2^-13, floor 2^-6; env ATTNPRED_TIE_GUARD /
+/* [host] guard switch and band (defaults: on, rel 2^-15, floor 2^-5; env ATTNPRED_TIE_GUARD /
  * ATTNPRED_TIE_REL / ATTNPRED_TIE_FLOOR).  Applies to later ap_sel_step calls (graphs keep the
  * values they were captured with). */
 int ap_sel_set_tie_guard(int enabled, float rel, float floor_frac);

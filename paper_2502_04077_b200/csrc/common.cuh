@@ -162,7 +162,7 @@ namespace tie {
 struct Params {
     int enabled;
     float rel, floor;   // band = rel * max(|tau|, floor * max|score|) around the k-th score tau
-    const float* w;     // the installed 4833 fp32 weights (c_w)
+    const double* w64;  // fp64 image of the installed weights (g_w64; w2 transposed to [k*9+tap][c])
     const int* wgen;    // the installed weight generation (g_wgen)
 };
 }  // namespace tie

@@ -45,6 +45,7 @@ __device__ __align__(16) uint4 g_bpack[2 * 9 * BTILE_BYTES / 16];
 constexpr int B96_BYTES = 96 * 16 * 2;
 __device__ __align__(16) uint4 g_bpack96[2 * 3 * B96_BYTES / 16];
 __device__ int g_wexp;            // power-of-2 exponent applied to w2
+__device__ double g_w64[AP_PARAM_COUNT];  // fp64 image for the exact-boundary guard (tieguard.cuh layout)
 __device__ int g_wgen;            // weight generation: bumped by every ap_set_weights; a map whose r-map was
                                   // built under another generation is recomputed in full (plan_task)
 __device__ float g_w1abs[16];     // sum_t |w1[c][t]|  (a1 magnitude bound)
@@ -102,6 +103,11 @@ __global__ void pack_weights_kernel() {
         }
         g_w1abs[0] = wm;
         g_b1abs[0] = bm;
+    }
+    for (int i = threadIdx.x; i < AP_PARAM_COUNT; i += blockDim.x) {  // w2 transposed to [k*9+tap][c]
+        const bool w2 = i >= OFF_W2 && i < OFF_B2;
+        const int dst = w2 ? OFF_W2 + ((i - OFF_W2) % 144) * 32 + (i - OFF_W2) / 144 : i;
+        g_w64[dst] = (double)c_w[i];
     }
     __half* base = reinterpret_cast<__half*>(g_bpack);
     for (int idx = threadIdx.x; idx < 9 * 32 * 16; idx += blockDim.x) {
@@ -753,17 +759,17 @@ static void tie_init() {
     g_tie_on = !(e && strcmp(e, "0") == 0);
     const char* r = getenv("ATTNPRED_TIE_REL");
     const char* f = getenv("ATTNPRED_TIE_FLOOR");
-    g_tie_rel = r ? (float)atof(r) : 1.220703125e-4f;  // 2^-13
-    g_tie_floor = f ? (float)atof(f) : 1.5625e-2f;     // 2^-6
+    g_tie_rel = r ? (float)atof(r) : 3.0517578125e-5f;  // 2^-15
+    g_tie_floor = f ? (float)atof(f) : 3.125e-2f;       // 2^-5
 }
 
 static tie::Params tie_params(int precision) {
-    static const float* w = nullptr;
+    static const double* w = nullptr;
     static const int* gen = nullptr;
     tie_init();
     if (!w) {
         void* p = nullptr;
-        if (cudaGetSymbolAddress(&p, c_w) == cudaSuccess) w = static_cast<const float*>(p);
+        if (cudaGetSymbolAddress(&p, g_w64) == cudaSuccess) w = static_cast<const double*>(p);
         if (cudaGetSymbolAddress(&p, g_wgen) == cudaSuccess) gen = static_cast<const int*>(p);
     }
     const int env_on = g_tie_on;
@@ -772,7 +778,7 @@ static tie::Params tie_params(int precision) {
     tp.enabled = env_on && precision != AP_PREC_F16 && w != nullptr;
     tp.rel = rel;
     tp.floor = flo;
-    tp.w = w;
+    tp.w64 = w;
     tp.wgen = gen;
     return tp;
 }

@@ -11,24 +11,34 @@
 //   B = the band.  If |B| > k - |A| the boundary is ambiguous: every block of B is re-scored in
 //   fp64 from the history window (the reference's arithmetic, summed in a fixed order) and the
 //   k - |A| best by (fp64 score desc, index asc) — selector.py:80's lexsort order — are taken.
-// Detection runs inside the top-k kernel; the re-scoring is one persistent launch over
-// (map, candidate) units, and the last unit of a map re-emits that map's block ids.
+// Detection runs inside the top-k kernel.  Re-scoring is one persistent launch over units of
+// (map, candidate, group of history rows): a candidate's 16 row groups run on different CTAs, the
+// last group of a candidate sums the partials in a fixed order, and the last candidate of a map
+// re-emits that map's block ids.
 #pragma once
 
 namespace ap {
 namespace tie {
 
 constexpr int CAP = 64;      // candidates per map; wider ambiguity falls back to the fp32 order (counted)
+constexpr int NG = 16;       // history-row groups per candidate (units)
+constexpr int MAX_RG = 8;    // rows per group: the guard covers H <= NG * MAX_RG = 128
 constexpr int HDR = 16;      // workspace header words
 constexpr int REC_HDR = 16;  // per-map record header words
-constexpr int REC = REC_HDR + 3 * CAP;  // + ids[CAP] int32 + scores[CAP] fp64
-constexpr int NT = 256;
+// record: header | ids[CAP] | cpend[CAP] | scores[CAP] fp64 | parts[CAP][NG] fp64
+constexpr int OFF_IDS = REC_HDR, OFF_CPEND = OFF_IDS + CAP, OFF_SC = OFF_CPEND + CAP, OFF_PARTS = OFF_SC + 2 * CAP;
+constexpr int REC = OFF_PARTS + 2 * CAP * NG;
+constexpr int NT = 128;      // refine CTA: 4 warps, lane = conv2 output channel
 
 enum { H_UNITS = 0, H_NEXT = 1, H_DONE = 2, H_OVERFLOW = 3, H_MAPS = 4, H_CANDS = 5 };
 enum { R_NA = 0, R_NEED, R_NB, R_KLO, R_KHI, R_PENDING, R_W, R_SINK_HI, R_LOCAL_LO, R_LOCAL_HI };
 
-__host__ __device__ inline int64_t rec_off(int n_maps) { return (HDR + (int64_t)n_maps * CAP + 1) & ~int64_t(1); }
+__host__ __device__ inline int64_t units_cap(int n_maps) { return (int64_t)n_maps * CAP * NG; }
+__host__ __device__ inline int64_t rec_off(int n_maps) { return (HDR + units_cap(n_maps) + 1) & ~int64_t(1); }
 __host__ __device__ inline int64_t ws_words(int n_maps) { return rec_off(n_maps) + (int64_t)n_maps * REC; }
+
+// fp64 weight image (g_w64, written by ap_set_weights): w1[144] b1[16] w2t[144][32] b2[32] w3[32] b3
+constexpr int W64_W1 = 0, W64_B1 = 144, W64_W2T = 160, W64_B2 = 4768, W64_W3 = 4800, W64_B3 = 4832;
 
 __device__ __forceinline__ float key_value(uint32_t k) {
     return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
@@ -55,15 +65,16 @@ __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn
     const int need = k - NA;
     if (NB <= need) return 0;
     int* ws = s.tie_ws;
-    if (NB > CAP) {
+    if (NB > CAP || s.history > NG * MAX_RG) {
         if (threadIdx.x == 0) atomicAdd(&ws[H_OVERFLOW], 1);
         return -NB;
     }
     int* rec = ws + rec_off(s.n_maps) + (int64_t)m * REC;
     for (int i = lo; i < hi; ++i) {
         const uint32_t key = keyfn(i);
-        if (key >= klo && key <= khi) rec[REC_HDR + pos++] = i;  // ascending block ids
+        if (key >= klo && key <= khi) rec[OFF_IDS + pos++] = i;  // ascending block ids
     }
+    for (int j = threadIdx.x; j < NB; j += NTH) rec[OFF_CPEND + j] = NG;
     if (threadIdx.x == 0) {
         rec[R_NA] = NA;
         rec[R_NEED] = need;
@@ -75,102 +86,78 @@ __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn
         rec[R_SINK_HI] = sink_hi;
         rec[R_LOCAL_LO] = local_lo;
         rec[R_LOCAL_HI] = local_hi;
-        *s_bcast = atomicAdd(&ws[H_UNITS], NB);
+        *s_bcast = atomicAdd(&ws[H_UNITS], NB * NG);
         atomicAdd(&ws[H_MAPS], 1);
         atomicAdd(&ws[H_CANDS], NB);
     }
     __syncthreads();
     const int ub = *s_bcast;
-    for (int j = threadIdx.x; j < NB; j += NTH) ws[HDR + ub + j] = m * CAP + j;
+    for (int u = threadIdx.x; u < NB * NG; u += NTH) ws[HDR + ub + u] = (m * CAP + u / NG) * NG + u % NG;
     return NB;
 }
 
 // ------------------------------------------------------------------ fp64 re-scoring
-// Shared memory (doubles): weights (w2 transposed to [k*9+tap][c]), the x window, the a1 window.
-constexpr int SW1 = 0, SB1 = 144, SW2 = 160, SB2 = SW2 + 144 * 32, SW3 = SB2 + 32, SB3 = SW3 + 32;
-constexpr int SX = SB3 + 8;                 // x window [68 rows][5 cols]
-constexpr int A1S = 49;                     // a1 row stride (48 + 1: conflict-free interleaved rows)
-constexpr int SA1 = SX + 68 * 5;            // a1 window [66 rows][A1S]
-constexpr int SRED = SA1 + 66 * A1S;        // [NT/32] warp partials
-constexpr int SMEM_DOUBLES = SRED + NT / 32 + 8;
-constexpr int SMEM_BYTES = SMEM_DOUBLES * 8;
-
-// score of block column `col` of map m: b3 + (1/H) sum_i sum_c w3[c] relu(s2[c][i][col]) in fp64,
-// every product and sum in a fixed order (deterministic).  All threads.
-__device__ double exact_score(const ap_selector& s, int m, int col, double* sm) {
+// sum over history rows [g*RG, g*RG+RG) of r_i = sum_c w3[c] relu(s2[c][i][col]), in fp64, fixed order.
+// x window [RG+4 rows][5 cols], a1 window [RG+2 rows][16 ch][3 cols] in shared memory; warp w takes
+// rows w, w+4, ..., lane = output channel c (conv2 = a 144-term dot per lane, weights w2t[kt][c]
+// coalesced across lanes, a1 values broadcast).  All threads.
+__device__ double group_partial(const ap_selector& s, const double* __restrict__ w64, int m, int col, int g,
+                                double* sx, double* sa1, double* srow) {
     const ap_map_state st = s.state[m];
     const int H = s.history, W = st.width, pitch = s.w_max;
+    const int RG = (H + NG - 1) / NG;
+    const int r0 = g * RG, nr = max(0, min(H, r0 + RG) - r0);
+    if (nr == 0) return 0.0;
     const float* ring = s.ring + (int64_t)m * H * pitch;
     const int64_t n_pushed = st.n_pushed;
     const int first_real = n_pushed >= H ? 0 : (int)(H - n_pushed);
-    const int tid = threadIdx.x, cp = tid >> 4, rg = tid & 15;
-    double* sx = sm + SX;
-    double* sa1 = sm + SA1;
-    double acc = 0.0;
-    for (int i0 = 0; i0 < H; i0 += 64) {
-        const int nrows = min(64, H - i0);
-        __syncthreads();
-        for (int idx = tid; idx < (nrows + 4) * 5; idx += NT) {
-            const int q = idx / 5, c = idx % 5, p = i0 - 2 + q, cc = col - 2 + c;
-            double v = 0.0;
-            if (p >= first_real && p < H && p >= 0 && cc >= 0 && cc < W) {
-                int64_t r = (n_pushed - H + p) % H;
-                if (r < 0) r += H;
-                v = (double)ring[r * pitch + cc];
-            }
-            sx[idx] = v;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int idx = tid; idx < (nr + 4) * 5; idx += NT) {  // x rows r0-2 .. r0+nr+1, cols col-2 .. col+2
+        const int q = idx / 5, c = idx % 5, p = r0 - 2 + q, cc = col - 2 + c;
+        double v = 0.0;
+        if (p >= first_real && p < H && p >= 0 && cc >= 0 && cc < W) {
+            int64_t r = (n_pushed - H + p) % H;
+            if (r < 0) r += H;
+            v = (double)ring[r * pitch + cc];
         }
-        __syncthreads();
-        for (int idx = tid; idx < (nrows + 2) * 48; idx += NT) {
-            const int r = idx / 48, kd = idx % 48, kk = kd / 3, dj = kd % 3;
-            const int p = i0 - 1 + r, c2 = col - 1 + dj;
-            double a = 0.0;
-            if (p >= 0 && p < H && c2 >= 0 && c2 < W) {  // conv2's zero padding of a1
-                a = sm[SB1 + kk];
+        sx[idx] = v;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (nr + 2) * 48; idx += NT) {  // a1 rows r0-1 .. r0+nr, cols col-1 .. col+1
+        const int r = idx / 48, kd = idx % 48, kk = kd / 3, dj = kd % 3;
+        const int p = r0 - 1 + r, c2 = col - 1 + dj;
+        double a = 0.0;
+        if (p >= 0 && p < H && c2 >= 0 && c2 < W) {  // conv2's zero padding of a1
+            double e = w64[W64_B1 + kk], o = 0.0;
 #pragma unroll
-                for (int t = 0; t < 9; ++t) a = fma(sm[SW1 + kk * 9 + t], sx[(r + t / 3) * 5 + dj + t % 3], a);
-                a = fmax(a, 0.0);
-            }
-            sa1[r * A1S + kd] = a;
-        }
-        __syncthreads();
-        double s0[4], s1[4];
+            for (int t = 0; t < 9; t += 2) e = fma(w64[W64_W1 + kk * 9 + t], sx[(r + t / 3) * 5 + dj + t % 3], e);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            s0[j] = sm[SB2 + 2 * cp];
-            s1[j] = sm[SB2 + 2 * cp + 1];
+            for (int t = 1; t < 9; t += 2) o = fma(w64[W64_W1 + kk * 9 + t], sx[(r + t / 3) * 5 + dj + t % 3], o);
+            a = fmax(e + o, 0.0);
         }
-#pragma unroll 1
-        for (int kk = 0; kk < 16; ++kk) {
+        sa1[r * 48 + kd] = a;
+    }
+    __syncthreads();
+    for (int ri = warp; ri < nr; ri += NT / 32) {
+        double e = w64[W64_B2 + lane], o = 0.0;  // two chains: even / odd input channels
+#pragma unroll 4
+        for (int kk = 0; kk < 16; kk += 2) {
 #pragma unroll
             for (int t = 0; t < 9; ++t) {
                 const int di = t / 3, dj = t % 3;
-                const double2 w = *reinterpret_cast<const double2*>(&sm[SW2 + (kk * 9 + t) * 32 + 2 * cp]);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const double av = sa1[(rg + 16 * j + di) * A1S + kk * 3 + dj];
-                    s0[j] = fma(w.x, av, s0[j]);
-                    s1[j] = fma(w.y, av, s1[j]);
-                }
+                e = fma(w64[W64_W2T + (kk * 9 + t) * 32 + lane], sa1[(ri + di) * 48 + kk * 3 + dj], e);
+                o = fma(w64[W64_W2T + ((kk + 1) * 9 + t) * 32 + lane], sa1[(ri + di) * 48 + (kk + 1) * 3 + dj], o);
             }
         }
+        double r = w64[W64_W3 + lane] * fmax(e + o, 0.0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (rg + 16 * j < nrows) {
-                acc = fma(sm[SW3 + 2 * cp], fmax(s0[j], 0.0), acc);
-                acc = fma(sm[SW3 + 2 * cp + 1], fmax(s1[j], 0.0), acc);
-            }
-        }
+        for (int off = 16; off; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+        if (lane == 0) srow[ri] = r;
     }
-    // fixed-order block reduction
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    __syncthreads();
-    if ((tid & 31) == 0) sm[SRED + (tid >> 5)] = acc;
     __syncthreads();
     double tot = 0.0;
-    for (int w = 0; w < NT / 32; ++w) tot += sm[SRED + w];
-    return sm[SB3] + tot / H;
+    for (int ri = 0; ri < nr; ++ri) tot += srow[ri];  // fixed order
+    return tot;
 }
 
 // Re-emit map m's middle blocks: A plus the `need` best re-scored candidates, ascending.
@@ -180,10 +167,10 @@ __device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/,
     const uint32_t klo = (uint32_t)__ldcg(rec + R_KLO), khi = (uint32_t)__ldcg(rec + R_KHI);
     const int sink_hi = __ldcg(rec + R_SINK_HI), local_lo = __ldcg(rec + R_LOCAL_LO),
               local_hi = __ldcg(rec + R_LOCAL_HI);
-    const int* ids = rec + REC_HDR;
-    const double* sc = reinterpret_cast<const double*>(rec + REC_HDR + CAP);
-    if ((int)threadIdx.x < NB) {
-        const int j = threadIdx.x, id = __ldcg(ids + j);
+    const int* ids = rec + OFF_IDS;
+    const double* sc = reinterpret_cast<const double*>(rec + OFF_SC);
+    for (int j = threadIdx.x; j < NB; j += NT) {
+        const int id = __ldcg(ids + j);
         const double v = __ldcg(sc + j);
         int rank = 0;
         for (int l = 0; l < NB; ++l) {
@@ -227,41 +214,38 @@ __device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/,
 }
 
 __global__ void __launch_bounds__(NT) refine_kernel(ap_selector s, Params tp) {
-    extern __shared__ double sm[];
+    __shared__ double sx[(MAX_RG + 4) * 5];
+    __shared__ double sa1[(MAX_RG + 2) * 48];
+    __shared__ double srow[MAX_RG];
     __shared__ int s_unit, s_last;
     __shared__ int flags[CAP];
     __shared__ int scan_tmp[NT / 32 + 2];
     int* ws = s.tie_ws;
-    bool staged = false;
+    const double* w64 = tp.w64;
     for (;;) {
         if (threadIdx.x == 0) s_unit = atomicAdd(&ws[H_NEXT], 1);
         __syncthreads();
         const int u = s_unit;
         if (u >= __ldcg(&ws[H_UNITS])) break;
-        if (!staged) {  // weights as fp64 (exact: they are fp32 values); w2 as [k*9+tap][c]
-            for (int i = threadIdx.x; i < 144; i += NT) sm[SW1 + i] = (double)tp.w[i];
-            for (int i = threadIdx.x; i < 16; i += NT) sm[SB1 + i] = (double)tp.w[144 + i];
-            for (int i = threadIdx.x; i < 4608; i += NT) {
-                const int c = i / 144, kt = i % 144;
-                sm[SW2 + kt * 32 + c] = (double)tp.w[160 + i];
-            }
-            for (int i = threadIdx.x; i < 32; i += NT) {
-                sm[SB2 + i] = (double)tp.w[4768 + i];
-                sm[SW3 + i] = (double)tp.w[4800 + i];
-            }
-            if (threadIdx.x == 0) sm[SB3] = (double)tp.w[4832];
-            staged = true;
-            __syncthreads();
-        }
-        const int m = u / CAP, j = u % CAP;
+        const int unit = __ldcg(&ws[HDR + u]);  // (map * CAP + candidate) * NG + group
+        const int g = unit % NG, j = (unit / NG) % CAP, m = unit / (NG * CAP);
         int* rec = ws + rec_off(s.n_maps) + (int64_t)m * REC;
-        const int col = __ldcg(rec + REC_HDR + j);
-        const double v = exact_score(s, m, col, sm);
+        const int col = __ldcg(rec + OFF_IDS + j);
+        const double part = group_partial(s, w64, m, col, g, sx, sa1, srow);
         if (threadIdx.x == 0) {
-            reinterpret_cast<double*>(rec + REC_HDR + CAP)[j] = v;
+            double* parts = reinterpret_cast<double*>(rec + OFF_PARTS) + j * NG;
+            parts[g] = part;
             __threadfence();
-            s_last = atomicSub(rec + R_PENDING, 1) == 1;
-            if (s_last) __threadfence();
+            s_last = 0;
+            if (atomicSub(rec + OFF_CPEND + j, 1) == 1) {  // last group of this candidate
+                __threadfence();
+                double tot = 0.0;
+                for (int q = 0; q < NG; ++q) tot += __ldcg(parts + q);  // fixed order
+                reinterpret_cast<double*>(rec + OFF_SC)[j] = w64[W64_B3] + tot / s.history;
+                __threadfence();
+                s_last = atomicSub(rec + R_PENDING, 1) == 1;  // last candidate of this map
+                if (s_last) __threadfence();
+            }
         }
         __syncthreads();
         if (s_last) finalize(s, m, flags, scan_tmp);

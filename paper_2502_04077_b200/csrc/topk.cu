@@ -370,11 +370,8 @@ void launch_sel_topk(const ap_selector& s, const tie::Params& tp, cudaStream_t s
     else sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s, tp);
     if (tp.enabled && s.tie_ws) {
         static int grid = 0;
-        if (!grid) {
-            cudaFuncSetAttribute(tie::refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tie::SMEM_BYTES);
-            grid = 2 * ap_device_sm_count();
-        }
-        tie::refine_kernel<<<grid, tie::NT, tie::SMEM_BYTES, stream>>>(s, tp);
+        if (!grid) grid = 4 * ap_device_sm_count();
+        tie::refine_kernel<<<grid, tie::NT, 0, stream>>>(s, tp);
     }
 }
 
