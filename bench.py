@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["decode", "cfg1"], default="decode",
+                    help="decode: configs[1] (32K LLaMA-3.1-8B decode, the headline); cfg1: configs[0] "
+                         "(32 heads x 4K x 64 steps of synthetic history maps -> predict + top-k us/layer)")
     ap.add_argument("--model", default="llama-3.1-8b")
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--budget", type=int, default=1024)
@@ -357,32 +360,30 @@ def measure_e2e(eng, n, batch, world, units=None):
 
 
 def measure_selector(eng, reps=20):
-    """Median CUDA-event time of the fused forecast + top-k launch (ap_sel_step) in its steady-state
-    form — one new row per map since the last update (incremental), width unchanged.  The decode
-    state is snapshotted and restored around the measurement."""
+    """Median CUDA-event time of the fused forecast + top-k (+ guard) launches (ap_sel_step) in their
+    steady state on the engine's REAL data: one eager decode step without its selector call (the
+    attention kernels emit this token's rows into every ring), then ap_sel_step timed `reps` times,
+    each from the same saved selector state (r-map rows, running sums, state, selection).  The decode
+    state is restored afterwards."""
     import torch
+    sel = eng.sel
     snap = eng._snapshot()
-    ring, rmap, rsum = eng.sel.ring.clone(), eng.sel.rmap.clone(), eng.sel.rsum.clone()
-    st = eng.sel.states()
-    t_now = int(st["row_len"].max())
-    comp = torch.rand(eng.sel.n_maps, eng.sel.w_max, device="cuda") ** 8
+    eng._step_body(eng.variant_for_next(), selector=False)
+    torch.cuda.synchronize()
+    keep = [t.clone() for t in (sel.state, sel.rmap, sel.rsum, sel.mid_blocks, sel.mid_mask)]
+    W = int(sel.states()["width"].max())
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for i in range(reps):
-        eng._restore(snap)
-        eng.sel.ring.copy_(ring)
-        eng.sel.rmap.copy_(rmap)
-        eng.sel.rsum.copy_(rsum)
-        eng.sel.push_compressed(comp, t_now)
+        for dst, src in zip((sel.state, sel.rmap, sel.rsum, sel.mid_blocks, sel.mid_mask), keep):
+            dst.copy_(src)
         ev[i][0].record()
-        eng.sel.step()
+        sel.step()
         ev[i][1].record()
     torch.cuda.synchronize()
     us = statistics.median(a.elapsed_time(b) * 1e3 for a, b in ev)
+    for dst, src in zip((sel.state, sel.rmap, sel.rsum, sel.mid_blocks, sel.mid_mask), keep):
+        dst.copy_(src)
     eng._restore(snap)
-    eng.sel.ring.copy_(ring)
-    eng.sel.rmap.copy_(rmap)
-    eng.sel.rsum.copy_(rsum)
-    W = int(st["width"].max())
     return us, W
 
 
@@ -589,6 +590,137 @@ def run_ours(args, rank, world):
         print(json.dumps(out), flush=True)
 
 
+# ---------------------------------------------------------------- cfg1: the selector alone
+def clustered_runs(rng, n_runs, run_len, lo, hi):
+    """The reference test helper that places re-access runs (pkg/tests/conftest.py:21-26), restated."""
+    import numpy as np
+    starts = rng.choice(np.arange(lo, hi - run_len), n_runs, replace=False)
+    return frozenset(int(p) for st in starts for p in range(int(st), int(st) + run_len))
+
+
+def cfg1_rows(seed=0, heads=32, prefill=4032, decode=64):
+    """BASELINE configs[0] maps: the reference's own generator (attncast.synth.gen_trace, synth.py:256-362)
+    with SURVEY §8(d)'s cfg1 settings, from baseline/_ref; Dirichlet(0.05) rows if it is not installed.
+    Returns ({step: float32 [heads, row_len(step)]} for steps -63..decode, source)."""
+    import numpy as np
+    ref = _reference_modules()
+    rng = np.random.default_rng(seed)
+    if ref is not None:
+        from attncast.synth import SynthConfig, gen_trace
+        sc = SynthConfig(head_dim=64, prefill_len=prefill, decode_steps=decode, query_drift=0.15, key_drift=0.15,
+                         seasonal_period=5, reaccess_positions=clustered_runs(rng, 4, 12, 100, 3900),
+                         rng_seed=seed, num_heads=heads)
+        tr = gen_trace(sc, keep_prefill_rows=64)
+        rows = {st: np.stack([np.asarray(tr.row(0, h, st), np.float32) for h in range(heads)])
+                for st in tr.header.steps}
+        return rows, "attncast.synth.gen_trace (reference, baseline/_ref)"
+    rows = {st: rng.dirichlet(np.full(prefill + st, 0.05), size=heads).astype(np.float32)
+            for st in range(-63, decode + 1)}
+    return rows, "Dirichlet(0.05) rows (reference generator not installed)"
+
+
+def run_cfg1(args, rank, world):
+    """configs[0]: predict + top-k us/layer.  One launch pair (push of the step's attention rows =
+    compress + ring append, then forecast + top-k + exact-boundary guard) covers 32 layers x 32 heads
+    = 1024 maps (the 32-head gen_trace maps replicated over 32 layers; a 32-map launch
+    is below launch latency).  Also: every step of 8 heads re-checked against the CPU oracle, and the
+    reference's prediction accuracy (evaluation.py:155-191) of the device's selections."""
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+    from oracle import hotpath as O
+    from paper_2502_04077_b200 import predictor
+    from paper_2502_04077_b200.batched import PUSH_DENSE, PUSH_PREFILL, BatchedSelector
+    from paper_2502_04077_b200.selector import SelectorConfig
+    heads, layers, decode = 32, 32, 64
+    rows, source = cfg1_rows(seed=0, heads=heads, decode=decode)
+    cfg = SelectorConfig(budget=args.budget)
+    ocfg = O.Config(budget=args.budget)
+    w = O.Weights.from_flat(O.init_weights(0).flat().astype(np.float32).astype(np.float64))  # APW1 image
+    predictor.install_weights(predictor.PredictorWeights.from_flat(w.flat()))
+    n_maps = heads * layers
+    t_last = max(r.shape[1] for r in rows.values())
+    sel = BatchedSelector(cfg, n_maps, w_max=-(-t_last // 16), precision=args.precision)
+    dev_rows = {st: torch.from_numpy(np.tile(r, (layers, 1))).cuda() for st, r in rows.items()}
+    for st in range(-63, 0):
+        sel.push_rows(dev_rows[st], dev_rows[st].shape[1], mode=PUSH_PREFILL)
+    K = cfg.middle_blocks
+    mids = torch.zeros(decode, n_maps, K, dtype=torch.int32, device="cuda")
+    nmid = torch.zeros(decode, n_maps, dtype=torch.int32, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(decode)]
+    st_view = sel.state.view(torch.int32).view(n_maps, -1)
+    from paper_2502_04077_b200 import _lib
+    n_mid_col = _lib.MapState.n_mid.offset // 4  # int32 index of ap_map_state.n_mid
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for s in range(decode):
+            r = dev_rows[s]
+            ev[s][0].record()
+            sel.push_rows(r, r.shape[1], mode=PUSH_DENSE)
+            sel.step()
+            ev[s][1].record()
+            mids[s].copy_(sel.mid_blocks[:, :K])
+            nmid[s].copy_(st_view[:, n_mid_col])
+        torch.cuda.synchronize()
+    sel.check_status()
+    us = [a.elapsed_time(b) * 1e3 for a, b in ev]
+    steady = us[args.warmup:] if decode > args.warmup + 3 else us
+    us_med = statistics.median(steady)
+    mids, nmid = mids.cpu().numpy(), nmid.cpu().numpy()
+    # parity: 8 heads (layer 0) through the oracle's evaluation loop, every step
+    mism, checked = 0, 0
+    for h in range(8):
+        ost = O.init_state(ocfg, [rows[st][h] for st in range(-63, 0)])
+        osel = None
+        for s in range(decode):
+            row = rows[s][h].astype(np.float64)
+            obs = row if osel is None else O.observed_from_selection(row, osel)
+            ost, osel = O.step(ost, ocfg, w, obs, full_row=row)
+            mism += mids[s, h, : nmid[s, h]].tolist() != ost.last_blocks
+            checked += 1
+    # accuracy of the device's selections, evaluation.py:155-191 (start_step 0), layer 0's 32 heads
+    ratios = []
+    for h in range(heads):
+        for s in range(decode):
+            t = rows[s].shape[1]
+            sel_tok = set(range(min(cfg.sink_tokens, t + 1))) | set(range(max(0, t + 1 - cfg.local_tokens), t + 1))
+            sel_tok |= O.expand_indices(mids[s, h, : nmid[s, h]].tolist(), 16, t)
+            nxt = rows[s + 1][h].astype(np.float64)
+            got = O.recovery_rate(nxt, sel_tok)
+            best = O.recovery_rate(nxt, O.topk(nxt, min(cfg.budget, nxt.size)))
+            ratios.append(got / best if best > 0 else 1.0)
+    H, W = cfg.history, -(-t_last // 16)
+    b_alg = n_maps * (t_last * 4 + (H + 1) * W * 4 + 4 * K)
+    peak, peak_kind = measured_peak()
+    achieved = b_alg / (us_med * 1e-6) / 1e9
+    cpu = None
+    if args.cpu_sample:
+        R = measure_reference(4096, args.budget, 1, args.cpu_sample)
+        rate = max(R["rate_par"], R["rate_all"])
+        cpu = {"value": round(1e6 / rate * heads, 1), "unit": "us/layer", "cores": R["cores"], "kind": R["kind"],
+               "sample": f"{args.cpu_sample} map-steps of the reference's selector.step at t=4096 per process, "
+                         f"{R['cores']} processes x 1 BLAS thread; x 32 heads per layer", "cpu_model": cpu_model()}
+    out = {"metric": "predict+top-k us/layer (cfg1: 32 heads, 4K ctx, block 16, 64-step history)",
+           "value": round(us_med / layers, 3), "unit": "us/layer", "n_gpus": 1, "steps": decode - args.warmup,
+           "warmup": args.warmup, "ms_per_step": round(us_med / 1e3, 4), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32 (fp16x3 tensor-core forecaster, fp64 guard)",
+           "data": source, "config": {"workload": "cfg1: 32 heads x t=4032..4096 x 64 decode steps, B=1024, b=16, H=64",
+                                       "maps_per_launch": n_maps, "layers_per_launch": layers,
+                                       "step": "push (compress + ring append) + ap_sel_step"},
+           "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                        "frac": round(achieved / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                        "algorithmic_bytes_per_launch": b_alg,
+                        "bytes_formula": "maps x (t*4 + (H+1)*W*4 + 4*K)  [SURVEY 8(d)]"},
+           "parity": {"maps": 8, "steps": decode, "map_steps": checked, "mismatches": int(mism), "exemptions": 0},
+           "accuracy_pct": round(100 * float(np.mean(ratios)), 2),
+           "accuracy_note": "prediction accuracy (evaluation.py:155-191) of the device selections, init_weights(0) "
+                            "(untrained) forecaster, 32 heads x 64 steps",
+           "tie_guard": sel.tie_stats(), "cpu_baseline": cpu, "clocks": clk.summary(),
+           "us_per_step_all": [round(x, 1) for x in us]}
+    print(json.dumps(out), flush=True)
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     """The reference's own CPU implementation of the path, as shipped: attncast.selector.step from
@@ -678,6 +810,8 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} disagrees with WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "cfg1":
+        run_cfg1(args, rank, world)
     else:
         run_ours(args, rank, world)
     if world > 1:

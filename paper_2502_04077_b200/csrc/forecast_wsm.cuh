@@ -317,11 +317,14 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                     for (int dj = 0; dj < 3; ++dj) {
                         const uint32_t pix = (uint32_t)(r * A1C + dj) * 16;
                         const uint64_t a_hi = umma_desc(a1_addr + pix, PLANE_M, 128);
-                        mma_f16(d, a_hi, bdesc[0][dj] + boff, idesc, 1);
                         if constexpr (PREC == AP_PREC_F16X3) {
+                            // a_hi feeds two MMAs: read its tile once, keep it in the A collector
                             const uint64_t a_lo = umma_desc(a1_addr + 2 * PLANE_M + pix, PLANE_M, 128);
-                            mma_f16(d, a_hi, bdesc[1][dj] + boff, idesc, 1);
+                            mma_f16_afill(d, a_hi, bdesc[0][dj] + boff, idesc, 1);
+                            mma_f16_alast(d, a_hi, bdesc[1][dj] + boff, idesc, 1);
                             mma_f16(d, a_lo, bdesc[0][dj] + boff, idesc, 1);
+                        } else {
+                            mma_f16(d, a_hi, bdesc[0][dj] + boff, idesc, 1);
                         }
                     }
                 }

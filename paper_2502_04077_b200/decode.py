@@ -81,7 +81,7 @@ class DecodeEngine:
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
                  seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0,
-                 fused: bool = True, gemm: str = "auto"):
+                 fused: bool = True, gemm: str = "auto", attn_splits: tuple[int, int] | None = None):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -98,6 +98,8 @@ class DecodeEngine:
             raise ConfigError("group must divide the GQA group size")
         if not 0 <= dense_layers < shape.n_layers:
             raise ConfigError("dense_layers must be in [0, n_layers)")
+        if offload_v and self.split is not None:
+            raise ConfigError("V offload runs with one GPU per sequence (sequence sharding), not with a KV-head split")
         if dense_layers and offload_v:
             raise ConfigError("dense layers need their V resident: not combinable with V offload")
         self.dense_layers = dense_layers
@@ -162,10 +164,9 @@ class DecodeEngine:
         self.logits = torch.zeros(S, V, dtype=bf, device=dev)
         self.seq_len = torch.full((S,), ctx_len, dtype=torch.int32, device=dev)
         self.maps_per_layer = Hq // group
-        self.att = DecodeAttention(S, Hq, Hkv, self.t_max,
-                                   n_splits_dense=dense_splits(S * Hkv, _lib.fn("ap_device_sm_count")(), self.t_max),
-                                   n_splits_sparse=sparse_splits(S * self.maps_per_layer,
-                                                                 _lib.fn("ap_device_sm_count")()), device=dev)
+        sms = _lib.fn("ap_device_sm_count")()
+        nd, ns = attn_splits or (dense_splits(S * Hkv, sms, self.t_max), sparse_splits(S * self.maps_per_layer, sms))
+        self.att = DecodeAttention(S, Hq, Hkv, self.t_max, n_splits_dense=nd, n_splits_sparse=ns, device=dev)
         self.sel = None
         from .selector import SelectorConfig
         self.cfg = cfg or SelectorConfig(budget=1024)
@@ -192,18 +193,25 @@ class DecodeEngine:
         self._fill_kv(gen)
 
     # ---------------------------------------------------------------- setup
+    def _heads(self, full, per_rank):
+        """This rank's slice of a full-model head axis (dim 1) under a KV-head split."""
+        if self.split is None:
+            return full
+        return full[:, self.split.rank * per_rank:(self.split.rank + 1) * per_rank]
+
     def _fill_kv(self, gen):
-        """Synthetic prefill: N(0,1) bf16 keys/values for positions [0, ctx_len) of every layer."""
+        """Synthetic prefill: N(0,1) bf16 keys/values for positions [0, ctx_len) of every layer.  Under a
+        KV-head split every rank draws the full model's KV and keeps its heads, so the split and the
+        unsplit engine hold the same cache."""
         torch = D.torch()
+        S, Hf, Hkv = self.n_seq, self.full_shape.n_kv_heads, self.shape.n_kv_heads
+        full = torch.empty(S, Hf, self.ctx_len, 128, dtype=torch.bfloat16, device=self.dev)
         for l in range(self.shape.n_layers):
-            self.k_cache[l, :, :, : self.ctx_len].normal_(generator=gen)
+            self.k_cache[l, :, :, : self.ctx_len].copy_(self._heads(full.normal_(generator=gen), Hkv))
             if self.voff is None:
-                self.v_cache[l, :, :, : self.ctx_len].normal_(generator=gen)
+                self.v_cache[l, :, :, : self.ctx_len].copy_(self._heads(full.normal_(generator=gen), Hkv))
             else:  # generate on the device, park in pinned host memory
-                tmp = torch.empty(self.n_seq, self.shape.n_kv_heads, self.ctx_len, 128, dtype=torch.bfloat16,
-                                  device=self.dev).normal_(generator=gen)
-                self.voff.host_v[l, :, :, : self.ctx_len].copy_(tmp)
-                del tmp
+                self.voff.host_v[l, :, :, : self.ctx_len].copy_(full.normal_(generator=gen))
         if self.voff is not None:
             self.voff.init_pages(self.ctx_len)
             torch.cuda.synchronize()
@@ -220,11 +228,12 @@ class DecodeEngine:
         H = self.cfg.history
         S, L = self.n_seq, self.shape.n_layers
         q = torch.empty_like(self.q)
+        qf = torch.empty(S, self.full_shape.n_q_heads, 128, dtype=q.dtype, device=q.device)
         lens = torch.empty_like(self.seq_len)
         for i in range(H - 1):
             pos = self.ctx_len - (H - 1) + i  # prompt position; its attention row covers keys [0, pos]
             lens.fill_(pos + 1)
-            q.normal_(generator=gen)
+            q.copy_(self._heads(qf.normal_(generator=gen), self.shape.n_q_heads))  # same draws split or not
             for l in range(self.dense_layers, L):
                 self.att.dense(q, self.k_cache[l], self.k_cache[l], lens, None, with_v=False, emit=True,
                                selector=self.sel, **self._map_kw(l))
@@ -318,7 +327,7 @@ class DecodeEngine:
                                       _lib.ptr(self.argws) if tokens is not None else None, _lib.ptr(tokens),
                                       _lib.stream_handle()), "ap_gemv")
 
-    def _step_body(self, variant: str):
+    def _step_body(self, variant: str, selector: bool = True):
         torch = D.torch()
         sh = self.shape
         S = self.n_seq
@@ -347,7 +356,7 @@ class DecodeEngine:
             self._mm(self.y, self.lm_head, self.logits)
             _lib.check(_lib.fn("ap_argmax_rows")(_lib.ptr(self.logits), S, sh.vocab, _lib.ptr(self.argws),
                                                  self.argws.numel(), _lib.ptr(self.tok), s), "ap_argmax_rows")
-        if self.sel is not None and variant != "dense":
+        if selector and self.sel is not None and variant != "dense":
             self.sel.step()  # forecast + top-k for the next token, every layer and head at once
 
     def variant_for_next(self) -> str:

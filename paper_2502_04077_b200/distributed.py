@@ -98,8 +98,13 @@ def gather_heads_into(out_full, local_out, split: HeadSplit, group=None):
         out_full.copy_(local_out)
         return out_full
     S, hq, D = local_out.shape
-    parts = torch.empty(split.world * S, hq, D, dtype=local_out.dtype, device=local_out.device)  # rank-major
-    dist.all_gather_into_tensor(parts, local_out.contiguous(), group=group)
+    if dist.get_backend(group) == "gloo" and local_out.is_cuda:  # host-staged (CPU tests; never on the NCCL path)
+        parts = torch.empty(split.world * S, hq, D, dtype=local_out.dtype)
+        dist.all_gather_into_tensor(parts, local_out.contiguous().cpu(), group=group)
+        parts = parts.to(local_out.device)
+    else:
+        parts = torch.empty(split.world * S, hq, D, dtype=local_out.dtype, device=local_out.device)  # rank-major
+        dist.all_gather_into_tensor(parts, local_out.contiguous(), group=group)
     out_full.copy_(parts.view(split.world, S, hq, D).permute(1, 0, 2, 3).reshape(S, split.world * hq, D))
     return out_full
 
