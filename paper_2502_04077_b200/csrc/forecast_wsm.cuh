@@ -22,14 +22,46 @@ namespace wsm {
 #ifndef AP_WSM_NX
 #define AP_WSM_NX 4
 #endif
+#ifndef AP_WSM_LAYOUT
+#define AP_WSM_LAYOUT 1
+#endif
+#if AP_WSM_LAYOUT
+// Warp w runs on scheduler w % 4.  Scheduler 1 (warps 1, 5, 9, 13) hosts only the MMA issuer, the
+// quadrant-1 epilogue warp, the producer and an idle warp, so the single thread that issues every
+// tcgen05.mma does not share its issue slots with conv1 warps; the 9 conv1 warps fill schedulers 0, 2, 3.
+#ifndef AP_WSM_CONV13
+#define AP_WSM_CONV13 0  // 1: warp 13 is a tenth conv1 warp (shares scheduler 1 with the MMA issuer)
+#endif
+constexpr int NCONV = 9 + AP_WSM_CONV13;
+#else
 constexpr int NCONV = AP_WSM_NCONV;         // conv1 warps (16 measured slower: shared-memory port)
+#endif
 constexpr int MO = 5;                       // output rows per band
 constexpr int MA = MO + 4;                  // a1 tile rows per band (2 segments x (n + 2))
 constexpr int MX = MO + 8;                  // x tile rows per band (2 segments x (n + 4))
 constexpr int NX = AP_WSM_NX;               // x tile stages
 constexpr int NA = 2;                       // a1 tile / accumulator stages
-constexpr int WARP_PROD = 0, WARP_MMA = 1, EPI0 = 2, NEPI = 4, CONV0 = 6;
+constexpr int NEPI = 4;
+#if AP_WSM_LAYOUT
+constexpr int WARP_PROD = 9, WARP_MMA = 1, EPI0 = 0;
+constexpr int NT = 16 * 32;
+enum { R_PROD, R_MMA, R_EPI, R_CONV, R_IDLE };
+__device__ __forceinline__ int role_of(int w) {
+    return w == WARP_PROD ? R_PROD : w == WARP_MMA ? R_MMA : (w == 0 || w == 2 || w == 3 || w == 5) ? R_EPI
+         : (w == 13 && !AP_WSM_CONV13) ? R_IDLE : R_CONV;
+}
+__device__ __forceinline__ int conv_rank(int w) {  // warps 4, 6, 7, 8, 10, 11, 12, 14, 15 (, 13) -> 0..8 (, 9)
+    return w == 13 ? 9 : w == 4 ? 0 : w < 9 ? w - 5 : w < 13 ? w - 6 : w - 7;
+}
+#else
+constexpr int WARP_PROD = 0, WARP_MMA = 1, EPI0 = 2, CONV0 = 6;
 constexpr int NT = (CONV0 + NCONV) * 32;
+enum { R_PROD, R_MMA, R_EPI, R_CONV, R_IDLE };
+__device__ __forceinline__ int role_of(int w) {
+    return w == WARP_PROD ? R_PROD : w == WARP_MMA ? R_MMA : w < EPI0 + NEPI ? R_EPI : R_CONV;
+}
+__device__ __forceinline__ int conv_rank(int w) { return w - CONV0; }
+#endif
 constexpr int NCONV_T = NCONV * 32;
 constexpr int TMEM = 512;
 constexpr int ACC_COLS = MO * 32;           // 160
@@ -151,7 +183,8 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
     const uint32_t tmem_base = *tmem_slot;
     if (tid == 0) WSM_CTA(1, gtimer());
 
-    if (warp == WARP_PROD) {
+    const int role = role_of(warp);
+    if (role == R_PROD) {
         // ------------------------------------------------------------------ producer (whole warp)
         const int G = gridDim.x, n_tasks = P.n_maps * P.n_chunks;
         const float b1max = g_b1abs[0], w1max = g_w1abs[0];
@@ -280,7 +313,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                 mbar_arrive(&x_full[s]);
             }
         }
-    } else if (warp == WARP_MMA) {
+    } else if (role == R_MMA) {
         // ------------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t b_addr = smem_u32(smem + Smem::off_b);
@@ -334,7 +367,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                 mbar_arrive(&acc_full[a]);  // releases info[a] to the epilogue
             }
         }
-    } else if (warp >= EPI0 && warp < EPI0 + NEPI) {
+    } else if (role == R_EPI) {
         // ------------------------------------------------------------------ epilogue
         const int quad = warp & 3, pix = quad * 32 + lane;
         const int wexp = g_wexp;
@@ -425,9 +458,9 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                 P.scores[(int64_t)I.map * P.score_stride + col] = c_w[OFF_B3] + (float)S / (float)H;
             }
         }
-    } else {
+    } else if (role == R_CONV) {
         // ------------------------------------------------------------------ conv1 workers
-        const int ct = tid - CONV0 * 32;
+        const int ct = conv_rank(warp) * 32 + lane;
         const int cw = ct >> 5;
         for (int b = 0;; ++b) {
             const int s = b % NX, a = b % NA;
