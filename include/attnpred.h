@@ -143,6 +143,9 @@ typedef struct ap_selector {
     int32_t* status;          /* [1] device status word                             */
     int32_t* tie_ws;          /* exact-boundary guard workspace, ap_sel_tie_ws_bytes(n_maps) bytes, zeroed
                                * once before first use; NULL disables the guard                         */
+    const int32_t* k_map;     /* [n_maps] per-map middle-block budget (budget allocation across layers /
+                               * heads: selector.py:47-50 evaluated per map), each <= k_mid (the pitch of
+                               * mid_blocks); NULL = k_mid for every map                                  */
 } ap_selector;
 
 /* Zero the state of every map (selector.init_state with no prefill rows). */

@@ -56,6 +56,7 @@ class Selector(ctypes.Structure):
         ("slot_width", ctypes.c_void_p), ("slot_xmax", ctypes.c_void_p),
         ("state", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("mid_blocks", ctypes.c_void_p),
         ("mid_mask", ctypes.c_void_p), ("status", ctypes.c_void_p), ("tie_ws", ctypes.c_void_p),
+        ("k_map", ctypes.c_void_p),
     ]
 
 

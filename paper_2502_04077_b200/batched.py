@@ -42,7 +42,8 @@ class BatchedSelector:
     w_max: the largest compressed width any map will reach (ceil(t_max/b)).
     """
 
-    def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "fp16x3", device=None, tie_guard: bool = True):
+    def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "fp16x3", device=None, tie_guard: bool = True,
+                 budgets=None):
         cfg.validate()
         if n_maps < 1 or w_max < 1:
             raise ParameterError("n_maps and w_max must be >= 1")
@@ -67,6 +68,13 @@ class BatchedSelector:
         self.mid_blocks = torch.zeros(n_maps, max(self.k_mid, 1), dtype=i32, device=dev)
         self.mid_mask = torch.zeros(n_maps, words, dtype=i32, device=dev)
         self.status = torch.zeros(1, dtype=i32, device=dev)
+        # budget allocation: per-map token budgets (selector.py:47-50 evaluated per map); cfg.budget is the
+        # largest, it sets the pitch of mid_blocks
+        self.k_map = None
+        if budgets is not None:
+            from .budget import middle_blocks_per_map
+            km = middle_blocks_per_map(budgets, n_maps, cfg)
+            self.k_map = torch.from_numpy(km).to(dev)
         # exact-boundary guard workspace (csrc/tieguard.cuh): near-tie candidates of the top-k boundary
         # are re-scored in fp64 so the block ids equal the float64 reference's
         self.tie_ws = None
@@ -82,6 +90,7 @@ class BatchedSelector:
             state=self.state.data_ptr(), scores=self.scores.data_ptr(), mid_blocks=self.mid_blocks.data_ptr(),
             mid_mask=self.mid_mask.data_ptr(), status=self.status.data_ptr(),
             tie_ws=None if self.tie_ws is None else self.tie_ws.data_ptr(),
+            k_map=None if self.k_map is None else self.k_map.data_ptr(),
         )
         self.reset()
 

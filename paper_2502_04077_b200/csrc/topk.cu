@@ -181,7 +181,9 @@ __global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s, tie::Params
         block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
         if (s_nan) raise_status(s.status, AP_ENUMERIC);
         const int available = W - n_masked;
-        const int k = s.k_mid < available ? s.k_mid : available;
+        // per-map middle budget (budget allocation policy; selector.py:47-50 per map), capped by the pitch
+        const int kcap = s.k_map ? min(max(s.k_map[m], 0), s.k_mid) : s.k_mid;
+        const int k = kcap < available ? kcap : available;
         for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
         __syncthreads();
         if (k > 0) {
@@ -273,7 +275,9 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
         block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
         if (s_nan) raise_status(s.status, AP_ENUMERIC);
         const int available = W - n_masked;
-        const int k = s.k_mid < available ? s.k_mid : available;
+        // per-map middle budget (budget allocation policy; selector.py:47-50 per map), capped by the pitch
+        const int kcap = s.k_map ? min(max(s.k_map[m], 0), s.k_mid) : s.k_mid;
+        const int k = kcap < available ? kcap : available;
         for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
         if (k > 0) {
             // radix select of the k-th largest key, 8 bits per pass

@@ -81,7 +81,8 @@ class DecodeEngine:
     def __init__(self, shape: ModelShape, n_seq: int, ctx_len: int, max_new: int, *, mode: str = "sparse",
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
                  seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0,
-                 fused: bool = True, gemm: str = "auto", attn_splits: tuple[int, int] | None = None):
+                 fused: bool = True, gemm: str = "auto", attn_splits: tuple[int, int] | None = None,
+                 layer_budgets=None):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -177,8 +178,9 @@ class DecodeEngine:
         self._wdigest = weights_digest(self.pweights)
         if mode == "sparse":
             install_weights(self.pweights)
+            self.layer_budgets = layer_budgets
             self.sel = BatchedSelector(self.cfg, S * self.sel_layers * self.maps_per_layer, self.t_max // 16,
-                                       precision=precision, device=dev)
+                                       precision=precision, device=dev, budgets=self._map_budgets())
         self.voff = None
         if offload_v:
             if mode != "sparse" or group != G:
@@ -238,6 +240,16 @@ class DecodeEngine:
                 self.att.dense(q, self.k_cache[l], self.k_cache[l], lens, None, with_v=False, emit=True,
                                selector=self.sel, **self._map_kw(l))
         torch.cuda.synchronize()
+
+    def _map_budgets(self):
+        """Per-map token budgets of the sparse layers (budget allocation; None = cfg.budget everywhere)."""
+        if getattr(self, "layer_budgets", None) is None:
+            return None
+        import numpy as np
+        lb = np.asarray(self.layer_budgets, dtype=np.int64)
+        if lb.shape != (self.sel_layers,):
+            raise ConfigError(f"layer_budgets needs one budget per sparse layer ({self.sel_layers})")
+        return np.tile(np.repeat(lb, self.maps_per_layer), self.n_seq)
 
     def _map_kw(self, l: int) -> dict:
         """Selector map range of layer l (layers below dense_layers own none)."""
@@ -442,7 +454,7 @@ class DecodeEngine:
         self.group = group
         self.maps_per_layer = self.shape.n_q_heads // group
         self.sel = BatchedSelector(self.cfg, self.n_seq * self.sel_layers * self.maps_per_layer,
-                                   self.t_max // 16, precision=prec, device=self.dev)
+                                   self.t_max // 16, precision=prec, device=self.dev, budgets=self._map_budgets())
         self.mode = "sparse"
         self.counter = 0
         self.seq_len.fill_(self.ctx_len)
