@@ -438,14 +438,17 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_ws_kernel(ConvParams P) {
             tc_fence_before();  // our tcgen05.ld reads of buffer a are complete before it is reused
             __syncwarp();
             if (warp == EPI0 && lane == 0) WS_TRACE(b, 7);
+            const bool last = I.last;  // read before the release: the MMA issuer refills the info slot after it
+            const int64_t sat = (int64_t)I.map * P.score_stride + col;
+            __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[a]);
-            if (I.last && live) {
+            if (last && live) {
                 float osum = 0.f;
 #pragma unroll
                 for (int k = 0; k < NOLD; ++k) osum += oldv[k];
                 S += Snew - (double)osum;
                 if (P.rsum) P.rsum[at] = S;
-                P.scores[(int64_t)I.map * P.score_stride + col] = c_w[OFF_B3] + (float)S / (float)H;
+                P.scores[sat] = c_w[OFF_B3] + (float)S / (float)H;
             }
         }
     } else {

@@ -450,12 +450,14 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
             tc_fence_before();
             __syncwarp();
             const bool last = I.last;
+            const int64_t sat = (int64_t)I.map * P.score_stride + col;
             if (warp == EPI0 && lane == 0) WSM_TRACE(b, 7);
-            if (lane == 0) mbar_arrive(&acc_empty[a]);  // (info[a] is not read after this)
+            __syncwarp();  // every lane has read ainfo[a]: the MMA issuer refills it once all four warps arrive
+            if (lane == 0) mbar_arrive(&acc_empty[a]);  // (ainfo[a] is not read after this)
             if (last && live) {
                 S += Snew - (double)osum;
                 if (P.rsum) P.rsum[at] = S;
-                P.scores[(int64_t)I.map * P.score_stride + col] = c_w[OFF_B3] + (float)S / (float)H;
+                P.scores[sat] = c_w[OFF_B3] + (float)S / (float)H;
             }
         }
     } else if (role == R_CONV) {

@@ -133,8 +133,11 @@ class DecodeEngine:
         # KV cache [L][S][Hkv][t_max][128]; with offload_v, V lives in pinned host memory and a small
         # device page pool fed by the cross-token prefetch (kernel 5), K stays resident
         self.offload = offload_v
-        self.k_cache = torch.empty(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
-        self.v_cache = None if offload_v else torch.empty(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
+        # zeroed, not torch.empty: the kernels load whole 16-token blocks and mask positions >= t in the
+        # scores, but P.V on the tensor cores would still turn a recycled NaN/inf in an unwritten V row
+        # into a NaN output (0 * NaN)
+        self.k_cache = torch.zeros(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
+        self.v_cache = None if offload_v else torch.zeros(L, n_seq, Hkv, self.t_max, 128, dtype=bf, device=dev)
         # activations
         S = n_seq
         self.r = torch.zeros(S, Hd, dtype=bf, device=dev)

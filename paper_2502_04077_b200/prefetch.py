@@ -40,7 +40,7 @@ class OffloadedV:
         n_pages = self.sink_pages + recent_pages + k_cap
         bf = torch.bfloat16
         # pinned (hence mapped under UVA) host V, layout [L][S][Hkv][t_max][128]
-        self.host_v = torch.empty(n_layers, n_seq, n_kv_heads, t_max, HEAD_DIM, dtype=bf, pin_memory=True)
+        self.host_v = torch.zeros(n_layers, n_seq, n_kv_heads, t_max, HEAD_DIM, dtype=bf, pin_memory=True)
         self.pages = torch.zeros(self.n_vmaps, n_pages, BLOCK, HEAD_DIM, dtype=bf, device=dev)
         i32 = torch.int32
         self.mid_page = torch.zeros(self.n_vmaps, k_cap, dtype=i32, device=dev)
