@@ -468,6 +468,65 @@ def roofline_for(eng, args, us, W, key):
                        "issued_frac_fp16x3": round(3 * tflops / tf_peak, 4) if args.precision == "fp16x3" else None}}
 
 
+def offload_extras(eng, args, shape, cfg, group, rank, units, elapsed, prefetch):
+    """cfg4 (V offloaded + cross-token prefetch): the prefetch kernel's own GB/s per launch (one cold
+    gather of every selected middle block of a layer, and the steady-state delta launches), the
+    DENSE-RESIDENT comparator (the whole KV on the device: 17 GB at 128K fits in HBM) plus a resident
+    sparse arm, and the reference's cross-token latency model (prefetchsim.py:130-151:
+    total = max(compute, predict + transfer), transfer = bytes / bw) evaluated on the measured parts."""
+    import torch
+    from paper_2502_04077_b200.decode import DecodeEngine
+    voff, sel = eng.voff, eng.sel
+    snap = eng._snapshot()
+    mps = eng.sel_layers * eng.maps_per_layer
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(4)]
+    cold = []
+    for i, l in enumerate(range(0, min(4, shape.n_layers))):  # cold: every middle block of layer l is new
+        voff.old_n.zero_()
+        b0 = int(voff.bytes_copied.item())
+        ev[i][0].record()
+        voff.prefetch(sel, l, mps)
+        ev[i][1].record()
+        torch.cuda.synchronize()
+        cold.append((int(voff.bytes_copied.item()) - b0, ev[i][0].elapsed_time(ev[i][1]) * 1e-3))
+    eng._restore(snap)
+    cold_bytes = sum(b for b, _ in cold) / len(cold)
+    cold_s = sum(t for _, t in cold) / len(cold)
+    out = {"cold_gather_bytes_per_launch": int(cold_bytes),
+           "cold_gather_GBps_per_launch": round(cold_bytes / cold_s / 1e9, 2),
+           "cold_gather_frac_of_h2d_peak": round(cold_bytes / cold_s / 1e9 / prefetch["h2d_copy_peak_GBps"], 3),
+           "steady_bytes_per_launch": prefetch["bytes_per_step"] // shape.n_layers}
+    # resident comparators on the same shape (a second engine: V on the device)
+    res = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * (args.warmup + args.steps) + 8, cfg=cfg,
+                       group=group, precision=args.precision, seed=rank)
+    res.init_history()
+    first_token(res)
+    for _ in range(args.warmup):
+        res.step()
+    r_el, _ = timed_steps(res, args.steps, 1)
+    us_sel, _ = measure_selector(res)
+    res.set_mode("dense")
+    res.capture_all()
+    for _ in range(args.warmup):
+        res.step()
+    d_el, _ = timed_steps(res, args.steps, 1)
+    del res
+    torch.cuda.empty_cache()
+    compute_ms = r_el / args.steps * 1e3  # the step with every byte resident: no transfer on the path
+    transfer_ms = prefetch["bytes_per_step"] / (prefetch["h2d_copy_peak_GBps"] * 1e9) * 1e3
+    predict_ms = us_sel * 1e-3
+    out.update({"sparse_resident_tok_s": round(args.batch * args.steps * units / r_el, 2),
+                "dense_resident_tok_s": round(args.batch * args.steps * units / d_el, 2),
+                "cross_token_model": {
+                    "compute_ms": round(compute_ms, 4), "predict_ms": round(predict_ms, 4),
+                    "transfer_ms": round(transfer_ms, 4),
+                    "model_total_ms": round(max(compute_ms, predict_ms + transfer_ms), 4),
+                    "measured_ms": round(elapsed / args.steps * 1e3, 4),
+                    "formula": "prefetchsim.py:147-151 total = max(compute, predict + transfer); compute = the "
+                               "resident sparse step, predict = ap_sel_step, transfer = V bytes per step / H2D peak"}})
+    return out
+
+
 def run_ours(args, rank, world):
     import torch
     from paper_2502_04077_b200.decode import SHAPES, DecodeEngine
@@ -539,6 +598,8 @@ def run_ours(args, rank, world):
         alt = {"selection": other, "value": round(args.batch * args.steps * units / a_el, 2), "unit": "tok/s",
                "roofline": roofline_for(eng, args, a_us, a_W, f"{args.model}:{args.ctx}:{other}:{args.precision}")}
 
+    if prefetch is not None:
+        prefetch.update(offload_extras(eng, args, shape, cfg, group, rank, units, elapsed, prefetch))
     dense = None
     if not args.no_dense:
         eng.set_mode("dense")

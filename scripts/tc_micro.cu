@@ -7,7 +7,8 @@
 
 using namespace ap;
 
-template <int N, bool TS>
+// TS: 0 = SS, 1 = TS (A from TMEM), 2 = SS with the A collector (fill / lastuse pairs: A read once per 2 MMAs)
+template <int N, int TS>
 __global__ void mma_bench(long long* out, int iters) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint32_t tslot;
@@ -27,7 +28,9 @@ __global__ void mma_bench(long long* out, int iters) {
         const uint64_t adesc = umma_desc(a_addr, 2048, 128), bdesc = umma_desc(b_addr, N * 16, 128);
         long long t0 = clock64();
         for (int i = 0; i < iters; ++i) {
-            if (TS) mma_f16_ts(t + 256, t, bdesc, idesc, 1);
+            if (TS == 1) mma_f16_ts(t + 256, t, bdesc, idesc, 1);
+            else if (TS == 2 && (i & 1) == 0) mma_f16_afill(t + 256, adesc, bdesc, idesc, 1);
+            else if (TS == 2) mma_f16_alast(t + 256, adesc, bdesc, idesc, 1);
             else mma_f16(t + 256, adesc, bdesc, idesc, 1);
         }
         mma_commit(&bar);
@@ -47,7 +50,7 @@ __global__ void mma_bench(long long* out, int iters) {
     if (tid < 32) tmem_dealloc(t, 512);
 }
 
-template <int N, bool TS>
+template <int N, int TS>
 void run(int iters) {
     long long* d;
     cudaMalloc(&d, 16);
@@ -56,18 +59,18 @@ void run(int iters) {
     long long h[2];
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     cudaError_t e = cudaGetLastError();
-    printf("N=%3d %s: %.1f cycles/MMA  (%.0f MAC/clk)   cp128x256b: %.1f cycles  %s\n", N, TS ? "TS" : "SS",
+    printf("N=%3d %s: %.1f cycles/MMA  (%.0f MAC/clk)   cp128x256b: %.1f cycles  %s\n", N, TS == 1 ? "TS" : TS == 2 ? "SS+collector" : "SS",
            (double)h[0] / iters, 128.0 * N * 16 * iters / h[0], (double)h[1] / iters, cudaGetErrorString(e));
     cudaFree(d);
 }
 
 int main() {
     const int it = 4096;
-    run<32, true>(it);  run<32, false>(it);
-    run<64, true>(it);  run<64, false>(it);
-    run<96, true>(it);  run<96, false>(it);
-    run<128, true>(it); run<128, false>(it);
-    run<192, true>(it); run<192, false>(it);
-    run<256, true>(it); run<256, false>(it);
+    run<32, 1>(it);  run<32, 0>(it);  run<32, 2>(it);
+    run<64, 1>(it);  run<64, 0>(it);  run<64, 2>(it);
+    run<96, 1>(it);  run<96, 0>(it);  run<96, 2>(it);
+    run<128, 1>(it); run<128, 0>(it); run<128, 2>(it);
+    run<192, 1>(it); run<192, 0>(it); run<192, 2>(it);
+    run<256, 1>(it); run<256, 0>(it); run<256, 2>(it);
     return 0;
 }
