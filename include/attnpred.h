@@ -239,6 +239,11 @@ int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, in
  * exp(blockmax - LSE_S) on touched blocks, 0 elsewhere) to the ring. */
 int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
                    int32_t group, int emit, void* stream);
+/* L2 warm-up for the next ap_attn_sparse of the same layer: prefetches (evict_last) the K/V blocks
+ * that pass will gather, except the block holding the newest token.  Meant for a side stream
+ * beside the layer's qkv projection; no results, no ordering requirement. */
+int ap_attn_sparse_prefetch(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                            int32_t group, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Cross-token prefetch (kernel 5) — the real counterpart of the cross_token

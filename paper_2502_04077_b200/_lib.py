@@ -120,6 +120,8 @@ SIGNATURES = {
     "ap_attn_set_calib_kernel": (ctypes.c_int, [ctypes.c_int]),
     "ap_attn_sparse": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.POINTER(Selector), _I32, _I32, _I32,
                                       ctypes.c_int, _P]),
+    "ap_attn_sparse_prefetch": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.POINTER(Selector), _I32, _I32,
+                                               _I32, _P]),
     "ap_prefetch": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.POINTER(VPages), _I32, _I32, _I32, _I32, _P]),
     "ap_v_append": (ctypes.c_int, [_P, _I32, _I32, _P, ctypes.POINTER(VPages), _I32, _I32, _P]),
     "ap_v_pages_init": (ctypes.c_int, [ctypes.POINTER(VPages), _I64, _I64, _P]),

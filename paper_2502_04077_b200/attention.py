@@ -83,6 +83,14 @@ class DecodeAttention:
         _lib.check(_lib.fn("ap_attn_dense")(ctypes.byref(desc), int(with_v), sel, map_base, mps, group, int(emit),
                                             _lib.stream_handle(stream)), "attn_dense")
 
+    def sparse_prefetch(self, q, k_cache, v_cache, seq_len, selector, *, map_base=0, maps_per_seq=None, group=1,
+                        stream=None):
+        """L2 warm-up of the blocks the next sparse() of this layer gathers (side stream)."""
+        desc = self._desc(q, k_cache, v_cache, seq_len, None, self.n_splits_sparse)
+        mps = maps_per_seq if maps_per_seq is not None else self.n_q_heads // group
+        _lib.check(_lib.fn("ap_attn_sparse_prefetch")(ctypes.byref(desc), ctypes.byref(selector._desc), map_base, mps,
+                                                      group, _lib.stream_handle(stream)), "attn_sparse_prefetch")
+
     def sparse(self, q, k_cache, v_cache, seq_len, out, selector, *, emit=True, map_base=0, maps_per_seq=None,
                group=1, vpages=None, layer=0, stream=None):
         """v_cache is ignored (may be any tensor) when ``vpages`` (an OffloadedV) supplies paged V."""

@@ -1223,6 +1223,42 @@ static int make_params(const ap_attn_layer* a, const ap_selector* sel, int32_t m
 }
 
 
+// ------------------------------------------------------------------ L2 warm-up for the sparse pass
+// One warp per map: the blocks the sparse pass of this layer will gather (sink | local | middle, as
+// sparse_cluster_kernel enumerates them) are prefetched into L2 with evict_last priority, plus the map's
+// state and middle-block ids.  Launched on a side stream at the start of the layer, it runs beside the
+// qkv projection (which holds every SM's shared memory but leaves threads free), so the sparse pass's
+// dependent loads and TMA block fetches hit L2 instead of HBM.  Reads only data older than this step's
+// newest token (the newest block is written by the projection; its prefetch is skipped).
+__global__ void __launch_bounds__(128) sparse_l2_prefetch_kernel(AttnParams P) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = blockIdx.x * 4 + warp, s = blockIdx.y;
+    const int maps = P.n_q_heads / P.group;
+    if (g >= maps) return;
+    const int64_t t = P.seq_len[s];
+    const int b = P.block;
+    const int map = s * P.maps_per_seq + P.map_base + g;
+    const ap_map_state ms = P.sel.state[map];
+    const int64_t sink_end = P.sel.sink < t ? P.sel.sink : t;
+    const int64_t local_start = t - P.sel.local > 0 ? t - P.sel.local : 0;
+    const int64_t sb = (sink_end + b - 1) / b, eb = (t + b - 1) / b;
+    int64_t lb = local_start / b;
+    if (lb < sb) lb = sb;
+    const int n_local = (int)(eb - lb);
+    const int n_units = (int)sb + n_local + ms.n_mid;
+    const int32_t* mid = P.sel.mid_blocks + (int64_t)map * (P.sel.k_mid > 0 ? P.sel.k_mid : 1);
+    const int kvh = (g * P.group) / (P.n_q_heads / P.n_kv_heads);
+    const char* kh = reinterpret_cast<const char*>(P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD);
+    const char* vh = reinterpret_cast<const char*>(P.v + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD);
+    for (int u = 0; u < n_units; ++u) {
+        const int64_t j = u < sb ? u : (u < sb + n_local ? lb + (u - sb) : (int64_t)__ldg(mid + (u - sb - n_local)));
+        if (j == eb - 1) continue;  // holds the newest token: written by the kernel before the sparse pass
+        const int64_t off = j * b * HD * 2 + lane * 128;  // 16 tokens x 256 B = 32 lanes x 128 B
+        asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(kh + off));
+        if (!P.paged) asm volatile("prefetch.global.L2::evict_last [%0];" :: "l"(vh + off));
+    }
+}
+
 // ------------------------------------------------------------------ calibration pass on tcgen05
 // The K-only dense pass of calibration steps (every M-th step reads all of K: 64 MiB per layer at
 // 32K for LLaMA-3.1-8B) as a TMA + tensor-core stream.  Per 128-token tile: two TMA boxes
@@ -1599,6 +1635,17 @@ int ap_attn_dense(const ap_attn_layer* a, int with_v, const ap_selector* sel, in
 
 int ap_attn_sparse_paged(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
                          int32_t group, int emit, const ap_vpages* vp, int32_t layer, void* stream);
+
+int ap_attn_sparse_prefetch(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
+                            int32_t group, void* stream) {
+    AttnParams P;
+    int rc = make_params(a, sel, map_base, maps_per_seq, group, P);
+    if (rc != AP_OK) return rc;
+    AP_REQUIRE(sel != nullptr, AP_EPARAM, "the L2 warm-up needs a selector");
+    const int maps = P.n_q_heads / P.group;
+    sparse_l2_prefetch_kernel<<<dim3((maps + 3) / 4, P.n_seq), 128, 0, as_stream(stream)>>>(P);
+    return launch_status("sparse_l2_prefetch_kernel");
+}
 
 int ap_attn_sparse(const ap_attn_layer* a, const ap_selector* sel, int32_t map_base, int32_t maps_per_seq,
                    int32_t group, int emit, void* stream) {

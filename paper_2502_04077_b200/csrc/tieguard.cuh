@@ -96,6 +96,62 @@ __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn
     return NB;
 }
 
+// The same for one warp holding a map's keys in registers (sel_topk_warp_kernel: block q * 32 + lane in
+// key[q]).  All lanes of the warp.
+template <int IPT>
+__device__ int detect_warp(const ap_selector& s, const Params& tp, int m, const uint32_t (&key)[IPT], int W, int k,
+                           uint32_t T, float amax, int sink_hi, int local_lo, int local_hi) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const float tau = key_value(T);
+    const float band = tp.rel * fmaxf(fabsf(tau), tp.floor * amax);
+    const uint32_t khi = order_key(tau + band), klo = order_key(tau - band);
+    int na = 0, nb = 0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+        na += key[q] > khi;
+        nb += key[q] >= klo && key[q] <= khi;
+    }
+    const int NA = (int)__reduce_add_sync(FULL, (unsigned)na), NB = (int)__reduce_add_sync(FULL, (unsigned)nb);
+    const int need = k - NA;
+    if (NB <= need) return 0;
+    int* ws = s.tie_ws;
+    if (NB > CAP || s.history > NG * MAX_RG) {
+        if (lane == 0) atomicAdd(&ws[H_OVERFLOW], 1);
+        return -NB;
+    }
+    int* rec = ws + rec_off(s.n_maps) + (int64_t)m * REC;
+    const unsigned lt = (1u << lane) - 1u;
+    int pos = 0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {  // ascending block ids
+        const bool in = key[q] >= klo && key[q] <= khi;
+        const unsigned bm = __ballot_sync(FULL, in);
+        if (in) rec[OFF_IDS + pos + __popc(bm & lt)] = q * 32 + lane;
+        pos += __popc(bm);
+    }
+    for (int j = lane; j < NB; j += 32) rec[OFF_CPEND + j] = NG;
+    int ub = 0;
+    if (lane == 0) {
+        rec[R_NA] = NA;
+        rec[R_NEED] = need;
+        rec[R_NB] = NB;
+        rec[R_KLO] = (int)klo;
+        rec[R_KHI] = (int)khi;
+        rec[R_PENDING] = NB;
+        rec[R_W] = W;
+        rec[R_SINK_HI] = sink_hi;
+        rec[R_LOCAL_LO] = local_lo;
+        rec[R_LOCAL_HI] = local_hi;
+        ub = atomicAdd(&ws[H_UNITS], NB * NG);
+        atomicAdd(&ws[H_MAPS], 1);
+        atomicAdd(&ws[H_CANDS], NB);
+    }
+    ub = __shfl_sync(FULL, ub, 0);
+    for (int u = lane; u < NB * NG; u += 32) ws[HDR + ub + u] = (m * CAP + u / NG) * NG + u % NG;
+    return NB;
+}
+
 // ------------------------------------------------------------------ fp64 re-scoring
 // sum over history rows [g*RG, g*RG+RG) of r_i = sum_c w3[c] relu(s2[c][i][col]), in fp64, fixed order.
 // x window [RG+4 rows][5 cols], a1 window [RG+2 rows][16 ch][3 cols] in shared memory; warp w takes

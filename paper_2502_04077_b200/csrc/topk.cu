@@ -9,6 +9,9 @@
 // finds the k-th largest key T; then one ordered pass takes every key > T and
 // the lowest-index keys == T until k are taken.  Output ids are ascending,
 // which is the set the reference returns.  Bit-exact on identical inputs.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "tieguard.cuh"
 
@@ -368,8 +371,117 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
     }
 }
 
+// Warp-per-map variant for rows of <= 32 * IPT blocks (W = 2049 at 32K needs IPT 72): lane l owns blocks
+// q * 32 + l, so a ballot over one q covers 32 consecutive blocks — exactly one word of the bitmask and
+// a run of ascending ids.  The k-th largest key comes from a 32-step binary search on the key bits (a
+// warp reduction per step, no CTA barriers); ties are ranked by ballots in index order.  Same results
+// as sel_topk_reg_kernel (the CTA form is kept for the generic path and A/B checks).
+template <int IPT>
+__global__ void __launch_bounds__(64) sel_topk_warp_kernel(ap_selector s, tie::Params tp) {
+    static_assert(IPT % 8 == 0, "eight counting chains");
+    const int lane = threadIdx.x & 31;
+    const int m = blockIdx.x * 2 + (threadIdx.x >> 5);
+    if (m >= s.n_maps) return;
+    const unsigned FULL = 0xffffffffu;
+    ap_map_state st = s.state[m];
+    const bool update = (st.counter % s.update_interval) == 0;
+    const int words = (s.w_max + 31) / 32;
+    uint32_t* mask = s.mid_mask + (int64_t)m * words;
+    int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
+    int count = st.n_mid, tie_n = 0;
+    if (update && s.k_mid > 0 && st.width > 0) {
+        const int W = st.width, b = s.block;
+        const int64_t t = st.row_len, nl = t + 1;
+        // covering blocks of sink [0, min(sink, nl)) and local [max(0, nl-local), nl) — selector.py:84-88,134-142
+        const int64_t sink_end = s.sink < nl ? s.sink : nl;
+        int sink_hi = sink_end > 0 ? (int)cdiv64(sink_end, b) : 0;
+        const int64_t ls = nl - s.local > 0 ? nl - s.local : 0;
+        const int local_lo = ls < nl ? (int)(ls / b) : 0;
+        int local_hi = ls < nl ? (int)cdiv64(nl, b) : 0;
+        sink_hi = sink_hi > W ? W : sink_hi;
+        local_hi = local_hi > W ? W : local_hi;
+        const float* sc = s.scores + (int64_t)m * s.w_max;
+        uint32_t key[IPT];
+        int n_masked = 0;
+        bool nan = false;
+        float amax = 0.f;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+            const int i = q * 32 + lane;
+            const float v = i < W ? sc[i] : -INFINITY;
+            nan |= v != v;
+            const bool masked = i >= W || i < sink_hi || (i >= local_lo && i < local_hi);
+            key[q] = masked ? 0u : order_key(v);  // 0 sorts below every real key (and is never taken)
+            n_masked += i < W && (masked || v == -INFINITY);
+            if (!masked && fabsf(v) <= 3.402823466e38f) amax = fmaxf(amax, fabsf(v));
+        }
+        if (__any_sync(FULL, nan) && lane == 0) raise_status(s.status, AP_ENUMERIC);
+        n_masked = __reduce_add_sync(FULL, n_masked);
+        amax = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(amax)));  // non-negative: bits order
+        const int available = W - n_masked;
+        const int kcap = s.k_map ? min(max(s.k_map[m], 0), s.k_mid) : s.k_mid;
+        const int k = kcap < available ? kcap : available;
+        for (int w = lane; w < words; w += 32) mask[w] = 0u;
+        count = 0;
+        if (k > 0) {
+            // T = the k-th largest key: the largest T with #(key >= T) >= k, bit by bit from the top
+            uint32_t T = 0;
+#pragma unroll 1
+            for (int bit = 31; bit >= 0; --bit) {
+                const uint32_t cand = T | (1u << bit);
+                int c[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // independent chains (IPT is a multiple of 8)
+#pragma unroll
+                for (int q = 0; q < IPT; ++q) c[q & 7] += key[q] >= cand;
+                const int cs = ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
+                if ((int)__reduce_add_sync(FULL, (unsigned)cs) >= k) T = cand;
+            }
+            int n_gt = 0;
+#pragma unroll
+            for (int q = 0; q < IPT; ++q) n_gt += key[q] > T;
+            const int take_eq = k - (int)__reduce_add_sync(FULL, (unsigned)n_gt);
+            // ordered emission: keys > T and the lowest-index take_eq keys == T, ascending
+            const unsigned lt = (1u << lane) - 1u;
+            int eq_before = 0, pos = 0;
+            __syncwarp();  // mask words cleared above by other lanes
+#pragma unroll
+            for (int q = 0; q < IPT; ++q) {
+                const unsigned eqm = __ballot_sync(FULL, key[q] == T);
+                const bool take = key[q] > T || (key[q] == T && eq_before + __popc(eqm & lt) < take_eq);
+                const unsigned tm = __ballot_sync(FULL, take);
+                eq_before += __popc(eqm);
+                if (take) mid[pos + __popc(tm & lt)] = q * 32 + lane;
+                if (lane == 0 && tm) mask[q] = tm;
+                pos += __popc(tm);
+            }
+            count = pos;
+            if (tp.enabled && s.tie_ws) tie_n = tie::detect_warp<IPT>(s, tp, m, key, W, k, T, amax, sink_hi,
+                                                                      local_lo, local_hi);
+        }
+        st.n_mid = count;
+        st.mid_clip = t;
+        st.r_pushed = st.n_pushed;
+        st.r_width = st.width;
+        st.r_wgen = tp.wgen ? *tp.wgen : 0;
+        st.tie_n = tie_n;
+    } else if (update && s.k_mid <= 0) {
+        for (int w = lane; w < words; w += 32) mask[w] = 0u;
+        st.n_mid = 0;
+    }
+    st.counter += 1;
+    __syncwarp();
+    if (lane == 0) s.state[m] = st;
+}
+
 void launch_sel_topk(const ap_selector& s, const tie::Params& tp, cudaStream_t stream) {
-    if (s.w_max <= 256 * 8) sel_topk_reg_kernel<256, 8><<<s.n_maps, 256, 0, stream>>>(s, tp);
+    static int warp_form = -1;
+    if (warp_form < 0) {
+        const char* e = getenv("ATTNPRED_TOPK_KERNEL");
+        warp_form = !(e && strcmp(e, "cta") == 0);
+    }
+    const unsigned wgrid = (unsigned)((s.n_maps + 1) / 2);
+    if (warp_form && s.w_max <= 32 * 16) sel_topk_warp_kernel<16><<<wgrid, 64, 0, stream>>>(s, tp);
+    else if (warp_form && s.w_max <= 32 * 72) sel_topk_warp_kernel<72><<<wgrid, 64, 0, stream>>>(s, tp);
+    else if (s.w_max <= 256 * 8) sel_topk_reg_kernel<256, 8><<<s.n_maps, 256, 0, stream>>>(s, tp);
     else if (s.w_max <= 256 * 16) sel_topk_reg_kernel<256, 16><<<s.n_maps, 256, 0, stream>>>(s, tp);
     else sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s, tp);
     if (tp.enabled && s.tie_ws) {

@@ -82,7 +82,7 @@ class DecodeEngine:
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
                  seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0,
                  fused: bool = True, gemm: str = "auto", attn_splits: tuple[int, int] | None = None,
-                 layer_budgets=None):
+                 layer_budgets=None, l2_warm: bool = True):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -193,6 +193,9 @@ class DecodeEngine:
                                    sink_tokens=self.cfg.sink_tokens, local_tokens=self.cfg.local_tokens, device=dev)
             self.pf_stream = torch.cuda.Stream(device=dev)
             self.pf_events = [torch.cuda.Event() for _ in range(L)]
+        # sparse-pass L2 warm-up on a side stream (ap_attn_sparse_prefetch), resident V only
+        self.l2_warm = l2_warm
+        self.warm_stream = torch.cuda.Stream(device=dev)
         self.counter = 0  # selector step counter (host mirror; all maps move in lockstep)
         self.graphs = {}
         self._fill_kv(gen)
@@ -268,6 +271,13 @@ class DecodeEngine:
         s = _lib.stream_handle()
         kc = self.k_cache[l]
         vc = self.v_cache[l] if self.voff is None else self.voff.layer_view(l)
+        warm = (self.l2_warm and variant in ("plain", "calib") and l >= self.dense_layers and self.voff is None)
+        if warm:  # L2 warm-up of this layer's selected K/V blocks, beside the qkv projection
+            main = torch.cuda.current_stream()
+            self.warm_stream.wait_stream(main)
+            with torch.cuda.stream(self.warm_stream):
+                self.att.sparse_prefetch(self.q, kc, vc, self.seq_len, self.sel, **self._map_kw(l),
+                                         stream=self.warm_stream)
         if self.fused:  # residual stream ping-pong: qkv reads r2 and writes r, gate/up the reverse
             # projection + RoPE + KV append in one pass over the qkv weights
             x_in, res, res_out = (self.r, None, None) if l == 0 else (self.mlp, self.r2, self.r)
@@ -292,6 +302,8 @@ class DecodeEngine:
             self.voff.append(self.qkv, sh.n_q_heads, self.seq_len, l)
             if variant in ("plain", "calib"):  # this layer's predicted V blocks must have arrived
                 torch.cuda.current_stream().wait_event(self.pf_events[l])
+        if warm:
+            torch.cuda.current_stream().wait_stream(self.warm_stream)
         if l < self.dense_layers:
             variant = "dense"  # layer-skip policy
         kw = self._map_kw(l) if variant != "dense" else {}
@@ -482,6 +494,8 @@ class DecodeEngine:
         # gemv x4 (qkv+rope fused) | rmsnorm x2, rope_append, silu_mul (+ 4 ap_gemm_tc at batch 5..16)
         per_layer = 4 if self.fused else 2 + 1 + 1 + (4 if self.tc else 0)
         att = {"dense": 1, "first": 1, "plain": 1, "calib": 2}[variant]
+        if self.l2_warm and self.voff is None and variant in ("plain", "calib"):
+            att += 1  # the L2 warm-up launch
         att_total = self.dense_layers + (L - self.dense_layers) * att
         sel = 2 if (self.sel is not None and variant != "dense") else 0
         off = 0
