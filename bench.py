@@ -69,7 +69,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=16, help="reference map-steps timed for cpu_baseline")
     ap.add_argument("--total-seqs", type=int, default=0,
                     help="cfg5: this many sequences in total, sharded over the ranks by seq_shard (0: --batch per GPU)")
-    ap.add_argument("--no-l2-warm", action="store_true", help="disable the sparse pass's L2 warm-up side stream")
+    ap.add_argument("--l2-warm", action="store_true", help="sparse pass L2 warm-up side stream (measured slower)")
     ap.add_argument("--parity-maps", type=int, default=8, help="maps re-checked against the CPU oracle after the run")
     ap.add_argument("--parity-steps", type=int, default=3, help="decode steps of the in-run parity check")
     ap.add_argument("--dense-layers", type=int, default=0,
@@ -554,7 +554,7 @@ def run_ours(args, rank, world):
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
                        precision=args.precision, seed=rank if split is None else 0, offload_v=args.offload,
                        head_split=split, dense_layers=args.dense_layers, gemm=args.gemm,
-                       l2_warm=not args.no_l2_warm)
+                       l2_warm=args.l2_warm)
     units = world if split is None else 1  # replicas: every rank decodes its own sequences
     eng.init_history()
     first_token(eng)

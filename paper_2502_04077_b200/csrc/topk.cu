@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
     }
 }
 
-// Warp-per-map variant for rows of <= 32 * IPT blocks (W = 2049 at 32K needs IPT 72): lane l owns blocks
+// Warp-per-map variant (opt-in, slower: see launch_sel_topk) for rows of <= 32 * IPT blocks (W = 2049 at 32K needs IPT 72): lane l owns blocks
 // q * 32 + l, so a ballot over one q covers 32 consecutive blocks — exactly one word of the bitmask and
 // a run of ascending ids.  The k-th largest key comes from a 32-step binary search on the key bits (a
 // warp reduction per step, no CTA barriers); ties are ranked by ballots in index order.  Same results
@@ -475,8 +475,10 @@ __global__ void __launch_bounds__(64) sel_topk_warp_kernel(ap_selector s, tie::P
 void launch_sel_topk(const ap_selector& s, const tie::Params& tp, cudaStream_t stream) {
     static int warp_form = -1;
     if (warp_form < 0) {
+        // opt-in (ATTNPRED_TOPK_KERNEL=warp): measured 27 us slower per 256-map launch at 32K than the
+        // CTA form (graph replay, scripts/dbg/forecast_knobs.py: 145.4 vs 118.8 us with the forecaster)
         const char* e = getenv("ATTNPRED_TOPK_KERNEL");
-        warp_form = !(e && strcmp(e, "cta") == 0);
+        warp_form = e && strcmp(e, "warp") == 0;
     }
     const unsigned wgrid = (unsigned)((s.n_maps + 1) / 2);
     if (warp_form && s.w_max <= 32 * 16) sel_topk_warp_kernel<16><<<wgrid, 64, 0, stream>>>(s, tp);
