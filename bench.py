@@ -360,6 +360,20 @@ def measure_e2e(eng, n, batch, world, units=None):
             "h2d_bytes_per_step": 8 * batch, "d2h_bytes_per_step": 8 * batch}
 
 
+def selector_in_step(eng, n=8):
+    """ap_sel_step as it runs inside the decode-step graph (external CUDA events around it in the
+    captured step, DecodeEngine(time_selector=True)): the last timed step's value, then n more steps
+    read one by one; median over the plain (non-calibration) steps."""
+    last = eng.selector_us()
+    plain = []
+    for _ in range(n):
+        v = eng.step()
+        us = eng.selector_us()
+        if v == "plain":
+            plain.append(us)
+    return statistics.median(plain) if plain else last, last
+
+
 def measure_selector(eng, reps=20):
     """Median CUDA-event time of the fused forecast + top-k (+ guard) launches (ap_sel_step) in their
     steady state on the engine's REAL data: one eager decode step without its selector call (the
@@ -551,10 +565,10 @@ def run_ours(args, rank, world):
         from paper_2502_04077_b200.distributed import HeadSplit
         split = HeadSplit(rank, world, shape.n_q_heads, shape.n_kv_heads)
         args.no_alt = True
-    eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 8, cfg=cfg, group=group,
+    eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 32, cfg=cfg, group=group,
                        precision=args.precision, seed=rank if split is None else 0, offload_v=args.offload,
                        head_split=split, dense_layers=args.dense_layers, gemm=args.gemm,
-                       l2_warm=args.l2_warm)
+                       l2_warm=args.l2_warm, time_selector=True)
     units = world if split is None else 1  # replicas: every rank decodes its own sequences
     eng.init_history()
     first_token(eng)
@@ -582,11 +596,17 @@ def run_ours(args, rank, world):
                 "frac": round(sb * args.steps / elapsed / 1e9 / peak, 4), "peak_kind": peak_kind,
                 "note": "algorithmic bytes of the whole decode step (weights once, selected KV, calibration K "
                         "share, history window) over the device-timed step"}
+    sel_last_us = eng.selector_us()  # ap_sel_step of the last timed step, read from the step graph
     e2e = measure_e2e(eng, args.steps, args.batch, world, units)
     tie_run = eng.sel.tie_stats()
     parity = inrun_parity(eng, args.parity_maps, args.parity_steps) if (rank == 0 and args.parity_maps > 0) else None
-    us, W = measure_selector(eng)
+    us_iso, W = measure_selector(eng)
+    us, _ = selector_in_step(eng)
     roofline = roofline_for(eng, args, us, W, f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
+    roofline["timing"] = ("median of ap_sel_step inside the captured decode-step graph (external CUDA events "
+                          "around it), plain steps after the timed region")
+    roofline["us_last_timed_step"] = round(sel_last_us, 2)
+    roofline["us_isolated_graph_l2_flushed"] = round(us_iso, 2)
 
     alt = None  # the other selection granularity on the same weights / KV
     if not args.no_alt and G > 1:
@@ -596,7 +616,8 @@ def run_ours(args, rank, world):
         for _ in range(args.warmup):
             eng.step()
         a_el, _ = timed_steps(eng, args.steps, world)
-        a_us, a_W = measure_selector(eng)
+        _, a_W = measure_selector(eng)
+        a_us, _ = selector_in_step(eng)
         alt = {"selection": other, "value": round(args.batch * args.steps * units / a_el, 2), "unit": "tok/s",
                "roofline": roofline_for(eng, args, a_us, a_W, f"{args.model}:{args.ctx}:{other}:{args.precision}")}
 

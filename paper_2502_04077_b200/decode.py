@@ -82,7 +82,7 @@ class DecodeEngine:
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
                  seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0,
                  fused: bool = True, gemm: str = "auto", attn_splits: tuple[int, int] | None = None,
-                 layer_budgets=None, l2_warm: bool = False):
+                 layer_budgets=None, l2_warm: bool = False, time_selector: bool = False):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -197,6 +197,11 @@ class DecodeEngine:
         # the per-layer fork/join measured 292 vs 311 tok/s at the headline shape
         self.l2_warm = l2_warm
         self.warm_stream = torch.cuda.Stream(device=dev)
+        # selector timing inside the step graph: external event record nodes around ap_sel_step
+        self.sel_ev = None
+        if time_selector:
+            self.sel_ev = (torch.cuda.Event(enable_timing=True, external=True),
+                           torch.cuda.Event(enable_timing=True, external=True))
         self.counter = 0  # selector step counter (host mirror; all maps move in lockstep)
         self.graphs = {}
         self._fill_kv(gen)
@@ -385,7 +390,16 @@ class DecodeEngine:
             _lib.check(_lib.fn("ap_argmax_rows")(_lib.ptr(self.logits), S, sh.vocab, _lib.ptr(self.argws),
                                                  self.argws.numel(), _lib.ptr(self.tok), s), "ap_argmax_rows")
         if selector and self.sel is not None and variant != "dense":
+            if self.sel_ev is not None:
+                self.sel_ev[0].record()
             self.sel.step()  # forecast + top-k for the next token, every layer and head at once
+            if self.sel_ev is not None:
+                self.sel_ev[1].record()
+
+    def selector_us(self) -> float:
+        """Duration of the last step's ap_sel_step launches (time_selector engines; synchronises)."""
+        self.sel_ev[1].synchronize()
+        return self.sel_ev[0].elapsed_time(self.sel_ev[1]) * 1e3
 
     def variant_for_next(self) -> str:
         if self.mode == "dense":
