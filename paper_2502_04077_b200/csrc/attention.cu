@@ -872,21 +872,32 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
     pdl_trigger();
     // Until pdl_wait: only data older than the previous kernel (positions, map state and selection,
     // the ring slot being replaced) — q and the newest K/V token come from the kernel just before.
-    const int64_t t = P.seq_len[s];
     const int b = P.block;
     const int map = s * P.maps_per_seq + P.map_base + g;
+    const int32_t* mid = P.sel.mid_blocks + (int64_t)map * (P.sel.k_mid > 0 ? P.sel.k_mid : 1);
+    // the map's whole middle-block row is fetched together with the position and the map state (one
+    // round trip instead of state -> ids), then sliced from shared memory
+    const int per_max = (((P.sel.sink + b - 1) / b + P.sel.local / b + 2 + P.sel.k_mid) + CL - 1) / CL;
+    int* s_mid = reinterpret_cast<int*>(sm_att + ATT_WARPS * NH * (HD + 2)) + per_max * (NH + 1);
+    const int mv = (int)threadIdx.x < P.sel.k_mid ? __ldg(mid + threadIdx.x) : 0;  // in flight with the two below
+    // 32-bit position arithmetic in the prologue (t < 2^31): 64-bit integer division is a ~100-cycle
+    // software routine, and the prologue sits on the critical path of every layer
+    const int t = P.seq_len[s];
     const ap_map_state ms = P.sel.state[map];
-    const int64_t sink_end = P.sel.sink < t ? P.sel.sink : t;
-    const int64_t local_start = t - P.sel.local > 0 ? t - P.sel.local : 0;
-    const int64_t sb = (sink_end + b - 1) / b;
-    const int64_t eb = (t + b - 1) / b;
-    int64_t lb = local_start / b;
+    if ((int)threadIdx.x < P.sel.k_mid) s_mid[threadIdx.x] = mv;
+    for (int i = threadIdx.x + ATT_THREADS; i < P.sel.k_mid; i += ATT_THREADS) s_mid[i] = mid[i];  // k_mid > 256
+    const int sink_end = P.sel.sink < t ? P.sel.sink : t;
+    const int local_start = t - P.sel.local > 0 ? t - P.sel.local : 0;
+    const int sb = (sink_end + b - 1) / b;
+    const int eb = (t + b - 1) / b;
+    int lb = local_start / b;
     if (lb < sb) lb = sb;
     const int n_local = (int)(eb - lb);
     const int n_units = (int)sb + n_local + ms.n_mid;
     const int per = (n_units + CL - 1) / CL;
     const int u0 = split * per, u1 = min(n_units, u0 + per);
-    const int32_t* mid = P.sel.mid_blocks + (int64_t)map * (P.sel.k_mid > 0 ? P.sel.k_mid : 1);
+    if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && g_att_trace_on)
+        g_att_trace[blockIdx.x * 16 + 12] = clock64() + (u1 & 0);  // after the state load is consumed
     const int h0 = g * NH;
     const int kvh = h0 / (P.n_q_heads / P.n_kv_heads);
     const __nv_bfloat16* kh = P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;
@@ -894,23 +905,28 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
     float* s_bm = sm_att + ATT_WARPS * NH * (HD + 2);  // [per][NH]
 
     const int Hh = P.sel.history;
-    const int slot = (int)(ms.n_pushed % Hh);
+    const int slot = (int)((uint32_t)ms.n_pushed % (uint32_t)Hh);  // n_pushed < 2^32
     float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
     const int64_t W = eb;
-    if constexpr (EMIT) {  // zero this CTA's share of the new row (and of [W, old width)), refilled after barrier 2
-        const int old_w = P.sel.slot_width[(int64_t)map * Hh + slot];
-        const int64_t Z = old_w > W ? old_w : W;
-        const int64_t z0 = Z * split / CL, z1 = Z * (split + 1) / CL;
-        for (int64_t j = z0 + threadIdx.x; j < z1; j += ATT_THREADS) dst[j] = 0.f;
+    ATT_TRACE(13);
+    if constexpr (EMIT) {  // zero this CTA's share of the whole ring row (rows are zero beyond their width;
+                           // no dependent read of the slot's old width), refilled after the exchange
+        const int Z = P.sel.w_max;
+        const int z0 = Z * split / CL, z1 = Z * (split + 1) / CL;
+        for (int j = z0 + threadIdx.x; j < z1; j += ATT_THREADS) dst[j] = 0.f;
         if (split == 0 && threadIdx.x == 0) P.sel.slot_xmax[(int64_t)map * Hh + slot] = 0.f;  // atomicMax'd later
     }
     // block id of each of this CTA's units (sink | local | middle), gathered once into shared memory
     int* s_blk = reinterpret_cast<int*>(s_bm + per * NH);
+    ATT_TRACE(9);
+    __syncthreads();  // s_mid landed
+    ATT_TRACE(10);
     for (int i = threadIdx.x; i < u1 - u0; i += ATT_THREADS) {
         const int u = u0 + i;
-        s_blk[i] = u < sb ? u : (u < sb + n_local ? (int)(lb + (u - sb)) : mid[u - sb - n_local]);
+        s_blk[i] = u < sb ? u : (u < sb + n_local ? (int)(lb + (u - sb)) : s_mid[u - sb - n_local]);
     }
     __syncthreads();
+    ATT_TRACE(11);
     auto block_of = [&](int u, bool& is_mid) -> int64_t {
         is_mid = u >= sb + n_local;
         return s_blk[u - u0];
@@ -935,7 +951,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
     // busy) with the blocks prefetched into L2 and no staging, so the kernel's small shared-memory
     // footprint lets the next projection's CTAs start on the same SMs.
     constexpr bool TC = NH >= 2;
-    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_blk + per) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(s_mid + P.sel.k_mid) + 1023) & ~uintptr_t(1023));
     uint8_t* my_ring = ring + warp * 2 * KV_STAGE;
     __shared__ __align__(8) uint64_t s_kvbar[ATT_WARPS][2];
     if (TC && lane == 0) {
@@ -1153,7 +1169,8 @@ static void launch_dense(const AttnParams& P, bool with_v, bool emit, cudaStream
 template <int NH, bool EMIT, int CL>
 static int launch_cluster(const AttnParams& P, cudaStream_t st) {
     const int units_max = (P.sel.sink + P.block - 1) / P.block + P.sel.local / P.block + 2 + P.sel.k_mid;
-    const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * (NH + 1)) * sizeof(float) +
+    const size_t sm = ((size_t)ATT_WARPS * NH * (HD + 2) + (size_t)((units_max + CL - 1) / CL) * (NH + 1) +
+                       (size_t)P.sel.k_mid) * sizeof(float) +
                       (NH >= 2 ? 1024 + (size_t)ATT_WARPS * 2 * KV_STAGE : 0);  // + the K/V staging rings (128 KB)
     auto k = sparse_cluster_kernel<NH, EMIT, CL>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -31,8 +31,8 @@ for it in range(4):
     torch.cuda.synchronize()
 buf = (ctypes.c_longlong * 256)()
 L.ap_attn_debug_trace(0, buf)
-a = np.array(buf, dtype=np.int64).reshape(16, 16)[:, :9]
-names = ["entry", "pre_pdl", "post_pdl", "blocks_done", "merged", "sync1", "final", "emitted", "exit"]
+a = np.array(buf, dtype=np.int64).reshape(16, 16)[:, :14]
+names = ["entry", "pre_pdl", "post_pdl", "blocks_done", "merged", "sync1", "final", "emitted", "exit", "loads_issued", "mid_landed", "blk_ready", "state_used", "slot"]
 t0 = a[a > 0].min()
 print("rank " + " ".join(f"{n:>11s}" for n in names))
 for r in range(16):
