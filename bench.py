@@ -455,6 +455,50 @@ def inrun_parity(eng, n_maps: int, n_steps: int):
                     "forward + mask + topk vs the device's middle blocks"}
 
 
+def engine_recovery(eng, n_heads=4):
+    """recovery_rate (evaluation.py:70-81) of the engine's REAL selections: one eager decode step
+    without its selector call (so the selection in force is the one its sparse pass used), then for
+    the last layer's first selection map: the dense float64 softmax row of each of its q-heads (q and K
+    from the device), the fraction of its mass on the selected tokens (sink | local | middle blocks,
+    selector.py:149) and on the best B tokens of that row (select_oracle, baselines.py:154-157); the
+    ratio is the reference's prediction accuracy for that row (evaluation.py:172-175)."""
+    import numpy as np
+    import torch
+    from oracle import hotpath as O
+    v = eng.variant_for_next()
+    eng._step_body(v, selector=False)
+    torch.cuda.synchronize()
+    l = eng.shape.n_layers - 1
+    cfg, sel = eng.cfg, eng.sel
+    m = (l - eng.dense_layers) * eng.maps_per_layer  # sequence 0, first map of the layer
+    st = sel.states()[m]
+    t = int(eng.seq_len[0].item())
+    mids = sel.mid_blocks[m, : int(st["n_mid"])].cpu().tolist()
+    S = set(range(min(cfg.sink_tokens, t))) | set(range(max(0, t - cfg.local_tokens), t))
+    S |= {p for p in O.expand_indices(mids, cfg.block_size, t) if p < int(st["mid_clip"])}
+    G = eng.shape.n_q_heads // eng.shape.n_kv_heads
+    kvh = (m % eng.maps_per_layer) * eng.group // G
+    K = eng.k_cache[l, 0, kvh, :t].float().cpu().numpy().astype(np.float64)
+    out = []
+    for h in range(min(n_heads, eng.group)):
+        q = eng.q[0, (m % eng.maps_per_layer) * eng.group + h].float().cpu().numpy().astype(np.float64)
+        z = K @ q / np.sqrt(q.size)
+        a = np.exp(z - z.max())
+        a /= a.sum()
+        got = O.recovery_rate(a, S)
+        best = O.recovery_rate(a, O.topk(a, min(cfg.budget, t)))
+        out.append((got, best))
+    eng.sel.step()  # complete the step (forecast for the next token) so the engine stays consistent
+    eng.counter += 1
+    got = float(np.mean([g for g, _ in out]))
+    best = float(np.mean([b for _, b in out]))
+    return {"layer": l, "map": m, "q_heads": len(out), "t": t, "selected_tokens": len(S),
+            "recovery_pct": round(100 * got, 3), "oracle_best_recovery_pct": round(100 * best, 3),
+            "accuracy_pct": round(100 * got / best, 2) if best > 0 else None,
+            "note": "random-init weights and N(0,1) keys give diffuse attention rows; this checks the plumbing "
+                    "of the engine's selections, the trained-forecaster quality is the cfg1 line's accuracy"}
+
+
 def roofline_for(eng, args, us, W, key):
     cfg = eng.cfg
     n_maps = eng.sel.n_maps
@@ -600,6 +644,7 @@ def run_ours(args, rank, world):
     e2e = measure_e2e(eng, args.steps, args.batch, world, units)
     tie_run = eng.sel.tie_stats()
     parity = inrun_parity(eng, args.parity_maps, args.parity_steps) if (rank == 0 and args.parity_maps > 0) else None
+    recovery = engine_recovery(eng) if (rank == 0 and args.parity_maps > 0 and eng.voff is None) else None
     us_iso, W = measure_selector(eng)
     us, _ = selector_in_step(eng)
     roofline = roofline_for(eng, args, us, W, f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
@@ -673,7 +718,7 @@ def run_ours(args, rank, world):
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "step_hbm": step_hbm, "cpu_baseline": cpu,
-        "alt_selection": alt, "prefetch": prefetch, "parity": parity,
+        "alt_selection": alt, "prefetch": prefetch, "parity": parity, "recovery": recovery,
         "tie_guard": dict(tie_run, steps=2 * args.steps + args.warmup + 1,
                           note="cumulative over warm-up, timed and e2e steps: maps whose top-k boundary was "
                                "ambiguous within the guard band and was re-scored in fp64"),
