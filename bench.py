@@ -495,8 +495,10 @@ def engine_recovery(eng, n_heads=4):
     return {"layer": l, "map": m, "q_heads": len(out), "t": t, "selected_tokens": len(S),
             "recovery_pct": round(100 * got, 3), "oracle_best_recovery_pct": round(100 * best, 3),
             "accuracy_pct": round(100 * got / best, 2) if best > 0 else None,
-            "note": "random-init weights and N(0,1) keys give diffuse attention rows; this checks the plumbing "
-                    "of the engine's selections, the trained-forecaster quality is the cfg1 line's accuracy"}
+            "chance_pct": round(100 * len(S) / t, 3),  # expected recovery of |S| tokens drawn at random
+            "note": "untrained forecaster (init_weights(0)) on a random-init model with N(0,1) keys: the "
+                    "selections recover about chance; this checks the plumbing of the engine's selections "
+                    "(the forecaster's accuracy on structured maps is the cfg1 line's accuracy_pct)"}
 
 
 def roofline_for(eng, args, us, W, key):
