@@ -413,6 +413,9 @@ def measure_selector(eng, reps=20):
     return us, W
 
 
+PARITY_TOL = {"fp32": (1e-3, 1e-2), "fp16x3": (1e-3, 1e-2), "fp16": (2e-2, 1e-1)}  # (rtol, floor): tests/parity.py
+
+
 def inrun_parity(eng, n_maps: int, n_steps: int):
     """After the timed run: for n_steps more decode steps, copy n_maps sampled maps' history windows
     (the rows the engine's attention kernels emitted) to the host and re-run the CPU oracle on them
@@ -429,7 +432,8 @@ def inrun_parity(eng, n_maps: int, n_steps: int):
     w = O.Weights.from_flat(eng.pweights.flat().astype(np.float32).astype(np.float64))
     rng = np.random.default_rng(7)
     picks = sorted(rng.choice(sel.n_maps, size=min(n_maps, sel.n_maps), replace=False).tolist())
-    mism, checked, worst = 0, 0, 0.0
+    mism, checked, worst, exempt, tie_steps = 0, 0, 0.0, 0, 0
+    rtol, flo = PARITY_TOL[sel.precision]
     for _ in range(n_steps):
         eng.step()
         import torch
@@ -445,11 +449,21 @@ def inrun_parity(eng, n_maps: int, n_steps: int):
             avail = int(np.count_nonzero(masked > -np.inf))
             want = sorted(O.topk(masked, min(ocfg.middle_blocks, avail)))
             got = sel.middle(m)
-            mism += got != want
-            floor = np.abs(pred).max() * 1e-2
-            worst = max(worst, float(np.max(np.abs(scores[m, :W] - pred) / (1e-3 * np.maximum(np.abs(pred), floor)))))
+            if got != want:  # a near tie within the precision's tolerance is an exemption, anything else a mismatch
+                fin = np.sort(masked[np.isfinite(masked)])[::-1]
+                kth = fin[len(want) - 1]
+                tol = rtol * max(abs(kth), flo * np.abs(fin).max())
+                diff = set(got) ^ set(want)
+                if all(abs(masked[j] - kth) <= tol for j in diff):
+                    exempt += len(diff)
+                    tie_steps += 1
+                else:
+                    mism += 1
+            floor = np.abs(pred).max() * flo
+            worst = max(worst, float(np.max(np.abs(scores[m, :W] - pred) / (rtol * np.maximum(np.abs(pred), floor)))))
             checked += 1
-    return {"maps": len(picks), "steps": n_steps, "map_steps": checked, "mismatches": int(mism), "exemptions": 0,
+    return {"maps": len(picks), "steps": n_steps, "map_steps": checked, "mismatches": int(mism),
+            "exemptions": int(exempt), "near_tie_map_steps": int(tie_steps), "precision": sel.precision,
             "worst_forecast_err_over_bound": round(worst, 4),
             "what": "engine-emitted history windows (sparse_renorm rows, calibration rows) -> CPU oracle "
                     "forward + mask + topk vs the device's middle blocks"}
@@ -526,7 +540,7 @@ def roofline_for(eng, args, us, W, key):
             "algorithmic_bytes_per_launch": b_alg,
             "tensor": {"algorithmic_flops_per_launch": f_inc, "achieved": round(tflops, 1), "peak": tf_peak,
                        "unit": "TFLOP/s", "frac": round(tflops / tf_peak, 4),
-                       "issued_frac_fp16x3": round(3 * tflops / tf_peak, 4) if args.precision == "fp16x3" else None}}
+                       "issued_frac_fp16x3": round(3 * tflops / tf_peak, 4) if eng.sel.precision == "fp16x3" else None}}
 
 
 def offload_extras(eng, args, shape, cfg, group, rank, units, elapsed, prefetch):
@@ -680,6 +694,22 @@ def run_ours(args, rank, world):
         d_elapsed, _ = timed_steps(eng, d_steps, world)
         dense = args.batch * d_steps * units / d_elapsed
 
+    fp16 = None  # the single-MMA fp16 forecaster (no exact-boundary guard): its speed and its counted exemptions
+    if not args.no_alt and args.precision != "fp16" and not args.offload:
+        eng.set_selection(group, precision="fp16")
+        first_token(eng)
+        for _ in range(args.warmup):
+            eng.step()
+        f_el, _ = timed_steps(eng, args.steps, world)
+        f_us, _ = selector_in_step(eng)
+        _, f_W = measure_selector(eng, reps=3)
+        f_par = inrun_parity(eng, args.parity_maps, args.parity_steps) if (rank == 0 and args.parity_maps > 0) else None
+        fp16 = {"precision": "fp16", "value": round(args.batch * args.steps * units / f_el, 2), "unit": "tok/s",
+                "roofline": roofline_for(eng, args, f_us, f_W, f"{args.model}:{args.ctx}:{args.group}:fp16"),
+                "parity": f_par,
+                "note": "one fp16 MMA per tap (11-bit operands, rtol 2e-2): 3x fewer MMAs than fp16x3, no guard, so "
+                        "selections may differ from the float64 reference at near ties (counted as exemptions)"}
+
     cpu = None
     if rank == 0 and world == 1:
         R = measure_reference(args.ctx, args.budget, 1, args.cpu_sample)
@@ -720,7 +750,7 @@ def run_ours(args, rank, world):
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "step_hbm": step_hbm, "cpu_baseline": cpu,
-        "alt_selection": alt, "prefetch": prefetch, "parity": parity, "recovery": recovery,
+        "alt_selection": alt, "fp16_forecaster": fp16, "prefetch": prefetch, "parity": parity, "recovery": recovery,
         "tie_guard": dict(tie_run, steps=2 * args.steps + args.warmup + 1,
                           note="cumulative over warm-up, timed and e2e steps: maps whose top-k boundary was "
                                "ambiguous within the guard band and was re-scored in fp64"),
