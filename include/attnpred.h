@@ -192,6 +192,9 @@ int ap_sel_tie_stats(const int32_t* tie_ws, int32_t* host_out3);
  * ATTNPRED_TIE_REL / ATTNPRED_TIE_FLOOR).  Applies to later ap_sel_step calls (graphs keep the
  * values they were captured with). */
 int ap_sel_set_tie_guard(int enabled, float rel, float floor_frac);
+/* [host] the guard band of the single-MMA fp16 forecaster (AP_PREC_F16; default rel 0 = no guard,
+ * env ATTNPRED_TIE_F16_REL / ATTNPRED_TIE_F16_FLOOR). */
+int ap_sel_set_tie_guard_f16(float rel, float floor_frac);
 
 /* Number of persistent CTAs the predictor kernels use (for reporting). */
 int ap_sel_grid_ctas(int precision);

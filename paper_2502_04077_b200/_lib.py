@@ -115,6 +115,7 @@ SIGNATURES = {
     "ap_sel_tie_ws_bytes": (ctypes.c_int64, [_I32]),
     "ap_sel_tie_stats": (ctypes.c_int, [_P, _P]),
     "ap_sel_set_tie_guard": (ctypes.c_int, [ctypes.c_int, ctypes.c_float, ctypes.c_float]),
+    "ap_sel_set_tie_guard_f16": (ctypes.c_int, [ctypes.c_float, ctypes.c_float]),
     "ap_attn_dense": (ctypes.c_int, [ctypes.POINTER(AttnLayerDesc), ctypes.c_int, ctypes.POINTER(Selector),
                                      _I32, _I32, _I32, ctypes.c_int, _P]),
     "ap_attn_set_calib_kernel": (ctypes.c_int, [ctypes.c_int]),

@@ -752,6 +752,8 @@ void launch_sel_topk(const ap_selector& s, const tie::Params& tp, cudaStream_t s
 // tests/test_gpu_parity_32k.py); ATTNPRED_TIE_REL / ATTNPRED_TIE_FLOOR override it.
 static int g_tie_on = -1;
 static float g_tie_rel = 0.f, g_tie_floor = 0.f;
+// the single-MMA fp16 forecaster (11-bit operands) needs a ~100x wider band; 0 = no guard for fp16
+static float g_tie16_rel = 0.f, g_tie16_floor = 0.f;
 
 static void tie_init() {
     if (g_tie_on >= 0) return;
@@ -761,6 +763,10 @@ static void tie_init() {
     const char* f = getenv("ATTNPRED_TIE_FLOOR");
     g_tie_rel = r ? (float)atof(r) : 3.0517578125e-5f;  // 2^-15
     g_tie_floor = f ? (float)atof(f) : 3.125e-2f;       // 2^-5
+    const char* r16 = getenv("ATTNPRED_TIE_F16_REL");
+    const char* f16 = getenv("ATTNPRED_TIE_F16_FLOOR");
+    g_tie16_rel = r16 ? (float)atof(r16) : 0.f;
+    g_tie16_floor = f16 ? (float)atof(f16) : 0.125f;
 }
 
 static tie::Params tie_params(int precision) {
@@ -773,9 +779,10 @@ static tie::Params tie_params(int precision) {
         if (cudaGetSymbolAddress(&p, g_wgen) == cudaSuccess) gen = static_cast<const int*>(p);
     }
     const int env_on = g_tie_on;
-    const float rel = g_tie_rel, flo = g_tie_floor;
+    const bool f16 = precision == AP_PREC_F16;
+    const float rel = f16 ? g_tie16_rel : g_tie_rel, flo = f16 ? g_tie16_floor : g_tie_floor;
     tie::Params tp;
-    tp.enabled = env_on && precision != AP_PREC_F16 && w != nullptr;
+    tp.enabled = env_on && w != nullptr && rel > 0.f;
     tp.rel = rel;
     tp.floor = flo;
     tp.w64 = w;
@@ -880,6 +887,14 @@ int ap_sel_set_tie_guard(int enabled, float rel, float floor_frac) {
     g_tie_on = enabled != 0;
     g_tie_rel = rel;
     g_tie_floor = floor_frac;
+    return AP_OK;
+}
+
+int ap_sel_set_tie_guard_f16(float rel, float floor_frac) {
+    AP_REQUIRE(rel >= 0.f && floor_frac >= 0.f, AP_EPARAM, "tie band parameters must be non-negative");
+    tie_init();
+    g_tie16_rel = rel;
+    g_tie16_floor = floor_frac;
     return AP_OK;
 }
 
