@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
     __shared__ int hist[256];
     __shared__ int scan_tmp[NT / 32 + 2];
     __shared__ int s_nan, s_amax, s_bcast;
+    __shared__ unsigned s_kmn, s_kmx;  // key range of the unmasked blocks
     const int m = blockIdx.x;
     ap_map_state st = s.state[m];
     const bool update = (st.counter % s.update_interval) == 0;
@@ -239,6 +240,8 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
     if (threadIdx.x == 0) {
         s_nan = 0;
         s_amax = 0;
+        s_kmn = 0xffffffffu;
+        s_kmx = 0u;
     }
     __syncthreads();
     int count = st.n_mid;
@@ -274,6 +277,21 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
         }
         if (nan) s_nan = 1;
         atomicMax(&s_amax, __float_as_int(amax));  // non-negative floats order as ints
+        {
+            unsigned kmn = 0xffffffffu, kmx = 0u;
+#pragma unroll
+            for (int q = 0; q < IPT; ++q)
+                if (key[q]) {
+                    kmn = min(kmn, key[q]);
+                    kmx = max(kmx, key[q]);
+                }
+            kmn = __reduce_min_sync(0xffffffffu, kmn);
+            kmx = __reduce_max_sync(0xffffffffu, kmx);
+            if ((threadIdx.x & 31) == 0) {
+                atomicMin(&s_kmn, kmn);
+                atomicMax(&s_kmx, kmx);
+            }
+        }
         int n_masked = 0;
         block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
         if (s_nan) raise_status(s.status, AP_ENUMERIC);
@@ -283,17 +301,28 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
         const int k = kcap < available ? kcap : available;
         for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
         if (k > 0) {
-            // radix select of the k-th largest key, 8 bits per pass
-            uint32_t prefix = 0, hi_mask = 0;
+            // radix select of the k-th largest key, 8 bits per pass.  Every unmasked key lies in [kmn, kmx],
+            // so the bytes above their highest differing bit are common: those passes are skipped.  Equal
+            // digits of a warp are counted with one atomic (match_any), not 32 serialised ones.
+            const uint32_t kmn = s_kmn, kmx = s_kmx;
+            const int top = (kmn ^ kmx) ? 31 - __clz(kmn ^ kmx) : -1;
+            const int first = top >= 0 ? top / 8 : -1;
+            uint32_t hi_mask = first >= 3 ? 0u : (0xffffffffu << ((first + 1) * 8));
+            uint32_t prefix = kmx & hi_mask;
             int remaining = k;
+            const int lane = threadIdx.x & 31;
 #pragma unroll 1
-            for (int pass = 3; pass >= 0; --pass) {
+            for (int pass = first; pass >= 0; --pass) {
                 const int shift = pass * 8;
                 for (int d = threadIdx.x; d < 256; d += NT) hist[d] = 0;
                 __syncthreads();
 #pragma unroll
-                for (int q = 0; q < IPT; ++q)
-                    if (((key[q] ^ prefix) & hi_mask) == 0) atomicAdd(&hist[(key[q] >> shift) & 0xFF], 1);
+                for (int q = 0; q < IPT; ++q) {
+                    const bool act = key[q] != 0u && ((key[q] ^ prefix) & hi_mask) == 0;
+                    const unsigned d = (key[q] >> shift) & 0xFFu;
+                    const unsigned grp = __match_any_sync(0xffffffffu, act ? d : 0x100u + lane);
+                    if (act && lane == __ffs(grp) - 1) atomicAdd(&hist[d], __popc(grp));
+                }
                 __syncthreads();
                 const int c = threadIdx.x < 256 ? hist[255 - threadIdx.x] : 0;
                 int total = 0;
