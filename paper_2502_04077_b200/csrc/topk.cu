@@ -302,27 +302,22 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
         for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
         if (k > 0) {
             // radix select of the k-th largest key, 8 bits per pass.  Every unmasked key lies in [kmn, kmx],
-            // so the bytes above their highest differing bit are common: those passes are skipped.  Equal
-            // digits of a warp are counted with one atomic (match_any), not 32 serialised ones.
+            // so the bytes above their highest differing bit are common: those passes are skipped.
+            // (Warp-aggregating equal digits with __match_any_sync measured slower: 147.5 vs 118.8 us.)
             const uint32_t kmn = s_kmn, kmx = s_kmx;
             const int top = (kmn ^ kmx) ? 31 - __clz(kmn ^ kmx) : -1;
             const int first = top >= 0 ? top / 8 : -1;
             uint32_t hi_mask = first >= 3 ? 0u : (0xffffffffu << ((first + 1) * 8));
             uint32_t prefix = kmx & hi_mask;
             int remaining = k;
-            const int lane = threadIdx.x & 31;
 #pragma unroll 1
             for (int pass = first; pass >= 0; --pass) {
                 const int shift = pass * 8;
                 for (int d = threadIdx.x; d < 256; d += NT) hist[d] = 0;
                 __syncthreads();
 #pragma unroll
-                for (int q = 0; q < IPT; ++q) {
-                    const bool act = key[q] != 0u && ((key[q] ^ prefix) & hi_mask) == 0;
-                    const unsigned d = (key[q] >> shift) & 0xFFu;
-                    const unsigned grp = __match_any_sync(0xffffffffu, act ? d : 0x100u + lane);
-                    if (act && lane == __ffs(grp) - 1) atomicAdd(&hist[d], __popc(grp));
-                }
+                for (int q = 0; q < IPT; ++q)
+                    if (key[q] != 0u && ((key[q] ^ prefix) & hi_mask) == 0) atomicAdd(&hist[(key[q] >> shift) & 0xFF], 1);
                 __syncthreads();
                 const int c = threadIdx.x < 256 ? hist[255 - threadIdx.x] : 0;
                 int total = 0;
