@@ -1100,7 +1100,7 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
         for (int r = 0; r < CL; ++r) s_w[h][r] = wr[r] / L;
     }
     __syncthreads();
-    if (threadIdx.x < HD) {  // rank r finalises q-heads r, r + CL, ... over the CL partials
+    if (threadIdx.x < HD) {  // warps 0-3: rank r finalises q-heads r, r + CL, ... over the CL partials
         for (int h = split; h < NH; h += CL) {
             float o = 0.f;
 #pragma unroll
@@ -1108,14 +1108,14 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
             P.out[((int64_t)s * P.n_q_heads + h0 + h) * HD + threadIdx.x] = __float2bfloat16_rn(o);
             if (threadIdx.x == 0 && P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = s_lse[h];
         }
-    }
-    ATT_TRACE(6);
-    if constexpr (EMIT) {
+        ATT_TRACE(6);
+    } else if constexpr (EMIT) {  // warps 4-7, concurrently: the compressed-row values of this CTA's units
+        const int et = threadIdx.x - HD;
         float lse[NH];
 #pragma unroll
         for (int h = 0; h < NH; ++h) lse[h] = s_lse[h];
         float mx = 0.f;
-        for (int u = u0 + threadIdx.x; u < u1; u += ATT_THREADS) {
+        for (int u = u0 + et; u < u1; u += ATT_THREADS - HD) {
             bool is_mid;
             const int64_t j = block_of(u, is_mid);
             float v = 0.f;
@@ -1127,17 +1127,17 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
             dst[j] = v;
             mx = track_row_max(mx, v, P.sel.status);
         }
-        mx = cta_max_nonneg(mx);
-        if (threadIdx.x == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && mx > 0.f)  // per warp (non-negative floats order as ints)
             atomicMax(reinterpret_cast<int*>(P.sel.slot_xmax + (int64_t)map * Hh + slot), __float_as_int(mx));
-            if (split == 0) {
-                ap_map_state st2 = ms;
-                P.sel.slot_width[(int64_t)map * Hh + slot] = (int32_t)W;
-                st2.n_pushed += 1;
-                st2.row_len = t;
-                st2.width = (int32_t)W;
-                P.sel.state[map] = st2;
-            }
+        if (split == 0 && et == 0) {
+            ap_map_state st2 = ms;
+            P.sel.slot_width[(int64_t)map * Hh + slot] = (int32_t)W;
+            st2.n_pushed += 1;
+            st2.row_len = t;
+            st2.width = (int32_t)W;
+            P.sel.state[map] = st2;
         }
     }
     ATT_TRACE(7);
