@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--total-seqs", type=int, default=0,
                     help="cfg5: this many sequences in total, sharded over the ranks by seq_shard (0: --batch per GPU)")
     ap.add_argument("--l2-warm", action="store_true", help="sparse pass L2 warm-up side stream (measured slower)")
+    ap.add_argument("--overlap-selector", type=int, default=0,
+                    help="batch 1: run each layer's selector step on this many reserved SMs beside the GEMVs")
     ap.add_argument("--parity-maps", type=int, default=8, help="maps re-checked against the CPU oracle after the run")
     ap.add_argument("--parity-steps", type=int, default=3, help="decode steps of the in-run parity check")
     ap.add_argument("--dense-layers", type=int, default=0,
@@ -628,7 +630,7 @@ def run_ours(args, rank, world):
     eng = DecodeEngine(shape, args.batch, args.ctx, max_new=2 * total_steps + 32, cfg=cfg, group=group,
                        precision=args.precision, seed=rank if split is None else 0, offload_v=args.offload,
                        head_split=split, dense_layers=args.dense_layers, gemm=args.gemm,
-                       l2_warm=args.l2_warm, time_selector=True)
+                       l2_warm=args.l2_warm, time_selector=True, overlap_selector=args.overlap_selector)
     units = world if split is None else 1  # replicas: every rank decodes its own sequences
     eng.init_history()
     first_token(eng)
@@ -656,17 +658,22 @@ def run_ours(args, rank, world):
                 "frac": round(sb * args.steps / elapsed / 1e9 / peak, 4), "peak_kind": peak_kind,
                 "note": "algorithmic bytes of the whole decode step (weights once, selected KV, calibration K "
                         "share, history window) over the device-timed step"}
-    sel_last_us = eng.selector_us()  # ap_sel_step of the last timed step, read from the step graph
+    sel_last_us = eng.selector_us() if eng.sel_ev is not None else None  # the last timed step's ap_sel_step
     e2e = measure_e2e(eng, args.steps, args.batch, world, units)
     tie_run = eng.sel.tie_stats()
     parity = inrun_parity(eng, args.parity_maps, args.parity_steps) if (rank == 0 and args.parity_maps > 0) else None
     recovery = engine_recovery(eng) if (rank == 0 and args.parity_maps > 0 and eng.voff is None) else None
     us_iso, W = measure_selector(eng)
-    us, _ = selector_in_step(eng)
+    if eng.sel_ev is not None:
+        us, _ = selector_in_step(eng)
+        timing = ("median of ap_sel_step inside the captured decode-step graph (external CUDA events around it), "
+                  "plain steps after the timed region")
+    else:  # overlap mode: per-layer steps on a side stream; time the all-layer launch on its own
+        us = us_iso
+        timing = "ap_sel_step over all maps in its own graph, L2 flushed (overlap mode steps it per layer)"
     roofline = roofline_for(eng, args, us, W, f"{args.model}:{args.ctx}:{args.group}:{args.precision}")
-    roofline["timing"] = ("median of ap_sel_step inside the captured decode-step graph (external CUDA events "
-                          "around it), plain steps after the timed region")
-    roofline["us_last_timed_step"] = round(sel_last_us, 2)
+    roofline["timing"] = timing
+    roofline["us_last_timed_step"] = None if sel_last_us is None else round(sel_last_us, 2)
     roofline["us_isolated_graph_l2_flushed"] = round(us_iso, 2)
 
     alt = None  # the other selection granularity on the same weights / KV
@@ -677,8 +684,8 @@ def run_ours(args, rank, world):
         for _ in range(args.warmup):
             eng.step()
         a_el, _ = timed_steps(eng, args.steps, world)
-        _, a_W = measure_selector(eng)
-        a_us, _ = selector_in_step(eng)
+        a_iso, a_W = measure_selector(eng)
+        a_us = selector_in_step(eng)[0] if eng.sel_ev is not None else a_iso
         alt = {"selection": other, "value": round(args.batch * args.steps * units / a_el, 2), "unit": "tok/s",
                "roofline": roofline_for(eng, args, a_us, a_W, f"{args.model}:{args.ctx}:{other}:{args.precision}")}
 
@@ -701,8 +708,8 @@ def run_ours(args, rank, world):
         for _ in range(args.warmup):
             eng.step()
         f_el, _ = timed_steps(eng, args.steps, world)
-        f_us, _ = selector_in_step(eng)
-        _, f_W = measure_selector(eng, reps=3)
+        f_iso, f_W = measure_selector(eng, reps=3)
+        f_us = selector_in_step(eng)[0] if eng.sel_ev is not None else f_iso
         f_par = inrun_parity(eng, args.parity_maps, args.parity_steps) if (rank == 0 and args.parity_maps > 0) else None
         fp16 = {"precision": "fp16", "value": round(args.batch * args.steps * units / f_el, 2), "unit": "tok/s",
                 "roofline": roofline_for(eng, args, f_us, f_W, f"{args.model}:{args.ctx}:{args.group}:fp16"),
@@ -747,6 +754,7 @@ def run_ours(args, rank, world):
                    "selection": {"kv": f"per KV head ({G} q-heads share a map)", "head": "per q-head"}[args.group],
                    "forecaster_precision": args.precision, "dense_layers": args.dense_layers,
                    "parallelism": f"replicas x{world}" if split is None else f"kv-head split x{world} + all-gather",
+                   "selector_overlap_sms": args.overlap_selector,
                    "steps_plain_vs_calibration": [plain, len(variants) - plain],
                    "l2": "working set ~20 GB (weights + KV) >> 126 MB L2; no flush needed"},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "step_hbm": step_hbm, "cpu_baseline": cpu,

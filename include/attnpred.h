@@ -60,6 +60,11 @@ int ap_version(void);
 const char* ap_last_error(void);
 /* [host] number of SMs of the current device (grid sizing in callers) */
 int ap_device_sm_count(void);
+/* [host] keep n SMs free of the persistent GEMV and calibration grids (their grids shrink to
+ * ap_sm_budget() = SMs - n) so a selector step on a side stream (ap_sel_step_grid with n CTAs) runs
+ * beside them; 0 (default) = every SM. */
+int ap_set_sm_reserve(int n);
+int ap_sm_budget(void);
 
 /* ---------------------------------------------------------------------------
  * Predictor weights — predictor.py:45-98 (PredictorWeights), APW1 order
@@ -182,6 +187,9 @@ int ap_sel_push_compressed(const ap_selector* s, const float* comp, int64_t comp
  * history window and ordered like selector.py:80, so the ids equal the
  * float64 reference's (per-map outcome in ap_map_state.tie_n). */
 int ap_sel_step(const ap_selector* s, int precision, void* stream);
+/* ap_sel_step with the persistent forecaster grid capped at grid_ctas CTAs (0 = one per SM) — for a
+ * selector step that runs on a few reserved SMs beside other kernels (ap_set_sm_reserve). */
+int ap_sel_step_grid(const ap_selector* s, int precision, int grid_ctas, void* stream);
 
 /* Bytes of the guard workspace for n_maps maps (zero it once before first use). */
 int64_t ap_sel_tie_ws_bytes(int32_t n_maps);

@@ -111,6 +111,9 @@ SIGNATURES = {
     "ap_sel_push_rows": (ctypes.c_int, [ctypes.POINTER(Selector), _P, ctypes.c_int, _I64, _I64, ctypes.c_int, _P]),
     "ap_sel_push_compressed": (ctypes.c_int, [ctypes.POINTER(Selector), _P, _I64, _I64, ctypes.c_int, _P]),
     "ap_sel_step": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.c_int, _P]),
+    "ap_sel_step_grid": (ctypes.c_int, [ctypes.POINTER(Selector), ctypes.c_int, ctypes.c_int, _P]),
+    "ap_set_sm_reserve": (ctypes.c_int, [ctypes.c_int]),
+    "ap_sm_budget": (ctypes.c_int, []),
     "ap_sel_grid_ctas": (ctypes.c_int, [ctypes.c_int]),
     "ap_sel_tie_ws_bytes": (ctypes.c_int64, [_I32]),
     "ap_sel_tie_stats": (ctypes.c_int, [_P, _P]),

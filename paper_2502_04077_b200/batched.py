@@ -123,6 +123,28 @@ class BatchedSelector:
         """selector.py:122-154 for every map: forecast + mask + top-k on update steps, then counter += 1."""
         self._call("ap_sel_step", _lib.PREC[self.precision], stream=stream)
 
+    def sub_desc(self, begin: int, count: int):
+        """A descriptor of maps [begin, begin + count) (same buffers, offset pointers; shared status and
+        guard workspace), for stepping one layer's maps on their own."""
+        if not (0 <= begin and count >= 1 and begin + count <= self.n_maps):
+            raise ParameterError("map range out of bounds")
+        d = _lib.Selector.from_buffer_copy(self._desc)
+        H, wm = self.cfg.history, self.w_max
+        words = (wm + 31) // 32
+        d.n_maps = count
+        for name, per_map in (("ring", 4 * H * wm), ("rmap", 4 * H * wm), ("rsum", 8 * wm), ("slot_width", 4 * H),
+                              ("slot_xmax", 4 * H), ("state", _STATE_DTYPE.itemsize), ("scores", 4 * wm),
+                              ("mid_blocks", 4 * max(self.k_mid, 1)), ("mid_mask", 4 * words), ("k_map", 4)):
+            base = getattr(d, name)
+            if base:
+                setattr(d, name, base + begin * per_map)
+        return d
+
+    def step_range(self, desc, grid_ctas: int = 0, stream=None) -> None:
+        """ap_sel_step_grid on a sub_desc(): the forecaster's persistent grid capped at grid_ctas CTAs."""
+        _lib.check(_lib.fn("ap_sel_step_grid")(ctypes.byref(desc), _lib.PREC[self.precision], int(grid_ctas),
+                                               _lib.stream_handle(stream)), "ap_sel_step_grid")
+
     # ------------------------------------------------------------ readback
     def states(self) -> np.ndarray:
         return self.state.cpu().numpy().view(_STATE_DTYPE)

@@ -1583,7 +1583,7 @@ static int launch(AttnParams P, cudaStream_t st) {
     auto k = calib_tc_kernel<NH>;
     // splits: one wave of one CTA per SM over the whole (KV head, sequence) grid (the splits of a KV
     // head wait for each other once, so they must all be resident)
-    int splits = ap_device_sm_count() / (P.n_kv_heads * P.n_seq);
+    int splits = ap_sm_budget() / (P.n_kv_heads * P.n_seq);  // every split resident: not on reserved SMs
     AP_REQUIRE(splits >= 1, AP_EPARAM, "calibration pass: more (sequence, KV head) pairs than SMs");
     splits = splits > P.n_splits ? P.n_splits : splits;
     P.n_splits = splits;

@@ -49,4 +49,21 @@ int ap_device_sm_count(void) {
     return n;
 }
 
+static int g_sm_reserve = 0;
+
+int ap_set_sm_reserve(int n) {
+    const int sms = ap_device_sm_count();
+    if (n < 0 || (sms > 0 && n >= sms)) {
+        ap::set_last_error("ap_set_sm_reserve: %d SMs cannot be reserved (device has %d)", n, sms);
+        return AP_EPARAM;
+    }
+    g_sm_reserve = n;
+    return AP_OK;
+}
+
+int ap_sm_budget(void) {
+    const int n = ap_device_sm_count() - g_sm_reserve;
+    return n < 1 ? 1 : n;
+}
+
 }  // extern "C"

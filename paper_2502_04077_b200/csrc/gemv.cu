@@ -387,7 +387,7 @@ int launch(Params P, cudaStream_t st) {
     const int units = paired(EPI) ? P.N / 2 : P.N;
     const int per_group = paired(EPI) ? GROUP / 2 : GROUP;
     int grid = (units + per_group - 1) / per_group;
-    const int sms = ap_device_sm_count();
+    const int sms = ap_sm_budget();  // the SMs not reserved for a concurrent selector step
     grid = grid < sms ? grid : sms;
     auto k = gemv_stream_kernel<NS, PRO, EPI>;
     static bool attr_set = false;

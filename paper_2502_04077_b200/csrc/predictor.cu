@@ -689,7 +689,7 @@ static int tc_kernel() {
     return v;
 }
 
-static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
+static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st, int grid_cap = 0) {
     ConvParams P = Pin;
     {
         static int dbg = -1;
@@ -699,8 +699,9 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st) {
         }
         P.debug = dbg;
     }
-    const int n_tasks = P.n_maps * P.n_chunks;
+    int n_tasks = P.n_maps * P.n_chunks;
     if (n_tasks == 0) return AP_OK;
+    if (grid_cap > 0 && grid_cap < n_tasks) n_tasks = grid_cap;  // (only used below to cap the grid)
     switch (precision) {
         case AP_PREC_FP32: {
             int g = grid_ctas<AP_PREC_FP32>();
@@ -836,7 +837,16 @@ int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W
     return launch_conv(P, precision, as_stream(stream));
 }
 
-int ap_sel_step(const ap_selector* s, int precision, void* stream) {
+static int sel_step_impl(const ap_selector* s, int precision, int grid_cap, void* stream);
+
+int ap_sel_step(const ap_selector* s, int precision, void* stream) { return sel_step_impl(s, precision, 0, stream); }
+
+int ap_sel_step_grid(const ap_selector* s, int precision, int grid_ctas, void* stream) {
+    AP_REQUIRE(grid_ctas >= 0, AP_EPARAM, "grid_ctas must be >= 0");
+    return sel_step_impl(s, precision, grid_ctas, stream);
+}
+
+static int sel_step_impl(const ap_selector* s, int precision, int grid_cap, void* stream) {
     AP_REQUIRE(s && s->n_maps > 0, AP_EPARAM, "bad selector descriptor");
     AP_REQUIRE(s->w_max % 4 == 0, AP_EPARAM, "w_max must be a multiple of 4 (16-byte rows for the bulk copies)");
     AP_REQUIRE(s->update_interval >= 1 && s->calib_period >= 1, AP_ECONFIG, "bad selector config");
@@ -860,7 +870,7 @@ int ap_sel_step(const ap_selector* s, int precision, void* stream) {
         P.update_interval = s->update_interval;
         P.k_mid = s->k_mid;
         P.status = s->status;
-        int rc = launch_conv(P, precision, st);
+        int rc = launch_conv(P, precision, st, grid_cap);
         if (rc != AP_OK) return rc;
     }
     launch_sel_topk(*s, tie_params(precision), st);

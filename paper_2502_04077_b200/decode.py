@@ -82,7 +82,8 @@ class DecodeEngine:
                  cfg=None, weights: PredictorWeights | None = None, group: int = 1, precision: str = "fp16x3",
                  seed: int = 0, offload_v: bool = False, head_split=None, dense_layers: int = 0,
                  fused: bool = True, gemm: str = "auto", attn_splits: tuple[int, int] | None = None,
-                 layer_budgets=None, l2_warm: bool = False, time_selector: bool = False):
+                 layer_budgets=None, l2_warm: bool = False, time_selector: bool = False,
+                 overlap_selector: int = 0):
         torch = D.torch()
         if mode not in ("sparse", "dense"):
             raise ConfigError("mode must be 'sparse' or 'dense'")
@@ -197,11 +198,24 @@ class DecodeEngine:
         # the per-layer fork/join measured 292 vs 311 tok/s at the headline shape
         self.l2_warm = l2_warm
         self.warm_stream = torch.cuda.Stream(device=dev)
+        # overlap_selector = R > 0: each layer's selector step (forecast + top-k for the next token) runs on
+        # a side stream right after that layer's attention, on R SMs kept free of the GEMV / calibration
+        # grids (ap_set_sm_reserve), instead of once for all layers at the end of the token
+        self.overlap = int(overlap_selector)
+        self.sel_stream = torch.cuda.Stream(device=dev) if self.overlap else None
+        self._sub = None
+        if self.overlap:
+            if mode != "sparse" or n_seq != 1 or offload_v or self.split is not None:
+                raise ConfigError("overlap_selector needs the resident sparse path at batch 1 (one layer's maps "
+                                  "contiguous)")
+            if not 0 < self.overlap < sms:
+                raise ConfigError("overlap_selector must reserve between 1 and SMs-1 SMs")
         # selector timing inside the step graph: external event record nodes around ap_sel_step
         self.sel_ev = None
-        if time_selector:
+        if time_selector and not self.overlap:
             self.sel_ev = (torch.cuda.Event(enable_timing=True, external=True),
                            torch.cuda.Event(enable_timing=True, external=True))
+        self._overlap_now = False
         self.counter = 0  # selector step counter (host mirror; all maps move in lockstep)
         self.graphs = {}
         self._fill_kv(gen)
@@ -262,6 +276,14 @@ class DecodeEngine:
         if lb.shape != (self.sel_layers,):
             raise ConfigError(f"layer_budgets needs one budget per sparse layer ({self.sel_layers})")
         return np.tile(np.repeat(lb, self.maps_per_layer), self.n_seq)
+
+    def _layer_sel(self, l: int):
+        """Sub-descriptor of layer l's selector maps (overlap mode)."""
+        if self._sub is None or self._sub[0] is not self.sel:
+            mpl = self.maps_per_layer
+            self._sub = (self.sel, {ll: self.sel.sub_desc((ll - self.dense_layers) * mpl, mpl)
+                                    for ll in range(self.dense_layers, self.shape.n_layers)})
+        return self._sub[1][l]
 
     def _map_kw(self, l: int) -> dict:
         """Selector map range of layer l (layers below dense_layers own none)."""
@@ -325,6 +347,9 @@ class DecodeEngine:
         else:
             self.att.sparse(self.q, kc, vc, self.seq_len, self.att_out, self.sel, emit=True, vpages=self.voff,
                             layer=l, **kw)
+        if self._overlap_now and l >= self.dense_layers:  # this layer's forecast + top-k beside the next GEMVs
+            self.sel_stream.wait_stream(torch.cuda.current_stream())
+            self.sel.step_range(self._layer_sel(l), grid_ctas=self.overlap, stream=self.sel_stream)
         if self.split is not None:  # one collective per layer: the heads' outputs over NVLink
             gather_heads_into(self.att_full, self.att_out, self.split)
         if self.fused:
@@ -365,6 +390,9 @@ class DecodeEngine:
         sh = self.shape
         S = self.n_seq
         s = _lib.stream_handle()
+        self._overlap_now = bool(self.overlap) and selector and variant in ("plain", "calib")
+        # GEMV / calibration grids leave the reserved SMs to the side-stream selector (captured with the graph)
+        _lib.check(_lib.fn("ap_set_sm_reserve")(self.overlap if self._overlap_now else 0), "ap_set_sm_reserve")
         _lib.check(_lib.fn("ap_advance")(_lib.ptr(self.seq_len), S, 1, s))
         main = torch.cuda.current_stream()
         if self.voff is not None and variant in ("plain", "calib"):
@@ -389,7 +417,10 @@ class DecodeEngine:
             self._mm(self.y, self.lm_head, self.logits)
             _lib.check(_lib.fn("ap_argmax_rows")(_lib.ptr(self.logits), S, sh.vocab, _lib.ptr(self.argws),
                                                  self.argws.numel(), _lib.ptr(self.tok), s), "ap_argmax_rows")
-        if selector and self.sel is not None and variant != "dense":
+        if self._overlap_now:
+            main.wait_stream(self.sel_stream)  # every layer's selector step has finished
+            _lib.check(_lib.fn("ap_set_sm_reserve")(0), "ap_set_sm_reserve")
+        elif selector and self.sel is not None and variant != "dense":
             if self.sel_ev is not None:
                 self.sel_ev[0].record()
             self.sel.step()  # forecast + top-k for the next token, every layer and head at once
@@ -512,7 +543,9 @@ class DecodeEngine:
         if self.l2_warm and self.voff is None and variant in ("plain", "calib"):
             att += 1  # the L2 warm-up launch
         att_total = self.dense_layers + (L - self.dense_layers) * att
-        sel = 2 if (self.sel is not None and variant != "dense") else 0
+        sel = 3 if (self.sel is not None and variant != "dense") else 0  # forecast, top-k, guard refine
+        if self.overlap and variant in ("plain", "calib"):
+            sel *= self.sel_layers  # one selector step per layer
         off = 0
         if self.voff is not None:
             off = L * (1 + (1 if variant in ("plain", "calib") else 0))  # v_append (+ prefetch) per layer

@@ -69,3 +69,24 @@ def test_layer_skip_config_errors():
         DecodeEngine(TINY, 1, CTX, 8, dense_layers=TINY.n_layers)
     with pytest.raises(ConfigError):
         DecodeEngine(TINY, 1, CTX, 8, dense_layers=1, offload_v=True, group=2)
+
+
+@pytest.mark.gpu
+def test_overlapped_selector_equals_end_of_token_step():
+    """overlap_selector: each layer's selector step on a side stream (reserved SMs) right after the
+    layer's attention gives the same selections, hence the same logits, as one step for all layers at
+    the end of the token."""
+    import torch
+    cfg = SelectorConfig(budget=256, calibration_period=3)
+    _, base, _ = _run("sparse", group=2, cfg=cfg, use_graph=True)
+    eng = DecodeEngine(TINY, 1, CTX, max_new=STEPS + 4, cfg=cfg, group=2, seed=3, overlap_selector=8)
+    eng.init_history()
+    ref = DecodeEngine(TINY, 1, CTX, max_new=STEPS + 4, cfg=cfg, group=2, seed=3)
+    ref.init_history()
+    for _ in range(STEPS):
+        eng.step()
+        ref.step()
+        torch.cuda.synchronize()
+        assert torch.equal(eng.sel.mid_blocks, ref.sel.mid_blocks)
+        assert torch.equal(eng.logits, ref.logits)
+    assert eng.sel.n_maps == TINY.n_layers * 2
