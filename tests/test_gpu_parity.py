@@ -257,3 +257,37 @@ def test_batched_selector_cfg1_shape(pkg, precision):
     if precision != "fp16":  # fp32-class modes: the exact-boundary guard leaves no near-tie flips
         assert not diverged and exempt == 0, f"{len(diverged)} maps diverged ({exempt} near-tie blocks)"
     print(f"batched {precision}: near-tie exemptions = {exempt} over {n_maps} maps x {steps} steps")
+
+
+def test_weight_change_invalidates_incremental_rows(pkg):
+    """ap_set_weights bumps a weight generation: a map whose r-map rows were built under other weights
+    recomputes them in full at its next update (otherwise the incremental form would mix weight sets)."""
+    import torch
+    from paper_2502_04077_b200.batched import PUSH_DENSE, PUSH_PREFILL, BatchedSelector
+    _, predictor, selector = pkg
+    rng = np.random.default_rng(31)
+    n_maps, t0 = 8, 1500
+    cfg = selector.SelectorConfig(budget=512)
+    ocfg = O.Config(budget=512)
+    wa = O.Weights.from_flat(O.init_weights(5).flat().astype(np.float32).astype(np.float64))
+    wb = O.Weights.from_flat(O.init_weights(6).flat().astype(np.float32).astype(np.float64))
+    prefill = [rng.dirichlet(np.full(t0 - 63 + i, 0.05), size=n_maps).astype(np.float32) for i in range(63)]
+    rows = [rng.dirichlet(np.full(t0 + s, 0.05), size=n_maps).astype(np.float32) for s in range(3)]
+    dev = BatchedSelector(cfg, n_maps, w_max=128)
+    for p in prefill:
+        dev.push_rows(torch.from_numpy(p).cuda(), p.shape[1], mode=PUSH_PREFILL)
+    ost = [O.init_state(ocfg, [p[m] for p in prefill]) for m in range(n_maps)]
+    osel = [None] * n_maps
+    for s, (w, r) in enumerate(zip((wa, wa, wb), rows)):  # the third step runs under other weights
+        predictor.install_weights(predictor.PredictorWeights.from_flat(w.flat()))
+        dev.push_rows(torch.from_numpy(r).cuda(), r.shape[1], mode=PUSH_DENSE)
+        dev.step()
+        dev.check_status()
+        scores = dev.scores.cpu().numpy()
+        for m in range(n_maps):
+            row = r[m].astype(np.float64)
+            obs = row if osel[m] is None else O.observed_from_selection(row, osel[m])
+            ost[m], osel[m] = O.step(ost[m], ocfg, w, obs, full_row=row)
+            ok, err = scores_close(scores[m, :ost[m].last_scores.size], ost[m].last_scores, "fp16x3")
+            assert ok, f"step {s} map {m}: err/bound {err:.3g}"
+            assert dev.middle(m) == ost[m].last_blocks
