@@ -122,7 +122,8 @@ typedef struct ap_map_state {
     int32_t r_wgen;    /* forecaster weight generation the r-map was built with (ap_set_weights bumps it) */
     int32_t tie_n;     /* exact-boundary guard at the last update: 0 = no ambiguity, n > 0 = n near-tie
                         * candidates re-scored in fp64, -n = n candidates exceeded the guard capacity */
-    int32_t pad_;
+    uint32_t prev_kth; /* order key of the k-th score at the last update (0 = none): the next update's top-k
+                        * first looks for its boundary in a narrow band around it */
 } ap_map_state;
 
 typedef struct ap_selector {
@@ -151,6 +152,10 @@ typedef struct ap_selector {
     const int32_t* k_map;     /* [n_maps] per-map middle-block budget (budget allocation across layers /
                                * heads: selector.py:47-50 evaluated per map), each <= k_mid (the pitch of
                                * mid_blocks); NULL = k_mid for every map                                  */
+    int32_t* fused_done;      /* [n_maps] zeroed once: with it, ap_sel_step runs forecast + top-k (+ guard)
+                               * as ONE launch (each map selected by the CTA that finishes its last
+                               * chunk; the count returns to 0 by the end of every step); NULL = separate
+                               * top-k launch                                                             */
 } ap_selector;
 
 /* Zero the state of every map (selector.init_state with no prefill rows). */

@@ -42,7 +42,7 @@ class MapState(ctypes.Structure):
         ("n_pushed", ctypes.c_int64), ("r_pushed", ctypes.c_int64), ("row_len", ctypes.c_int64),
         ("counter", ctypes.c_int64), ("mid_clip", ctypes.c_int64), ("width", ctypes.c_int32),
         ("r_width", ctypes.c_int32), ("n_mid", ctypes.c_int32), ("r_wgen", ctypes.c_int32),
-        ("tie_n", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("tie_n", ctypes.c_int32), ("prev_kth", ctypes.c_uint32),
     ]
 
 
@@ -56,7 +56,7 @@ class Selector(ctypes.Structure):
         ("slot_width", ctypes.c_void_p), ("slot_xmax", ctypes.c_void_p),
         ("state", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("mid_blocks", ctypes.c_void_p),
         ("mid_mask", ctypes.c_void_p), ("status", ctypes.c_void_p), ("tie_ws", ctypes.c_void_p),
-        ("k_map", ctypes.c_void_p),
+        ("k_map", ctypes.c_void_p), ("fused_done", ctypes.c_void_p),
     ]
 
 

@@ -18,6 +18,8 @@ from __future__ import annotations
 
 import ctypes
 
+import os
+
 import numpy as np
 
 from . import _device as D
@@ -29,7 +31,7 @@ PUSH_PREFILL, PUSH_DENSE, PUSH_OBSERVED = 0, 1, 2
 _STATE_DTYPE = np.dtype([
     ("n_pushed", "<i8"), ("r_pushed", "<i8"), ("row_len", "<i8"), ("counter", "<i8"), ("mid_clip", "<i8"),
     ("width", "<i4"), ("r_width", "<i4"), ("n_mid", "<i4"), ("r_wgen", "<i4"),
-    ("tie_n", "<i4"), ("pad_", "<i4"),
+    ("tie_n", "<i4"), ("prev_kth", "<u4"),
 ])
 assert _STATE_DTYPE.itemsize == _lib.MAP_STATE_BYTES
 
@@ -43,7 +45,7 @@ class BatchedSelector:
     """
 
     def __init__(self, cfg, n_maps: int, w_max: int, precision: str = "fp16x3", device=None, tie_guard: bool = True,
-                 budgets=None):
+                 budgets=None, fused: bool | None = None):
         cfg.validate()
         if n_maps < 1 or w_max < 1:
             raise ParameterError("n_maps and w_max must be >= 1")
@@ -81,6 +83,12 @@ class BatchedSelector:
         if tie_guard:
             nb = int(_lib.fn("ap_sel_tie_ws_bytes")(self.n_maps))
             self.tie_ws = torch.zeros(-(-nb // 4), dtype=i32, device=dev)
+        # fused=True: forecast + top-k (+ guard) as one launch (ap_selector.fused_done: per-map chunk
+        # counters).  Off by default — it measured slower than the two launches;
+        # ATTNPRED_FUSED_SELECT=1 turns it on for every selector.
+        if fused is None:
+            fused = os.environ.get("ATTNPRED_FUSED_SELECT") == "1"
+        self.fused_done = torch.zeros(n_maps, dtype=i32, device=dev) if fused else None
         self._desc = _lib.Selector(
             n_maps=n_maps, history=H, block=cfg.block_size, w_max=w_max, k_mid=self.k_mid,
             sink=cfg.sink_tokens, local=cfg.local_tokens, calib_period=cfg.calibration_period,
@@ -91,6 +99,7 @@ class BatchedSelector:
             mid_mask=self.mid_mask.data_ptr(), status=self.status.data_ptr(),
             tie_ws=None if self.tie_ws is None else self.tie_ws.data_ptr(),
             k_map=None if self.k_map is None else self.k_map.data_ptr(),
+            fused_done=None if self.fused_done is None else self.fused_done.data_ptr(),
         )
         self.reset()
 
@@ -134,7 +143,8 @@ class BatchedSelector:
         d.n_maps = count
         for name, per_map in (("ring", 4 * H * wm), ("rmap", 4 * H * wm), ("rsum", 8 * wm), ("slot_width", 4 * H),
                               ("slot_xmax", 4 * H), ("state", _STATE_DTYPE.itemsize), ("scores", 4 * wm),
-                              ("mid_blocks", 4 * max(self.k_mid, 1)), ("mid_mask", 4 * words), ("k_map", 4)):
+                              ("mid_blocks", 4 * max(self.k_mid, 1)), ("mid_mask", 4 * words), ("k_map", 4),
+                              ("fused_done", 4)):
             base = getattr(d, name)
             if base:
                 setattr(d, name, base + begin * per_map)

@@ -169,10 +169,25 @@ struct Params {
 
 __host__ __device__ __forceinline__ int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+__device__ __forceinline__ void st_volatile(int* p, int v) { *reinterpret_cast<volatile int*>(p) = v; }
+__device__ __forceinline__ int ld_volatile(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
 // ------------------------------------------------------------ block reduce/scan
-template <int NT>
-__device__ __forceinline__ int block_excl_scan(int v, int* smem_warp /*[NT/32+1]*/, int& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// A thread group that synchronises as one: the whole CTA, or NTH threads of it starting at thread BASE
+// on named barrier ID (a warp-specialised kernel's role running a CTA-style algorithm).
+struct CtaGroup {
+    __device__ __forceinline__ int tid() const { return threadIdx.x; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+template <int ID, int NTH, int BASE>
+struct BarGroup {
+    __device__ __forceinline__ int tid() const { return (int)threadIdx.x - BASE; }
+    __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" :: "n"(ID), "n"(NTH) : "memory"); }
+};
+
+template <int NT, class G>
+__device__ __forceinline__ int group_excl_scan(int v, int* smem_warp /*[NT/32+1]*/, int& total, const G& g) {
+    const int lane = g.tid() & 31, warp = g.tid() >> 5;
     int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -180,7 +195,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* smem_warp /*[NT/32+1]
         if (lane >= o) x += y;
     }
     if (lane == 31) smem_warp[warp] = x;
-    __syncthreads();
+    g.sync();
     if (warp == 0) {
         int w = (lane < NT / 32) ? smem_warp[lane] : 0;
 #pragma unroll
@@ -190,11 +205,15 @@ __device__ __forceinline__ int block_excl_scan(int v, int* smem_warp /*[NT/32+1]
         }
         if (lane < NT / 32) smem_warp[lane] = w;  // inclusive warp totals
     }
-    __syncthreads();
+    g.sync();
     int base = warp ? smem_warp[warp - 1] : 0;
     total = smem_warp[NT / 32 - 1];
-    __syncthreads();
+    g.sync();
     return base + x - v;
+}
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int* smem_warp /*[NT/32+1]*/, int& total) {
+    return group_excl_scan<NT>(v, smem_warp, total, CtaGroup{});
 }
 
 // ============================================================ tcgen05 / TMEM

@@ -97,7 +97,7 @@ __global__ void sel_reset_kernel(ap_selector s) {
     if (i < s.n_maps) {
         ap_map_state z;
         z.n_pushed = 0; z.r_pushed = -1; z.row_len = 0; z.counter = 0; z.mid_clip = 0;
-        z.width = 0; z.r_width = 0; z.n_mid = 0; z.r_wgen = 0; z.tie_n = 0; z.pad_ = 0;
+        z.width = 0; z.r_width = 0; z.n_mid = 0; z.r_wgen = 0; z.tie_n = 0; z.prev_kth = 0;
         s.state[i] = z;
     }
     // slot content unknown after a reset: the first push into a slot zero-fills [W, w_max), so ring rows

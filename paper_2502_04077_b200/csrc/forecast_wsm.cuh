@@ -63,12 +63,26 @@ __device__ __forceinline__ int role_of(int w) {
 __device__ __forceinline__ int conv_rank(int w) { return w - CONV0; }
 #endif
 constexpr int NCONV_T = NCONV * 32;
+// Fused selection (FUSE): once a CTA has no more bands, its warps split into four groups of four that run
+// kernel 3 (top-k + exact-boundary guard) on the CTA's maps (map m on CTA m % gridDim.x) as soon as every
+// chunk of the map is forecast, then help with the guard's fp64 re-scoring.
+constexpr int SEL_NT = 128, SEL_IPT = 24;   // rows of <= 3072 blocks (48K tokens at b = 16)
+constexpr int NGRP = NT / SEL_NT;
+constexpr int QN = 256;                     // arrival queue: ((map + 1) << 3 | arrivals) events, 1 = end
+constexpr int BAR_EPI = 7, BAR_GRP0 = 8;    // named barriers: epilogue warps at the end, select group g
+struct RtGroup {  // select group g: threads [128 g, 128 g + 128), named barrier BAR_GRP0 + g
+    int g;
+    __device__ __forceinline__ int tid() const { return (int)threadIdx.x - g * SEL_NT; }
+    __device__ __forceinline__ void sync() const {
+        asm volatile("bar.sync %0, %1;" :: "r"(BAR_GRP0 + g), "n"(SEL_NT) : "memory");
+    }
+};
 constexpr int TMEM = 512;
 constexpr int ACC_COLS = MO * 32;           // 160
 constexpr int PLANE_M = MA * A1C * 16;      // one 8-channel fp16 plane of the a1 tile
 static_assert(NA * ACC_COLS <= TMEM, "TMEM budget");
 
-__device__ long long g_trace[64 * 8];  // debug bit 16: CTA 0 timeline of its first 64 bands
+__device__ long long g_trace[64 * 16];  // debug bit 16: CTA 0 timeline of its first 64 bands
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -79,7 +93,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define WSM_CTA(e, v) \
     if ((dbg & 32) && (threadIdx.x & 31) == 0 && blockIdx.x < 320) ws::g_prof[blockIdx.x * 8 + (e)] = (v);
 #define WSM_TRACE(b, e) \
-    if ((dbg & 16) && blockIdx.x == 0 && (b) < 64) g_trace[(b) * 8 + (e)] = clock64();
+    if ((dbg & 16) && blockIdx.x == 0 && (b) < 64) g_trace[(b) * 16 + (e)] = clock64();
 
 // real a1 rows of the steady-state incremental band: tile row, first output (band index), outputs fed, B block
 __host__ __device__ constexpr int STD_R(int i) { return i + 1; }
@@ -119,10 +133,33 @@ struct Smem {
     static constexpr int off_info = off_meta + NX * (int)sizeof(Meta);          // Meta[NA] (conv1 -> MMA / epi)
     static constexpr int off_ainfo = off_info + NA * (int)sizeof(Meta);         // EpiInfo[NA]
     static constexpr int off_eold = (off_ainfo + NA * (int)sizeof(EpiInfo) + 15) / 16 * 16;  // EOld[NA]
-    static constexpr int off_bar = off_eold + NA * (int)sizeof(EOld);
+    // FUSE, after the last band: per select group SelSmem + RefineSmem over the (then idle) a1 tiles
+    static constexpr int kSel = ((int)sizeof(SelSmem<SEL_NT, SEL_IPT>) + 15) / 16 * 16;
+    static constexpr int kGrp = (kSel + (int)sizeof(tie::RefineSmem) + 15) / 16 * 16;
+    static constexpr int off_grp = off_a1;
+    // arrival queue int[QN], tail, head
+    static constexpr int off_q = (off_eold + NA * (int)sizeof(EOld) + 15) / 16 * 16;
+    static constexpr int off_bar = (off_q + (QN + 4) * 4 + 7) / 8 * 8;
     // x_full[NX], x_empty[NX], a1_full[NA], a1_empty[NA], acc_full[NA], acc_empty[NA], eold_empty[NA], tmem slot
     static constexpr int total = off_bar + 8 * (2 * NX + 5 * NA) + 16;
 };
+
+// FUSE: a map is complete after NEPI * n_chunks arrivals — each epilogue warp at a task's last band, the
+// producer NEPI at once for a skipped task.  Arrivals are queued in shared memory (CTA-scope release
+// only: no device-scope fence on the forecasting warps' path) to the counter warp (warp 13, otherwise
+// idle), which drains a batch, publishes it with one device-scope fence and counts it into
+// ap_selector.fused_done.  Map m is selected by CTA m % gridDim.x, whose select group waits for the
+// map's count (maps complete in task order, so each CTA's one or two maps come due at different times;
+// handing a map to whichever CTA counted it last instead piles the maps onto the slowest counters).
+__device__ __forceinline__ void ring_push(int* q, int cap, int v) {  // q[cap] = tail, q[cap + 1] = head
+    const int slot = atomicAdd(&q[cap], 1);
+    while (slot - ld_volatile(&q[cap + 1]) >= cap) __nanosleep(64);
+    st_volatile(&q[slot % cap], v);
+}
+__device__ __forceinline__ void sel_arrive(uint8_t* smem, int map, int n) {
+    __threadfence_block();  // the arriving warp's score stores before the event
+    ring_push(reinterpret_cast<int*>(smem + Smem::off_q), QN, ((map + 1) << 3) | n);
+}
 
 // Output rows of band bi of a task: the task's row list is [0, H) (full) or {0, 1} ∪ [lo2, H)
 // (incremental), taken MO at a time; a band is one or two contiguous segments.
@@ -141,7 +178,9 @@ __device__ __forceinline__ void band_segs(int full, int lo2, int H, int bi, int 
     }
 }
 
-template <int PREC>
+static_assert(NGRP * Smem::kGrp <= NA * Smem::kA1, "select scratch fits the a1 tiles");
+
+template <int PREC, bool FUSE>
 __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) {
     extern __shared__ __align__(1024) uint8_t smem[];
     Meta* meta = reinterpret_cast<Meta*>(smem + Smem::off_meta);
@@ -160,13 +199,16 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int H = P.H;
     const bool sel = P.state != nullptr;
-    const int dbg = P.debug;  // profiling only: 1 no conv1 arithmetic, 2 no MMAs, 4 no epilogue arithmetic
+    const int dbg = P.debug;  // profiling only: 1 no conv1 arithmetic, 2 no MMAs, 4 no epilogue arithmetic,
+                              // 64 no accumulator clearing
     if (tid == 0) WSM_CTA(0, gtimer());
 
     {  // B operands once per persistent CTA; barriers; TMEM
         const uint4* src = g_bpack96;
         uint4* dst = reinterpret_cast<uint4*>(smem + Smem::off_b);
-        for (int i = tid; i < Smem::kB / 16; i += NT) dst[i] = src[i];
+        for (int i = tid; i < Smem::kB / 16; i += (int)blockDim.x) dst[i] = src[i];
+        if (FUSE)
+            for (int i = tid; i < QN + 4; i += (int)blockDim.x) reinterpret_cast<int*>(smem + Smem::off_q)[i] = 0;
         if (tid == 0) {
             for (int s = 0; s < NX; ++s) {
                 mbar_init(&x_full[s], 1);
@@ -204,6 +246,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
             if (have && P.state) st = P.state[map];
             const Task T = have ? plan_task(P, st, chunk) : Task{true, true, false, 0, 0, 0};
             const bool live = have && !T.skip;
+            if (FUSE && have && !live) sel_arrive(smem, map, NEPI);  // nothing to forecast: the whole count
             const int base_slot = sel ? slot_of(row_index(T.n_pushed, H, 0), H) : 0;
             const int first_real = (!sel || T.n_pushed >= H) ? 0 : (int)(H - T.n_pushed);
             unsigned todo = __ballot_sync(0xffffffffu, live);
@@ -450,6 +493,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                     tmem_ld16_start(t0 + k * 32 + 16, rb);
                     tmem_ld_wait(ra);
                     tmem_ld_wait(rb);
+                    if (k == 0 && warp == EPI0 && lane == 0) WSM_TRACE(b, 8);
                     if (!one_mul) {  // scale too extreme for one multiply (never for attention rows)
 #pragma unroll
                         for (int n = 0; n < 16; ++n) {
@@ -479,13 +523,15 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                     }
                 }
                 if (n_out > 0) tmem_ld_wait(ra);
-                for (int k = 0; k < n_out; ++k) tmem_zero32(t0 + k * 32);  // cleared for the next band
+                if (warp == EPI0 && lane == 0) WSM_TRACE(b, 9);
+                for (int k = 0; k < ((dbg & 64) ? 0 : n_out); ++k) tmem_zero32(t0 + k * 32);  // cleared for the next band
                 Snew += (double)bsum;
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             tc_fence_before();
             __syncwarp();
             const bool last = I.last;
+            const int mapi = I.map;
             const int64_t sat = (int64_t)I.map * P.score_stride + col;
             if (warp == EPI0 && lane == 0) WSM_TRACE(b, 7);
             __syncwarp();  // every lane has read ainfo[a]: the MMA issuer refills it once all four warps arrive
@@ -494,6 +540,39 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                 S += Snew - (double)osum;
                 if (P.rsum) P.rsum[at] = S;
                 P.scores[sat] = c_w[OFF_B3] + (float)S / (float)H;
+            }
+            if (FUSE && last) {
+                __syncwarp();
+                if (lane == 0) sel_arrive(smem, mapi, 1);
+            }
+        }
+        if (FUSE) {  // every epilogue warp's arrivals are in: no more maps complete in this CTA
+            asm volatile("bar.sync %0, %1;" :: "n"(BAR_EPI), "n"(NEPI * 32) : "memory");
+            if (warp == EPI0 && lane == 0) ring_push(reinterpret_cast<int*>(smem + Smem::off_q), QN, 1);
+        }
+    } else if (FUSE && role == R_IDLE) {
+        // ------------------------------------------------------------------ arrival counter (warp 13, lane 0)
+        if (lane == 0) {
+            int* q = reinterpret_cast<int*>(smem + Smem::off_q);
+            int head = 0;
+            bool end = false;
+            while (!end) {
+                int evs[16], n_ev = 0, v;
+                while (n_ev < 16 && (v = ld_volatile(&q[head % QN])) != 0) {
+                    st_volatile(&q[head % QN], 0);
+                    ++head;
+                    evs[n_ev++] = v;
+                }
+                if (!n_ev) {
+                    __nanosleep(64);
+                    continue;
+                }
+                st_volatile(&q[QN + 1], head);
+                __threadfence();  // the arrivals' score stores (CTA-scope ordered before the events) before the counts
+                for (int i = 0; i < n_ev; ++i) {
+                    if (evs[i] == 1) end = true;
+                    else atomicAdd(&P.sel.fused_done[(evs[i] >> 3) - 1], evs[i] & 7);
+                }
             }
         }
     } else if (role == R_CONV) {
@@ -658,6 +737,73 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
         }
     }
 
+    if (FUSE) {
+        // ------------------------------------------------------------------ selection (kernel 3)
+        // this CTA has no more bands: group g (warps 4g .. 4g+3, together once each has left its role)
+        // selects maps blockIdx.x + (g + NGRP j) * gridDim.x, each once all its chunks' arrivals are counted
+        const RtGroup grp{warp / 4};
+        const int gt = grp.tid();
+        uint8_t* gs = smem + Smem::off_grp + grp.g * Smem::kGrp;
+        auto& sh = *reinterpret_cast<SelSmem<SEL_NT, SEL_IPT>*>(gs);
+        auto& rs = *reinterpret_cast<tie::RefineSmem*>(gs + Smem::kSel);
+        const int target = NEPI * P.n_chunks;
+        __syncthreads();  // every role is done (the last MMAs too): the a1 tiles are free for the group scratch
+        if (tid == 0) WSM_CTA(5, gtimer());
+        for (int m = blockIdx.x + grp.g * gridDim.x; m < P.n_maps; m += NGRP * gridDim.x) {
+            if (gt == 0) {
+                while (ld_volatile(&P.sel.fused_done[m]) != target) __nanosleep(128);
+                __threadfence();  // every chunk's scores before the selection reads them
+            }
+            grp.sync();
+            select_map<SEL_NT, SEL_IPT>(P.sel, P.tp, m, grp, sh);
+            if (gt == 0) P.sel.fused_done[m] = 0;  // every arrival of this launch is in: reset for the next
+        }
+        if (gt == 0 && grp.g == 0) WSM_CTA(6, gtimer());
+        int* ws = P.sel.tie_ws;
+        if (P.tp.enabled && ws) {
+            // exact-boundary guard: fp64 re-scoring units of every CTA's maps, taken from the shared list as
+            // they appear, until all CTAs have selected all their maps and the list is drained
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(&ws[tie::H_SELDONE], 1);
+            }
+            for (;;) {
+                if (gt == 0) {
+                    const int u = atomicAdd(&ws[tie::H_NEXT], 1);
+                    int val = 0;
+                    for (;;) {
+                        const int done = ld_volatile(&ws[tie::H_SELDONE]);
+                        __threadfence();
+                        if (u < ld_volatile(&ws[tie::H_UNITS])) {
+                            while ((val = ld_volatile(&ws[tie::HDR + u])) == 0) __nanosleep(32);
+                            st_volatile(&ws[tie::HDR + u], 0);
+                            break;
+                        }
+                        if (done == (int)gridDim.x) break;  // the list is final and u is past its end
+                        __nanosleep(256);
+                    }
+                    rs.val = val - 1;
+                }
+                grp.sync();
+                const int unit = rs.val;
+                if (unit < 0) break;
+                __threadfence();
+                tie::refine_unit(P.sel, P.tp, unit, rs.sx, rs.sa1, rs.srow, rs.flags, rs.scan_tmp, &rs.last, grp);
+            }
+            __syncthreads();
+            if (tid == 0) {  // the last CTA out resets the work list for the next step
+                __threadfence();
+                if (atomicAdd(&ws[tie::H_DONE], 1) == (int)gridDim.x - 1) {
+                    ws[tie::H_UNITS] = 0;
+                    ws[tie::H_NEXT] = 0;
+                    ws[tie::H_DONE] = 0;
+                    ws[tie::H_SELDONE] = 0;
+                    __threadfence();
+                }
+            }
+        }
+    }
     tc_fence_before();
     __syncthreads();
     if (tid == 0) WSM_CTA(3, gtimer());

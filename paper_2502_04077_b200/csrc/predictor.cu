@@ -142,6 +142,9 @@ struct ConvParams {
     int32_t n_maps, H, W_explicit, n_chunks, update_interval, k_mid;
     int32_t* status;
     int32_t debug;  // ATTNPRED_FORECAST_DEBUG bit mask (profiling only): 1 no conv1, 2 no MMA, 4 no epilogue
+    int32_t fuse;   // forecast + top-k (+ guard) in one launch (wsm kernel, selector mode)
+    ap_selector sel;  // (fuse) the descriptor the maps are selected with
+    tie::Params tp;   // (fuse) exact-boundary guard parameters
 };
 
 // Which history rows a task recomputes: full = [0, H); incremental (s new rows
@@ -616,6 +619,7 @@ __global__ void __launch_bounds__(NTHREADS, 2) conv_forecast_kernel(ConvParams P
 }  // namespace ap
 #include "forecast_ws.cuh"
 #include "forecast_ts.cuh"
+#include "select.cuh"
 #include "forecast_wsm.cuh"
 namespace ap {
 
@@ -623,11 +627,20 @@ template <int PREC>
 static int grid_ctas_wsm() {
     static int cached = 0;
     if (!cached) {
-        cudaFuncSetAttribute(wsm::conv_forecast_wsm_kernel<PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(wsm::conv_forecast_wsm_kernel<PREC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              wsm::Smem::total);
-        cached = ap_device_sm_count();  // one 16-warp CTA (and all 512 TMEM columns) per SM
+        cudaFuncSetAttribute(wsm::conv_forecast_wsm_kernel<PREC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             wsm::Smem::total);
+        cached = ap_device_sm_count();  // one 16- (20-) warp CTA (and all 512 TMEM columns) per SM
     }
     return cached;
+}
+template <int PREC>
+static void launch_wsm(const ConvParams& P, int n_tasks, cudaStream_t st) {
+    const int g = grid_ctas_wsm<PREC>();
+    const unsigned grid = (unsigned)(g < n_tasks ? g : n_tasks);
+    if (P.fuse) wsm::conv_forecast_wsm_kernel<PREC, true><<<grid, wsm::NT, wsm::Smem::total, st>>>(P);
+    else wsm::conv_forecast_wsm_kernel<PREC, false><<<grid, wsm::NT, wsm::Smem::total, st>>>(P);
 }
 
 template <int PREC>
@@ -710,8 +723,7 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st, in
         }
         case AP_PREC_F16X3: {
             if (P.pitch % 4 == 0 && tc_kernel() == 3) {
-                int g = grid_ctas_wsm<AP_PREC_F16X3>();
-                wsm::conv_forecast_wsm_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, wsm::NT, wsm::Smem::total, st>>>(P);
+                launch_wsm<AP_PREC_F16X3>(P, n_tasks, st);
             } else if (P.pitch % 4 == 0 && tc_kernel() == 2) {
                 int g = grid_ctas_ts<AP_PREC_F16X3>();
                 ts::conv_forecast_ts_kernel<AP_PREC_F16X3><<<g < n_tasks ? g : n_tasks, ts::NT, ts::Smem::total, st>>>(P);
@@ -726,8 +738,7 @@ static int launch_conv(const ConvParams& Pin, int precision, cudaStream_t st, in
         }
         case AP_PREC_F16: {
             if (P.pitch % 4 == 0 && tc_kernel() == 3) {
-                int g = grid_ctas_wsm<AP_PREC_F16>();
-                wsm::conv_forecast_wsm_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, wsm::NT, wsm::Smem::total, st>>>(P);
+                launch_wsm<AP_PREC_F16>(P, n_tasks, st);
             } else if (P.pitch % 4 == 0 && tc_kernel() == 2) {
                 int g = grid_ctas_ts<AP_PREC_F16>();
                 ts::conv_forecast_ts_kernel<AP_PREC_F16><<<g < n_tasks ? g : n_tasks, ts::NT, ts::Smem::total, st>>>(P);
@@ -839,6 +850,14 @@ int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W
 
 static int sel_step_impl(const ap_selector* s, int precision, int grid_cap, void* stream);
 
+// Forecast + top-k (+ guard) as one launch when the descriptor carries fused_done: the warp-specialised
+// tensor-core forecaster selects its maps after its last band (rows of <= SEL_NT * SEL_IPT blocks); other
+// precisions / kernels / widths take the separate top-k launch.
+static bool fused_select(const ap_selector& s, int precision) {
+    return s.fused_done && s.k_mid > 0 && (precision == AP_PREC_F16X3 || precision == AP_PREC_F16) &&
+           tc_kernel() == 3 && s.w_max % 4 == 0 && s.w_max <= wsm::SEL_NT * wsm::SEL_IPT;
+}
+
 int ap_sel_step(const ap_selector* s, int precision, void* stream) { return sel_step_impl(s, precision, 0, stream); }
 
 int ap_sel_step_grid(const ap_selector* s, int precision, int grid_ctas, void* stream) {
@@ -870,8 +889,11 @@ static int sel_step_impl(const ap_selector* s, int precision, int grid_cap, void
         P.update_interval = s->update_interval;
         P.k_mid = s->k_mid;
         P.status = s->status;
+        P.fuse = fused_select(*s, precision);
+        P.sel = *s;
+        P.tp = tie_params(precision);
         int rc = launch_conv(P, precision, st, grid_cap);
-        if (rc != AP_OK) return rc;
+        if (rc != AP_OK || P.fuse) return rc;  // fused: the forecaster launch also selected every map
     }
     launch_sel_topk(*s, tie_params(precision), st);
     return launch_status("sel_topk_kernel");
@@ -886,7 +908,7 @@ int ap_debug_prof(unsigned long long* host_out, int n) {
 int ap_debug_trace(long long* host_out) {
     const int k = tc_kernel();
     const cudaError_t e = k == 2   ? cudaMemcpyFromSymbol(host_out, ts::g_trace, sizeof(long long) * 64 * 8)
-                          : k == 3 ? cudaMemcpyFromSymbol(host_out, wsm::g_trace, sizeof(long long) * 64 * 8)
+                          : k == 3 ? cudaMemcpyFromSymbol(host_out, wsm::g_trace, sizeof(long long) * 64 * 16)
                                    : cudaMemcpyFromSymbol(host_out, ws::g_trace, sizeof(long long) * 64 * 8);
     return e == cudaSuccess ? AP_OK : AP_ECUDA;
 }

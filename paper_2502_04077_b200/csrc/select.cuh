@@ -1,0 +1,289 @@
+// One map's top-k selection (kernel 3's body) for any thread group: the standalone top-k kernel runs
+// it with a whole CTA per map, the fused forecaster (forecast_wsm.cuh) with four warps of each of its
+// CTAs on the maps whose last chunk that CTA finished.
+#pragma once
+
+#include "tieguard.cuh"
+
+namespace ap {
+
+// Band variant (the default for rows of <= NT * IPT blocks).  Scores move little between two updates
+// of a map (an incremental forecast changes five of H history rows), so the boundary is first looked
+// for in a narrow band around the previous update's k-th score (ap_map_state.prev_kth): one counting
+// pass gives the keys above the band and in it; if the k-th key falls inside a band of at most TK_CAND
+// keys, those are ranked against each other by (key desc, index asc) — selector.py:80's order — and the
+// selection is exact after ~6 CTA barriers.  Otherwise (first update, calibration jumps, heavy ties) the
+// 8-bit radix passes of sel_topk_reg_kernel run on the same registers.  The radix form alone spent
+// 19.7k cycles per map on CTA 0 (scripts/dbg/topk_trace.py), most of it in same-address shared atomics:
+// the scores' bulk shares a few digits.
+constexpr int TK_CAND = 128;
+
+template <int NT, int IPT>
+struct SelSmem {  // shared memory of one map's selection by an NT-thread group
+    int hist[256];
+    int scan_tmp[NT / 32 + 2];
+    uint32_t c_key[TK_CAND];
+    int c_id[TK_CAND];
+    uint32_t mask[NT * IPT / 32 + 1];
+    int nan, amax, nmask, above, band, cnt, bcast;
+    unsigned kmn, kmx, tmin;
+};
+
+// Map m's update (or counter tick) by the NT threads of grp; rows of <= NT * IPT blocks.
+template <int NT, int IPT, class G>
+__device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, const G& grp, SelSmem<NT, IPT>& sh) {
+    static_assert(IPT <= 32 && IPT % 4 == 0, "one take bit per key, 16-byte loads");
+    int* hist = sh.hist;
+    int* scan_tmp = sh.scan_tmp;
+    uint32_t* c_key = sh.c_key;
+    int* c_id = sh.c_id;
+    uint32_t* s_mask = sh.mask;
+    int &s_nan = sh.nan, &s_amax = sh.amax, &s_nmask = sh.nmask, &s_above = sh.above, &s_band = sh.band,
+        &s_cnt = sh.cnt, &s_bcast = sh.bcast;
+    unsigned &s_kmn = sh.kmn, &s_kmx = sh.kmx, &s_tmin = sh.tmin;
+    const int tid = grp.tid(), lane = tid & 31;
+    // the row's scores are requested before the map state they depend on arrives (one round trip, not two)
+    const float* sc = s.scores + (int64_t)m * s.w_max;
+    const int i0 = tid * IPT;
+    float vals[IPT];
+    if (i0 + IPT <= s.w_max) {  // 16-byte loads (w_max % 4 == 0, i0 % 4 == 0); L2: other CTAs wrote them
+#pragma unroll
+        for (int v4 = 0; v4 < IPT / 4; ++v4) {
+            const float4 f = __ldcg(reinterpret_cast<const float4*>(sc + i0) + v4);
+            vals[4 * v4] = f.x; vals[4 * v4 + 1] = f.y; vals[4 * v4 + 2] = f.z; vals[4 * v4 + 3] = f.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) vals[q] = i0 + q < s.w_max ? __ldcg(sc + i0 + q) : -INFINITY;
+    }
+    ap_map_state st = s.state[m];
+    const bool update = (st.counter % s.update_interval) == 0;
+    const int words = (s.w_max + 31) / 32;
+    uint32_t* mask = s.mid_mask + (int64_t)m * words;
+    int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
+    int count = st.n_mid;
+    int tie_n = 0;
+    uint32_t kth = st.prev_kth;
+    if (update && s.k_mid > 0 && st.width > 0) {
+        for (int w = tid; w < words; w += NT) s_mask[w] = 0u;
+        if (tid == 0) {
+            s_nan = 0; s_amax = 0; s_nmask = 0; s_above = 0; s_band = 0; s_cnt = 0;
+            s_kmn = 0xffffffffu; s_kmx = 0u; s_tmin = 0xffffffffu;
+        }
+        const int W = st.width;
+        const unsigned b = (unsigned)s.block;
+        const int64_t t = st.row_len;
+        // covering blocks of sink [0, min(sink, nl)) and local [max(0, nl-local), nl) — selector.py:84-88,134-142
+        // (32-bit: positions < 2^31; 64-bit division is a ~100-cycle software routine on the critical path)
+        const unsigned nl = (unsigned)(t + 1);
+        const unsigned sink_end = (unsigned)s.sink < nl ? (unsigned)s.sink : nl;
+        int sink_hi = (int)((sink_end + b - 1) / b);
+        const unsigned ls = nl > (unsigned)s.local ? nl - (unsigned)s.local : 0u;
+        const int local_lo = ls < nl ? (int)(ls / b) : 0;  // (an empty local window covers no block)
+        int local_hi = ls < nl ? (int)((nl + b - 1) / b) : 0;
+        sink_hi = sink_hi > W ? W : sink_hi;
+        local_hi = local_hi > W ? W : local_hi;
+        uint32_t key[IPT];
+        int nm = 0;
+        bool nan = false;
+        float amax = 0.f;
+        unsigned kmn = 0xffffffffu, kmx = 0u;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+            const int i = i0 + q;
+            const float v = i < W ? vals[q] : -INFINITY;
+            nan |= v != v;
+            const bool masked = i >= W || (i < sink_hi) || (i >= local_lo && i < local_hi);
+            key[q] = masked ? 0u : order_key(v);  // 0 sorts below every real key (and is never taken)
+            nm += i < W && (masked || v == -INFINITY);
+            if (!masked && fabsf(v) <= 3.402823466e38f) amax = fmaxf(amax, fabsf(v));
+            if (key[q]) {
+                kmn = min(kmn, key[q]);
+                kmx = max(kmx, key[q]);
+            }
+        }
+        // band around the previous k-th score: +-2^-8 |tau|
+        uint32_t blo = 1u, bhi = 0u;  // empty band: no previous boundary
+        if (kth) {
+            const float tau = tie::key_value(kth), d = fmaxf(0.00390625f * fabsf(tau), 1e-30f);
+            blo = order_key(tau - d);
+            bhi = order_key(tau + d);
+        }
+        int na = 0, nb = 0;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q) {
+            na += key[q] > bhi;
+            nb += key[q] >= blo && key[q] <= bhi;
+        }
+        grp.sync();  // shared state initialised
+        // CTA reductions: one shared atomic per warp
+        nm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nm);
+        na = (int)__reduce_add_sync(0xffffffffu, (unsigned)na);
+        nb = (int)__reduce_add_sync(0xffffffffu, (unsigned)nb);
+        kmn = __reduce_min_sync(0xffffffffu, kmn);
+        kmx = __reduce_max_sync(0xffffffffu, kmx);
+        const unsigned am = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));  // non-negative floats
+        if (__any_sync(0xffffffffu, nan) && lane == 0) s_nan = 1;
+        if (lane == 0) {
+            atomicAdd(&s_nmask, nm);
+            if (na) atomicAdd(&s_above, na);
+            if (nb) atomicAdd(&s_band, nb);
+            atomicMin(&s_kmn, kmn);
+            atomicMax(&s_kmx, kmx);
+            atomicMax(&s_amax, (int)am);
+        }
+        grp.sync();
+        if (s_nan) raise_status(s.status, AP_ENUMERIC);
+        const int available = W - s_nmask;
+        const int kcap = s.k_map ? min(max(s.k_map[m], 0), s.k_mid) : s.k_mid;
+        const int k = kcap < available ? kcap : available;
+        uint32_t take = 0u;  // bit q: block i0 + q is selected
+        if (k > 0) {
+            const int above = s_above, band = s_band;
+            if (above < k && above + band >= k && band <= TK_CAND) {
+                // fast path: the k-th key is in the band; rank the band's keys among themselves
+                const int need = k - above;
+                uint32_t inband = 0u;
+#pragma unroll
+                for (int q = 0; q < IPT; ++q)
+                    if (key[q] >= blo && key[q] <= bhi) {
+                        const int slot = atomicAdd(&s_cnt, 1);
+                        c_key[slot] = key[q];
+                        c_id[slot] = i0 + q;
+                        inband |= 1u << q;
+                    }
+                grp.sync();
+                    if (tid < band) {  // one thread per band key: its rank among the band (key desc, index asc)
+                    const uint32_t kq = c_key[tid];
+                    const int iq = c_id[tid];
+                    int rank = 0;
+#pragma unroll 4
+                    for (int j = 0; j < band; ++j) {
+                        const uint32_t kj = c_key[j];
+                        rank += kj > kq || (kj == kq && c_id[j] < iq);
+                    }
+                    if (rank < need) atomicOr(&s_mask[iq >> 5], 1u << (iq & 31));  // (s_mask: scratch here)
+                }
+                grp.sync();
+#pragma unroll
+                for (int q = 0; q < IPT; ++q)
+                    if (key[q] > bhi || ((inband >> q) & 1u && (s_mask[(i0 + q) >> 5] >> ((i0 + q) & 31)) & 1u))
+                        take |= 1u << q;
+                grp.sync();  // every band decision read: s_mask is rebuilt from `take` below
+                for (int w = tid; w < words; w += NT) s_mask[w] = 0u;
+                grp.sync();
+            } else {
+                // radix select of the k-th largest key, 8 bits per pass, skipping the bytes every unmasked
+                // key shares (they all lie in [kmn, kmx])
+                kmn = s_kmn;
+                kmx = s_kmx;
+                const int top = (kmn ^ kmx) ? 31 - __clz(kmn ^ kmx) : -1;
+                const int first = top >= 0 ? top / 8 : -1;
+                uint32_t hi_mask = first >= 3 ? 0u : (0xffffffffu << ((first + 1) * 8));
+                uint32_t prefix = kmx & hi_mask;
+                int remaining = k;
+#pragma unroll 1
+                for (int pass = first; pass >= 0; --pass) {
+                    const int shift = pass * 8;
+                    for (int d = tid; d < 256; d += NT) hist[d] = 0;
+                    grp.sync();
+#pragma unroll
+                    for (int q = 0; q < IPT; ++q)
+                        if (key[q] != 0u && ((key[q] ^ prefix) & hi_mask) == 0) atomicAdd(&hist[(key[q] >> shift) & 0xFF], 1);
+                    grp.sync();
+                    int c = 0;
+                    for (int d = tid * 256 / NT; d < (tid + 1) * 256 / NT; ++d) c += hist[255 - d];
+                    int total = 0;
+                    int run = group_excl_scan<NT>(c, scan_tmp, total, grp);
+                    for (int d = tid * 256 / NT; d < (tid + 1) * 256 / NT; ++d) {
+                        const int hd = hist[255 - d];
+                        if (run < remaining && run + hd >= remaining) {
+                            scan_tmp[NT / 32] = 255 - d;
+                            scan_tmp[NT / 32 + 1] = run;
+                        }
+                        run += hd;
+                    }
+                    grp.sync();
+                    remaining -= scan_tmp[NT / 32 + 1];
+                    prefix |= (uint32_t)scan_tmp[NT / 32] << shift;
+                    hi_mask |= 0xFFu << shift;
+                    grp.sync();
+                }
+                const uint32_t T = prefix;  // keys > T, and the lowest-index `remaining` keys == T
+                int n_eq = 0;
+#pragma unroll
+                for (int q = 0; q < IPT; ++q) n_eq += key[q] == T;
+                int te = 0;
+                int eq_rank = group_excl_scan<NT>(n_eq, scan_tmp, te, grp);
+#pragma unroll
+                for (int q = 0; q < IPT; ++q) {
+                    if (key[q] > T) {
+                        take |= 1u << q;
+                    } else if (key[q] == T) {
+                        if (eq_rank < remaining) take |= 1u << q;
+                        ++eq_rank;
+                    }
+                }
+            }
+            // ordered emission (ascending ids) and the bitmask image in shared memory
+            int total = 0;
+            int pos = group_excl_scan<NT>(__popc(take), scan_tmp, total, grp);
+            unsigned tmin = 0xffffffffu;
+#pragma unroll
+            for (int q = 0; q < IPT; ++q)
+                if (take & (1u << q)) {
+                    mid[pos++] = i0 + q;
+                    tmin = min(tmin, key[q]);
+                }
+            if (take && 32 % IPT == 0) {  // all of this thread's ids lie in one mask word
+                uint32_t w = 0u;
+#pragma unroll
+                for (int q = 0; q < IPT; ++q)
+                    if (take & (1u << q)) w |= 1u << ((i0 + q) & 31);
+                atomicOr(&s_mask[i0 >> 5], w);
+            } else if (take) {
+                uint32_t bits[(IPT + 31) / 32 + 1] = {};
+#pragma unroll
+                for (int q = 0; q < IPT; ++q)
+                    if (take & (1u << q)) bits[((i0 + q) >> 5) - (i0 >> 5)] |= 1u << ((i0 + q) & 31);
+#pragma unroll
+                for (int wq = 0; wq < (IPT + 31) / 32 + 1; ++wq)
+                    if (bits[wq]) atomicOr(&s_mask[(i0 >> 5) + wq], bits[wq]);
+            }
+            tmin = __reduce_min_sync(0xffffffffu, tmin);
+            if (lane == 0 && tmin != 0xffffffffu) atomicMin(&s_tmin, tmin);
+            count = total;
+        } else {
+            count = 0;
+        }
+        grp.sync();
+        for (int w = tid; w < words; w += NT) mask[w] = s_mask[w];
+        kth = k > 0 ? s_tmin : 0u;
+        if (k > 0 && tp.enabled && s.tie_ws) {
+            auto kf = [&](int i) -> uint32_t {
+                const bool masked = (i < sink_hi) || (i >= local_lo && i < local_hi);
+                return masked ? 0u : order_key(sc[i]);
+            };
+            tie_n = tie::detect<NT>(s, tp, m, kf, W, k, kth, __int_as_float(s_amax), sink_hi, local_lo, local_hi,
+                                    scan_tmp, &s_bcast, grp);
+        }
+        if (tid == 0) {
+            st.n_mid = count;
+            st.mid_clip = t;
+            st.r_pushed = st.n_pushed;
+            st.r_width = st.width;
+            st.r_wgen = tp.wgen ? *tp.wgen : 0;
+            st.tie_n = tie_n;
+            st.prev_kth = kth;
+        }
+    } else if (update && s.k_mid <= 0) {
+        for (int w = tid; w < words; w += NT) mask[w] = 0u;
+        if (tid == 0) st.n_mid = 0;
+    }
+    if (tid == 0) {
+        st.counter += 1;
+        s.state[m] = st;
+    }
+}
+
+}  // namespace ap

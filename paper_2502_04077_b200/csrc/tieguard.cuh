@@ -30,7 +30,7 @@ constexpr int OFF_IDS = REC_HDR, OFF_CPEND = OFF_IDS + CAP, OFF_SC = OFF_CPEND +
 constexpr int REC = OFF_PARTS + 2 * CAP * NG;
 constexpr int NT = 128;      // refine CTA: 4 warps, lane = conv2 output channel
 
-enum { H_UNITS = 0, H_NEXT = 1, H_DONE = 2, H_OVERFLOW = 3, H_MAPS = 4, H_CANDS = 5 };
+enum { H_UNITS = 0, H_NEXT = 1, H_DONE = 2, H_OVERFLOW = 3, H_MAPS = 4, H_CANDS = 5, H_SELDONE = 6 };
 enum { R_NA = 0, R_NEED, R_NB, R_KLO, R_KHI, R_PENDING, R_W, R_SINK_HI, R_LOCAL_LO, R_LOCAL_HI };
 
 __host__ __device__ inline int64_t units_cap(int n_maps) { return (int64_t)n_maps * CAP * NG; }
@@ -46,13 +46,15 @@ __device__ __forceinline__ float key_value(uint32_t k) {
 
 // All threads of the top-k CTA.  keyfn(i) = the masked order key of block i (0 = masked).
 // Returns the map's tie_n (0 unambiguous, NB re-scored candidates, -NB overflow).
-template <int NTH, typename KeyFn>
+template <int NTH, typename KeyFn, class G = CtaGroup>
 __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn, int W, int k, uint32_t T,
-                      float amax, int sink_hi, int local_lo, int local_hi, int* scan_tmp, int* s_bcast) {
+                      float amax, int sink_hi, int local_lo, int local_hi, int* scan_tmp, int* s_bcast,
+                      const G& grp = G{}) {
     const float tau = key_value(T);
     const float band = tp.rel * fmaxf(fabsf(tau), tp.floor * amax);
     const uint32_t khi = order_key(tau + band), klo = order_key(tau - band);
-    const int per = (W + NTH - 1) / NTH, lo = min(W, (int)threadIdx.x * per), hi = min(W, lo + per);
+    const int tid = grp.tid();
+    const int per = (W + NTH - 1) / NTH, lo = min(W, tid * per), hi = min(W, lo + per);
     int na = 0, nb = 0;
     for (int i = lo; i < hi; ++i) {
         const uint32_t key = keyfn(i);
@@ -60,13 +62,13 @@ __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn
         nb += key >= klo && key <= khi;
     }
     int NA = 0, NB = 0;
-    block_excl_scan<NTH>(na, scan_tmp, NA);
-    int pos = block_excl_scan<NTH>(nb, scan_tmp, NB);
+    group_excl_scan<NTH>(na, scan_tmp, NA, grp);
+    int pos = group_excl_scan<NTH>(nb, scan_tmp, NB, grp);
     const int need = k - NA;
     if (NB <= need) return 0;
     int* ws = s.tie_ws;
     if (NB > CAP || s.history > NG * MAX_RG) {
-        if (threadIdx.x == 0) atomicAdd(&ws[H_OVERFLOW], 1);
+        if (tid == 0) atomicAdd(&ws[H_OVERFLOW], 1);
         return -NB;
     }
     int* rec = ws + rec_off(s.n_maps) + (int64_t)m * REC;
@@ -74,8 +76,8 @@ __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn
         const uint32_t key = keyfn(i);
         if (key >= klo && key <= khi) rec[OFF_IDS + pos++] = i;  // ascending block ids
     }
-    for (int j = threadIdx.x; j < NB; j += NTH) rec[OFF_CPEND + j] = NG;
-    if (threadIdx.x == 0) {
+    for (int j = tid; j < NB; j += NTH) rec[OFF_CPEND + j] = NG;
+    if (tid == 0) {
         rec[R_NA] = NA;
         rec[R_NEED] = need;
         rec[R_NB] = NB;
@@ -90,9 +92,11 @@ __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn
         atomicAdd(&ws[H_MAPS], 1);
         atomicAdd(&ws[H_CANDS], NB);
     }
-    __syncthreads();
+    __threadfence();  // the record before its units: a fused consumer may take a unit as soon as it is listed
+    grp.sync();
     const int ub = *s_bcast;
-    for (int u = threadIdx.x; u < NB * NG; u += NTH) ws[HDR + ub + u] = (m * CAP + u / NG) * NG + u % NG;
+    // units listed as value + 1 (0 = not written yet; the consumer clears its entry for the next step)
+    for (int u = tid; u < NB * NG; u += NTH) st_volatile(ws + HDR + ub + u, (m * CAP + u / NG) * NG + u % NG + 1);
     return NB;
 }
 
@@ -148,7 +152,8 @@ __device__ int detect_warp(const ap_selector& s, const Params& tp, int m, const 
         atomicAdd(&ws[H_CANDS], NB);
     }
     ub = __shfl_sync(FULL, ub, 0);
-    for (int u = lane; u < NB * NG; u += 32) ws[HDR + ub + u] = (m * CAP + u / NG) * NG + u % NG;
+    __threadfence();
+    for (int u = lane; u < NB * NG; u += 32) st_volatile(ws + HDR + ub + u, (m * CAP + u / NG) * NG + u % NG + 1);
     return NB;
 }
 
@@ -157,8 +162,9 @@ __device__ int detect_warp(const ap_selector& s, const Params& tp, int m, const 
 // x window [RG+4 rows][5 cols], a1 window [RG+2 rows][16 ch][3 cols] in shared memory; warp w takes
 // rows w, w+4, ..., lane = output channel c (conv2 = a 144-term dot per lane, weights w2t[kt][c]
 // coalesced across lanes, a1 values broadcast).  All threads.
+template <class G = CtaGroup>
 __device__ double group_partial(const ap_selector& s, const double* __restrict__ w64, int m, int col, int g,
-                                double* sx, double* sa1, double* srow) {
+                                double* sx, double* sa1, double* srow, const G& grp = G{}) {
     const ap_map_state st = s.state[m];
     const int H = s.history, W = st.width, pitch = s.w_max;
     const int RG = (H + NG - 1) / NG;
@@ -167,7 +173,7 @@ __device__ double group_partial(const ap_selector& s, const double* __restrict__
     const float* ring = s.ring + (int64_t)m * H * pitch;
     const int64_t n_pushed = st.n_pushed;
     const int first_real = n_pushed >= H ? 0 : (int)(H - n_pushed);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = grp.tid(), lane = tid & 31, warp = tid >> 5;
     for (int idx = tid; idx < (nr + 4) * 5; idx += NT) {  // x rows r0-2 .. r0+nr+1, cols col-2 .. col+2
         const int q = idx / 5, c = idx % 5, p = r0 - 2 + q, cc = col - 2 + c;
         double v = 0.0;
@@ -178,7 +184,7 @@ __device__ double group_partial(const ap_selector& s, const double* __restrict__
         }
         sx[idx] = v;
     }
-    __syncthreads();
+    grp.sync();
     for (int idx = tid; idx < (nr + 2) * 48; idx += NT) {  // a1 rows r0-1 .. r0+nr, cols col-1 .. col+1
         const int r = idx / 48, kd = idx % 48, kk = kd / 3, dj = kd % 3;
         const int p = r0 - 1 + r, c2 = col - 1 + dj;
@@ -193,7 +199,7 @@ __device__ double group_partial(const ap_selector& s, const double* __restrict__
         }
         sa1[r * 48 + kd] = a;
     }
-    __syncthreads();
+    grp.sync();
     for (int ri = warp; ri < nr; ri += NT / 32) {
         double e = w64[W64_B2 + lane], o = 0.0;  // two chains: even / odd input channels
 #pragma unroll 4
@@ -210,14 +216,16 @@ __device__ double group_partial(const ap_selector& s, const double* __restrict__
         for (int off = 16; off; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
         if (lane == 0) srow[ri] = r;
     }
-    __syncthreads();
+    grp.sync();
     double tot = 0.0;
     for (int ri = 0; ri < nr; ++ri) tot += srow[ri];  // fixed order
     return tot;
 }
 
 // Re-emit map m's middle blocks: A plus the `need` best re-scored candidates, ascending.
-__device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/, int* scan_tmp) {
+template <class G = CtaGroup>
+__device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/, int* scan_tmp, const G& grp = G{}) {
+    const int tid = grp.tid();
     const int* rec = s.tie_ws + rec_off(s.n_maps) + (int64_t)m * REC;
     const int NB = __ldcg(rec + R_NB), need = __ldcg(rec + R_NEED), W = __ldcg(rec + R_W);
     const uint32_t klo = (uint32_t)__ldcg(rec + R_KLO), khi = (uint32_t)__ldcg(rec + R_KHI);
@@ -225,7 +233,7 @@ __device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/,
               local_hi = __ldcg(rec + R_LOCAL_HI);
     const int* ids = rec + OFF_IDS;
     const double* sc = reinterpret_cast<const double*>(rec + OFF_SC);
-    for (int j = threadIdx.x; j < NB; j += NT) {
+    for (int j = tid; j < NB; j += NT) {
         const int id = __ldcg(ids + j);
         const double v = __ldcg(sc + j);
         int rank = 0;
@@ -235,13 +243,13 @@ __device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/,
         }
         flags[j] = rank < need;
     }
-    __syncthreads();
+    grp.sync();
     const float* row = s.scores + (int64_t)m * s.w_max;
     auto keyof = [&](int i) -> uint32_t {
         const bool masked = i < sink_hi || (i >= local_lo && i < local_hi);
         return masked ? 0u : order_key(row[i]);
     };
-    const int per = (W + NT - 1) / NT, lo = min(W, (int)threadIdx.x * per), hi = min(W, lo + per);
+    const int per = (W + NT - 1) / NT, lo = min(W, (int)tid * per), hi = min(W, lo + per);
     int c0 = 0;  // first candidate at or after lo
     while (c0 < NB && __ldcg(ids + c0) < lo) ++c0;
     int n_sel = 0, c = c0;
@@ -251,12 +259,12 @@ __device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/,
         else if (key >= klo && key <= khi) n_sel += flags[c++];
     }
     int total = 0;
-    int pos = block_excl_scan<NT>(n_sel, scan_tmp, total);
+    int pos = group_excl_scan<NT>(n_sel, scan_tmp, total, grp);
     const int words = (s.w_max + 31) / 32;
     uint32_t* mask = s.mid_mask + (int64_t)m * words;
     int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
-    for (int w = threadIdx.x; w < words; w += NT) mask[w] = 0u;
-    __syncthreads();
+    for (int w = tid; w < words; w += NT) mask[w] = 0u;
+    grp.sync();
     c = c0;
     for (int i = lo; i < hi; ++i) {
         const uint32_t key = keyof(i);
@@ -269,43 +277,65 @@ __device__ void finalize(const ap_selector& s, int m, int* flags /*[CAP] smem*/,
     }
 }
 
-__global__ void __launch_bounds__(NT) refine_kernel(ap_selector s, Params tp) {
-    __shared__ double sx[(MAX_RG + 4) * 5];
-    __shared__ double sa1[(MAX_RG + 2) * 48];
-    __shared__ double srow[MAX_RG];
-    __shared__ int s_unit, s_last;
-    __shared__ int flags[CAP];
-    __shared__ int scan_tmp[NT / 32 + 2];
+// One unit of the fp64 re-scoring ((map * CAP + candidate) * NG + group): the group's partial, the
+// candidate's score once its last group is in, the map's re-emission once its last candidate is.
+// All threads of grp (NT of them).
+template <class G>
+__device__ void refine_unit(const ap_selector& s, const Params& tp, int unit, double* sx, double* sa1, double* srow,
+                            int* flags, int* scan_tmp, int* s_last, const G& grp) {
     int* ws = s.tie_ws;
     const double* w64 = tp.w64;
-    for (;;) {
-        if (threadIdx.x == 0) s_unit = atomicAdd(&ws[H_NEXT], 1);
-        __syncthreads();
-        const int u = s_unit;
-        if (u >= __ldcg(&ws[H_UNITS])) break;
-        const int unit = __ldcg(&ws[HDR + u]);  // (map * CAP + candidate) * NG + group
-        const int g = unit % NG, j = (unit / NG) % CAP, m = unit / (NG * CAP);
-        int* rec = ws + rec_off(s.n_maps) + (int64_t)m * REC;
-        const int col = __ldcg(rec + OFF_IDS + j);
-        const double part = group_partial(s, w64, m, col, g, sx, sa1, srow);
-        if (threadIdx.x == 0) {
-            double* parts = reinterpret_cast<double*>(rec + OFF_PARTS) + j * NG;
-            parts[g] = part;
+    const int g = unit % NG, j = (unit / NG) % CAP, m = unit / (NG * CAP);
+    int* rec = ws + rec_off(s.n_maps) + (int64_t)m * REC;
+    const int col = __ldcg(rec + OFF_IDS + j);
+    const double part = group_partial(s, w64, m, col, g, sx, sa1, srow, grp);
+    if (grp.tid() == 0) {
+        double* parts = reinterpret_cast<double*>(rec + OFF_PARTS) + j * NG;
+        parts[g] = part;
+        __threadfence();
+        *s_last = 0;
+        if (atomicSub(rec + OFF_CPEND + j, 1) == 1) {  // last group of this candidate
             __threadfence();
-            s_last = 0;
-            if (atomicSub(rec + OFF_CPEND + j, 1) == 1) {  // last group of this candidate
-                __threadfence();
-                double tot = 0.0;
-                for (int q = 0; q < NG; ++q) tot += __ldcg(parts + q);  // fixed order
-                reinterpret_cast<double*>(rec + OFF_SC)[j] = w64[W64_B3] + tot / s.history;
-                __threadfence();
-                s_last = atomicSub(rec + R_PENDING, 1) == 1;  // last candidate of this map
-                if (s_last) __threadfence();
-            }
+            double tot = 0.0;
+            for (int q = 0; q < NG; ++q) tot += __ldcg(parts + q);  // fixed order
+            reinterpret_cast<double*>(rec + OFF_SC)[j] = w64[W64_B3] + tot / s.history;
+            __threadfence();
+            *s_last = atomicSub(rec + R_PENDING, 1) == 1;  // last candidate of this map
+            if (*s_last) __threadfence();
+        }
+    }
+    grp.sync();
+    if (*s_last) finalize(s, m, flags, scan_tmp, grp);
+    grp.sync();
+}
+
+// Shared-memory scratch of one re-scoring group.
+struct RefineSmem {
+    double sx[(MAX_RG + 4) * 5];
+    double sa1[(MAX_RG + 2) * 48];
+    double srow[MAX_RG];
+    int flags[CAP];
+    int scan_tmp[NT / 32 + 2];
+    int unit, val, last;
+};
+
+// Separate-launch form (after the top-k kernel: every unit is listed before this starts).  A template
+// so that only the translation unit launching it (topk.cu) instantiates it.
+template <int = 0>
+__global__ void __launch_bounds__(NT) refine_kernel(ap_selector s, Params tp) {
+    __shared__ RefineSmem sm;
+    int* ws = s.tie_ws;
+    for (;;) {
+        if (threadIdx.x == 0) sm.unit = atomicAdd(&ws[H_NEXT], 1);
+        __syncthreads();
+        const int u = sm.unit;
+        if (u >= __ldcg(&ws[H_UNITS])) break;
+        if (threadIdx.x == 0) {
+            sm.val = __ldcg(&ws[HDR + u]) - 1;
+            ws[HDR + u] = 0;  // cleared for the next step
         }
         __syncthreads();
-        if (s_last) finalize(s, m, flags, scan_tmp);
-        __syncthreads();
+        refine_unit(s, tp, sm.val, sm.sx, sm.sa1, sm.srow, sm.flags, sm.scan_tmp, &sm.last, CtaGroup{});
     }
     if (threadIdx.x == 0) {  // the last CTA out resets the work list for the next step
         __threadfence();

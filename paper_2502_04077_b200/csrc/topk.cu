@@ -13,7 +13,7 @@
 #include <cstring>
 
 #include "common.cuh"
-#include "tieguard.cuh"
+#include "select.cuh"
 
 namespace ap {
 
@@ -225,8 +225,15 @@ __global__ void __launch_bounds__(NT) sel_topk_kernel(ap_selector s, tie::Params
 // Register-resident variant for rows of <= NT * IPT blocks (the usual case: W = 2048 at 32K): thread
 // t owns blocks [t * IPT, t * IPT + IPT), loaded once; the radix passes and the ordered emission run
 // on registers (the generic kernel re-reads the row from global memory on every pass).
+#ifdef AP_TOPK_TRACE  // profiling only: CTA 0's phase clocks of the last launch
+__device__ long long g_topk_trace[16];
+#define TOPK_TRACE(e) if (blockIdx.x == 0 && threadIdx.x == 0) g_topk_trace[e] = clock64();
+#else
+#define TOPK_TRACE(e)
+#endif
 template <int NT, int IPT>
 __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Params tp) {
+    TOPK_TRACE(0);
     __shared__ int hist[256];
     __shared__ int scan_tmp[NT / 32 + 2];
     __shared__ int s_nan, s_amax, s_bcast;
@@ -244,6 +251,7 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
         s_kmx = 0u;
     }
     __syncthreads();
+    TOPK_TRACE(1);
     int count = st.n_mid;
     int tie_n = 0;
     if (update && s.k_mid > 0 && st.width > 0) {
@@ -296,6 +304,7 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
         block_excl_scan<NT>(n_masked_local, scan_tmp, n_masked);
         if (s_nan) raise_status(s.status, AP_ENUMERIC);
         const int available = W - n_masked;
+        TOPK_TRACE(2);
         // per-map middle budget (budget allocation policy; selector.py:47-50 per map), capped by the pitch
         const int kcap = s.k_map ? min(max(s.k_map[m], 0), s.k_mid) : s.k_mid;
         const int k = kcap < available ? kcap : available;
@@ -335,6 +344,10 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
             }
             const uint32_t T = prefix;
             const int take_eq = remaining;
+            TOPK_TRACE(3);
+#ifdef AP_TOPK_TRACE
+            if (blockIdx.x == 0 && threadIdx.x == 0) g_topk_trace[8] = first + 1;
+#endif
             // ordered emission: keys > T and the lowest-index take_eq keys == T, ascending
             int n_eq = 0;
 #pragma unroll
@@ -366,6 +379,7 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
             for (int wq = 0; wq < (IPT + 31) / 32 + 1; ++wq)
                 if (bits[wq]) atomicOr(&mask[(i0 >> 5) + wq], bits[wq]);
             count = total;
+            TOPK_TRACE(4);
             if (tp.enabled && s.tie_ws) {
                 auto kf = [&](int i) -> uint32_t {
                     const bool masked = (i < sink_hi) || (i >= local_lo && i < local_hi);
@@ -374,6 +388,7 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
                 tie_n = tie::detect<NT>(s, tp, m, kf, W, k, T, __int_as_float(s_amax), sink_hi, local_lo, local_hi,
                                         scan_tmp, &s_bcast);
             }
+            TOPK_TRACE(5);
         } else {
             count = 0;
         }
@@ -393,6 +408,13 @@ __global__ void __launch_bounds__(NT) sel_topk_reg_kernel(ap_selector s, tie::Pa
         st.counter += 1;
         s.state[m] = st;
     }
+    TOPK_TRACE(6);
+}
+
+template <int NT, int IPT>
+__global__ void __launch_bounds__(NT) sel_topk_band_kernel(ap_selector s, tie::Params tp) {
+    __shared__ SelSmem<NT, IPT> sh;
+    select_map<NT, IPT>(s, tp, blockIdx.x, CtaGroup{}, sh);
 }
 
 // Warp-per-map variant (opt-in, slower: see launch_sel_topk) for rows of <= 32 * IPT blocks (W = 2049 at 32K needs IPT 72): lane l owns blocks
@@ -497,29 +519,39 @@ __global__ void __launch_bounds__(64) sel_topk_warp_kernel(ap_selector s, tie::P
 }
 
 void launch_sel_topk(const ap_selector& s, const tie::Params& tp, cudaStream_t stream) {
-    static int warp_form = -1;
+    static int warp_form = -1, radix_form = 0;
     if (warp_form < 0) {
         // opt-in (ATTNPRED_TOPK_KERNEL=warp): measured 27 us slower per 256-map launch at 32K than the
-        // CTA form (graph replay, scripts/dbg/forecast_knobs.py: 145.4 vs 118.8 us with the forecaster)
+        // CTA form (graph replay, scripts/dbg/forecast_knobs.py: 145.4 vs 118.8 us with the forecaster);
+        // ATTNPRED_TOPK_KERNEL=radix: the 8-bit radix CTA form the range-bin kernel replaced
         const char* e = getenv("ATTNPRED_TOPK_KERNEL");
         warp_form = e && strcmp(e, "warp") == 0;
+        radix_form = e && strcmp(e, "radix") == 0;
     }
     const unsigned wgrid = (unsigned)((s.n_maps + 1) / 2);
     if (warp_form && s.w_max <= 32 * 16) sel_topk_warp_kernel<16><<<wgrid, 64, 0, stream>>>(s, tp);
     else if (warp_form && s.w_max <= 32 * 72) sel_topk_warp_kernel<72><<<wgrid, 64, 0, stream>>>(s, tp);
+    else if (!radix_form && s.w_max <= 256 * 8) sel_topk_band_kernel<256, 8><<<s.n_maps, 256, 0, stream>>>(s, tp);
+    else if (!radix_form && s.w_max <= 256 * 16) sel_topk_band_kernel<256, 16><<<s.n_maps, 256, 0, stream>>>(s, tp);
     else if (s.w_max <= 256 * 8) sel_topk_reg_kernel<256, 8><<<s.n_maps, 256, 0, stream>>>(s, tp);
     else if (s.w_max <= 256 * 16) sel_topk_reg_kernel<256, 16><<<s.n_maps, 256, 0, stream>>>(s, tp);
     else sel_topk_kernel<256><<<s.n_maps, 256, 0, stream>>>(s, tp);
     if (tp.enabled && s.tie_ws) {
         static int grid = 0;
         if (!grid) grid = 4 * ap_device_sm_count();
-        tie::refine_kernel<<<grid, tie::NT, 0, stream>>>(s, tp);
+        tie::refine_kernel<><<<grid, tie::NT, 0, stream>>>(s, tp);
     }
 }
 
 }  // namespace ap
 
 using namespace ap;
+
+#ifdef AP_TOPK_TRACE
+extern "C" int ap_debug_topk_trace(long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, g_topk_trace, sizeof(long long) * 16) == cudaSuccess ? AP_OK : AP_ECUDA;
+}
+#endif
 
 extern "C" int64_t ap_sel_tie_ws_bytes(int32_t n_maps) {
     return n_maps < 1 ? 0 : 4 * tie::ws_words(n_maps);

@@ -21,3 +21,7 @@ v = (a[:, 3] - a[:, 2]) / 1000.0
 print(f"drain (exit - last band issued) median {np.median(v):.2f} us")
 v = (a[:, 1] - a[:, 0]) / 1000.0
 print(f"setup (TMEM alloc, B tile, barriers) median {np.median(v):.2f} us")
+if a.shape[0] and a[:, 5].max() > 0:  # fused selection: all roles done, group 0's selections done
+    for name, col in [("roles_done", 5), ("group0_selected", 6)]:
+        v = us(a[:, col])
+        print(f"{name:15s} min {v.min():8.2f}  median {np.median(v):8.2f}  max {v.max():8.2f} us")

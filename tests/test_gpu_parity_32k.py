@@ -55,7 +55,7 @@ def _rows(rng, n_maps, t, group):
     return r.reshape(n_maps, group, t).max(axis=1)
 
 
-def run_parity(pool, n_maps, t0, steps, group, seed, precision="fp16x3", w_max=None):
+def run_parity(pool, n_maps, t0, steps, group, seed, precision="fp16x3", w_max=None, fused=False):
     """Drive device and oracle side by side; returns (mismatches, worst err/band, tie stats, worst score err)."""
     import torch
     from paper_2502_04077_b200 import predictor
@@ -69,7 +69,7 @@ def run_parity(pool, n_maps, t0, steps, group, seed, precision="fp16x3", w_max=N
     predictor.install_weights(predictor.PredictorWeights.from_flat(w.flat()))
     H = cfg.history
     w_max = w_max or -(-(t0 + steps) // 16)
-    dev = BatchedSelector(cfg, n_maps, w_max=w_max, precision=precision)
+    dev = BatchedSelector(cfg, n_maps, w_max=w_max, precision=precision, fused=fused)
     prefill = []
     for i in range(H - 1):
         p = _rows(rng, n_maps, t0 - (H - 1) + i, group)
@@ -108,6 +108,8 @@ def run_parity(pool, n_maps, t0, steps, group, seed, precision="fp16x3", w_max=N
                 fin_mask = np.isfinite(masked)
                 e = np.abs(scores[m, :W].astype(np.float64) - want)[fin_mask].max()
                 worst_band = max(worst_band, e / band)
+    if fused:  # every map's chunk counter returned to zero for the next launch
+        assert int(dev.fused_done.abs().sum().item()) == 0
     return mismatches, worst_band, dev.tie_stats(), worst_score
 
 
@@ -120,6 +122,29 @@ def test_selection_parity_32k(pkg_loaded, pool, group):
     assert mism == 0, f"{mism} map-steps chose different middle blocks than the float64 oracle"
     assert worst_band <= 0.5, f"forecast error reaches {worst_band:.3g} of the guard band (premise: <= 0.5)"
     assert tie["overflow"] == 0
+
+
+def test_selection_parity_32k_fused(pkg_loaded, pool):
+    """The single-launch form (forecast + top-k + guard in the forecaster kernel, ap_selector.fused_done)
+    selects exactly what the oracle does, and leaves every per-map chunk counter at zero."""
+    mism, worst_band, tie, worst_score = run_parity(pool, 64, 32760, 12, 4, seed=4, fused=True)
+    print(f"32K fused: mismatches={mism}, worst forecast err/bound={worst_score:.3g}, guard={tie}")
+    assert mism == 0
+    assert tie["overflow"] == 0
+
+
+def test_selection_parity_wide_guard_band_fused(pkg_loaded, pool):
+    """Wide guard band through the fused launch: the in-kernel fp64 re-scoring (units taken by every
+    CTA from the shared list) must re-emit the oracle's ids."""
+    from paper_2502_04077_b200 import _lib
+    _lib.check(_lib.fn("ap_sel_set_tie_guard")(1, ctypes.c_float(1e-3), ctypes.c_float(FLOOR)))
+    try:
+        mism, _, tie, _ = run_parity(pool, 32, 4070, 8, 1, seed=9, fused=True)
+    finally:
+        _lib.check(_lib.fn("ap_sel_set_tie_guard")(1, ctypes.c_float(REL), ctypes.c_float(FLOOR)))
+    print(f"wide band fused: mismatches={mism}, guard={tie}")
+    assert tie["refined_maps"] > 0
+    assert mism == 0
 
 
 def test_selection_parity_wide_guard_band(pkg_loaded, pool):
