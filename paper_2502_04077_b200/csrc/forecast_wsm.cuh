@@ -66,7 +66,8 @@ constexpr int NCONV_T = NCONV * 32;
 // Fused selection (FUSE): once a CTA has no more bands, its warps split into four groups of four that run
 // kernel 3 (top-k + exact-boundary guard) on the CTA's maps (map m on CTA m % gridDim.x) as soon as every
 // chunk of the map is forecast, then help with the guard's fp64 re-scoring.
-constexpr int SEL_NT = 128, SEL_IPT = 24;   // rows of <= 3072 blocks (48K tokens at b = 16)
+constexpr int SEL_NT = 128;                 // guard re-scoring group (tie::NT)
+constexpr int SEL_IPT = 8;                  // selection by the whole CTA: rows of <= NT * 8 = 4096 blocks
 constexpr int NGRP = NT / SEL_NT;
 constexpr int QN = 256;                     // arrival queue: ((map + 1) << 3 | arrivals) events, 1 = end
 constexpr int BAR_EPI = 7, BAR_GRP0 = 8;    // named barriers: epilogue warps at the end, select group g
@@ -134,8 +135,8 @@ struct Smem {
     static constexpr int off_ainfo = off_info + NA * (int)sizeof(Meta);         // EpiInfo[NA]
     static constexpr int off_eold = (off_ainfo + NA * (int)sizeof(EpiInfo) + 15) / 16 * 16;  // EOld[NA]
     // FUSE, after the last band: per select group SelSmem + RefineSmem over the (then idle) a1 tiles
-    static constexpr int kSel = ((int)sizeof(SelSmem<SEL_NT, SEL_IPT>) + 15) / 16 * 16;
-    static constexpr int kGrp = (kSel + (int)sizeof(tie::RefineSmem) + 15) / 16 * 16;
+    static constexpr int kSel = ((int)sizeof(SelSmem<NT, SEL_IPT>) + 15) / 16 * 16;
+    static constexpr int kGrp = ((int)sizeof(tie::RefineSmem) + 15) / 16 * 16;
     static constexpr int off_grp = off_a1;
     // arrival queue int[QN], tail, head
     static constexpr int off_q = (off_eold + NA * (int)sizeof(EOld) + 15) / 16 * 16;
@@ -156,8 +157,8 @@ __device__ __forceinline__ void ring_push(int* q, int cap, int v) {  // q[cap] =
     while (slot - ld_volatile(&q[cap + 1]) >= cap) __nanosleep(64);
     st_volatile(&q[slot % cap], v);
 }
-__device__ __forceinline__ void sel_arrive(uint8_t* smem, int map, int n) {
-    __threadfence_block();  // the arriving warp's score stores before the event
+__device__ __forceinline__ void sel_arrive(uint8_t* smem, int map, int n, int dbg) {
+    if (!(dbg & 256)) __threadfence_block();  // the arriving warp's score stores before the event
     ring_push(reinterpret_cast<int*>(smem + Smem::off_q), QN, ((map + 1) << 3) | n);
 }
 
@@ -178,7 +179,7 @@ __device__ __forceinline__ void band_segs(int full, int lo2, int H, int bi, int 
     }
 }
 
-static_assert(NGRP * Smem::kGrp <= NA * Smem::kA1, "select scratch fits the a1 tiles");
+static_assert(Smem::kSel + NGRP * Smem::kGrp <= NA * Smem::kA1, "select scratch fits the a1 tiles");
 
 template <int PREC, bool FUSE>
 __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) {
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
     const int H = P.H;
     const bool sel = P.state != nullptr;
     const int dbg = P.debug;  // profiling only: 1 no conv1 arithmetic, 2 no MMAs, 4 no epilogue arithmetic,
-                              // 64 no accumulator clearing
+                              // 64 no accumulator clearing, 128 / 256 no fence at fused arrival counting / queuing
     if (tid == 0) WSM_CTA(0, gtimer());
 
     {  // B operands once per persistent CTA; barriers; TMEM
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
             if (have && P.state) st = P.state[map];
             const Task T = have ? plan_task(P, st, chunk) : Task{true, true, false, 0, 0, 0};
             const bool live = have && !T.skip;
-            if (FUSE && have && !live) sel_arrive(smem, map, NEPI);  // nothing to forecast: the whole count
+            if (FUSE && have && !live) sel_arrive(smem, map, NEPI, dbg);  // nothing to forecast: the whole count
             const int base_slot = sel ? slot_of(row_index(T.n_pushed, H, 0), H) : 0;
             const int first_real = (!sel || T.n_pushed >= H) ? 0 : (int)(H - T.n_pushed);
             unsigned todo = __ballot_sync(0xffffffffu, live);
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
             }
             if (FUSE && last) {
                 __syncwarp();
-                if (lane == 0) sel_arrive(smem, mapi, 1);
+                if (lane == 0) sel_arrive(smem, mapi, 1, dbg);
             }
         }
         if (FUSE) {  // every epilogue warp's arrivals are in: no more maps complete in this CTA
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                     continue;
                 }
                 st_volatile(&q[QN + 1], head);
-                __threadfence();  // the arrivals' score stores (CTA-scope ordered before the events) before the counts
+                if (!(dbg & 128)) __threadfence();  // the arrivals' score stores (CTA-ordered before the events) before the counts
                 for (int i = 0; i < n_ev; ++i) {
                     if (evs[i] == 1) end = true;
                     else atomicAdd(&P.sel.fused_done[(evs[i] >> 3) - 1], evs[i] & 7);
@@ -739,26 +740,25 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
 
     if (FUSE) {
         // ------------------------------------------------------------------ selection (kernel 3)
-        // this CTA has no more bands: group g (warps 4g .. 4g+3, together once each has left its role)
-        // selects maps blockIdx.x + (g + NGRP j) * gridDim.x, each once all its chunks' arrivals are counted
+        // this CTA has no more bands: the whole CTA selects maps blockIdx.x + j * gridDim.x, each once all
+        // its chunks' arrivals are counted; then groups of four warps help with the guard's re-scoring
+        auto& sh = *reinterpret_cast<SelSmem<NT, SEL_IPT>*>(smem + Smem::off_grp);
         const RtGroup grp{warp / 4};
         const int gt = grp.tid();
-        uint8_t* gs = smem + Smem::off_grp + grp.g * Smem::kGrp;
-        auto& sh = *reinterpret_cast<SelSmem<SEL_NT, SEL_IPT>*>(gs);
-        auto& rs = *reinterpret_cast<tie::RefineSmem*>(gs + Smem::kSel);
+        auto& rs = *reinterpret_cast<tie::RefineSmem*>(smem + Smem::off_grp + Smem::kSel + grp.g * Smem::kGrp);
         const int target = NEPI * P.n_chunks;
-        __syncthreads();  // every role is done (the last MMAs too): the a1 tiles are free for the group scratch
+        __syncthreads();  // every role is done (the last MMAs too): the a1 tiles are free for the scratch
         if (tid == 0) WSM_CTA(5, gtimer());
-        for (int m = blockIdx.x + grp.g * gridDim.x; m < P.n_maps; m += NGRP * gridDim.x) {
-            if (gt == 0) {
+        for (int m = blockIdx.x; m < P.n_maps; m += gridDim.x) {
+            if (tid == 0) {
                 while (ld_volatile(&P.sel.fused_done[m]) != target) __nanosleep(128);
                 __threadfence();  // every chunk's scores before the selection reads them
             }
-            grp.sync();
-            select_map<SEL_NT, SEL_IPT>(P.sel, P.tp, m, grp, sh);
-            if (gt == 0) P.sel.fused_done[m] = 0;  // every arrival of this launch is in: reset for the next
+            __syncthreads();
+            select_map<NT, SEL_IPT>(P.sel, P.tp, m, CtaGroup{}, sh);
+            if (tid == 0) P.sel.fused_done[m] = 0;  // every arrival of this launch is in: reset for the next
         }
-        if (gt == 0 && grp.g == 0) WSM_CTA(6, gtimer());
+        if (tid == 0) WSM_CTA(6, gtimer());
         int* ws = P.sel.tie_ws;
         if (P.tp.enabled && ws) {
             // exact-boundary guard: fp64 re-scoring units of every CTA's maps, taken from the shared list as

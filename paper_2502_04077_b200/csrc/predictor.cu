@@ -851,11 +851,11 @@ int ap_predict_forward(const float* grids, int32_t n_grids, int32_t H, int32_t W
 static int sel_step_impl(const ap_selector* s, int precision, int grid_cap, void* stream);
 
 // Forecast + top-k (+ guard) as one launch when the descriptor carries fused_done: the warp-specialised
-// tensor-core forecaster selects its maps after its last band (rows of <= SEL_NT * SEL_IPT blocks); other
+// tensor-core forecaster selects its maps after its last band (rows of <= NT * SEL_IPT blocks); other
 // precisions / kernels / widths take the separate top-k launch.
 static bool fused_select(const ap_selector& s, int precision) {
     return s.fused_done && s.k_mid > 0 && (precision == AP_PREC_F16X3 || precision == AP_PREC_F16) &&
-           tc_kernel() == 3 && s.w_max % 4 == 0 && s.w_max <= wsm::SEL_NT * wsm::SEL_IPT;
+           tc_kernel() == 3 && s.w_max % 4 == 0 && s.w_max <= wsm::NT * wsm::SEL_IPT;
 }
 
 int ap_sel_step(const ap_selector* s, int precision, void* stream) { return sel_step_impl(s, precision, 0, stream); }

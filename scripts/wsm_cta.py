@@ -3,7 +3,7 @@ producer's last band, exit, bands per CTA — for the last launch of scripts/ben
 import ctypes, os, sys, runpy
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["ATTNPRED_FORECAST_DEBUG"] = "32"
+os.environ["ATTNPRED_FORECAST_DEBUG"] = str(32 | int(os.environ.get("ATTNPRED_FORECAST_DEBUG", "0")))
 from paper_2502_04077_b200 import _lib
 sys.argv = ["bench_select.py", "--heads", os.environ.get("HEADS", "8"), "--steps", "2", "--warmup", "1"]
 runpy.run_path(os.path.join(os.path.dirname(__file__), "bench_select.py"), run_name="__main__")
