@@ -19,6 +19,9 @@ namespace wsm {
 #ifndef AP_WSM_NCONV
 #define AP_WSM_NCONV 10
 #endif
+#ifndef AP_CNT_SLEEP
+#define AP_CNT_SLEEP 64
+#endif
 #ifndef AP_WSM_NX
 #define AP_WSM_NX 4
 #endif
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(NT, 1) conv_forecast_wsm_kernel(ConvParams P) 
                     evs[n_ev++] = v;
                 }
                 if (!n_ev) {
-                    __nanosleep(64);
+                    __nanosleep(AP_CNT_SLEEP);  // rarely: this warp shares a scheduler with the MMA issuer
                     continue;
                 }
                 st_volatile(&q[QN + 1], head);
