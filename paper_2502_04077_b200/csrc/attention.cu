@@ -1316,7 +1316,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 
 // grid (n_splits, Hkv, S), one wave (every CTA resident; the splits of a KV head wait for each other
 // once, for the LSE); 256 threads.  P.counters[s * Hq + h0]: split arrivals (self-resetting);
-// P.counters[S * Hq + s * Hq + h0]: LSE-ready epoch (= the map's n_pushed + 1 of this step).
+// partial[(s, h0, split)][2]: split's (m, l)-published epoch (= the map's n_pushed + 1 of this step).
 template <int NH>
 __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_constant__ CUtensorMap kmap,
                                                                   AttnParams P) {
@@ -1442,6 +1442,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_c
                 }
             }
         }
+        if (warp == 2) ATT_TRACE2(3);  // this epilogue warp's last tile
         // (m, l) of the split: over the 32 lanes, then the 4 warps
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
@@ -1474,38 +1475,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_c
         part[0] = M;
         part[1] = L;
     }
-    // ---- the last split of this KV head combines the (m, l) into the LSE and publishes it
-    volatile int32_t* ready = P.counters + (int64_t)P.n_seq * P.n_q_heads + (int64_t)s * P.n_q_heads + h0;
     const int64_t W = (t + P.block - 1) / P.block;
     ATT_TRACE(7);
-    if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) {
-        ATT_TRACE(8);
-        if (warp < NH) {  // warp h: lane = split (one round trip for all partials)
-            const int h = warp;
-            const float* part = P.partial + ((int64_t)s * P.n_q_heads + h0 + h) * P.n_splits * (HD + 2);
-            const float ms = lane < P.n_splits ? __ldcg(part + lane * (HD + 2)) : -INFINITY;
-            const float ls = lane < P.n_splits ? __ldcg(part + lane * (HD + 2) + 1) : 0.f;
-            float M = ms;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-            float L = (ms == -INFINITY) ? 0.f : ls * exp2f(ms - M);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
-            if (lane == 0) {
-                const float lse = M + log2f(L);
-                if (P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = lse;
-                P.partial[((int64_t)s * P.n_q_heads + h0 + h) * P.n_splits * (HD + 2) + 2] = lse;
-            }
-        }
-        if (threadIdx.x < NH / P.group + (NH % P.group != 0)) {  // per map: the row max starts from 0
+    if (split == 0) {  // before split 0 publishes: the row maxima start from 0, the ring row is zero beyond W
+        if (threadIdx.x < NH / P.group + (NH % P.group != 0)) {
             const int map = s * P.maps_per_seq + P.map_base + (h0 + threadIdx.x * P.group) / P.group;
             P.sel.slot_xmax[(int64_t)map * Hh + (int)((epoch - 1) % Hh)] = 0.f;
         }
-        __syncthreads();
-        if (threadIdx.x == 0)  // release: the LSE and the xmax resets above, ordered by the barrier
-            asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(ready), "r"((int32_t)epoch) : "memory");
-        ATT_TRACE(9);
-        for (int g0 = 0; g0 < NH; g0 += P.group) {  // zero the ring row beyond W (rarely any)
+        for (int g0 = 0; g0 < NH; g0 += P.group) {  // (rarely any)
             const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;
             const int slot = (int)((epoch - 1) % Hh);
             float* dst = P.sel.ring + ((int64_t)map * Hh + slot) * P.sel.w_max;
@@ -1513,20 +1490,70 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_c
             for (int64_t j = W + threadIdx.x; j < old_w; j += ATT_THREADS) dst[j] = 0.f;
         }
     }
-    // ---- every split emits the compressed-row values of its own blocks once the LSE is out
-    if (threadIdx.x == 0) {
-        int32_t v;
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
-            if (v == (int32_t)epoch) break;
-            __nanosleep(32);
+    // ---- every split publishes its (m, l) with this step's epoch and combines all splits' itself (no
+    // last-split hop: the LSE is ready one round trip after the slowest split's partials land)
+    int* flag0 = reinterpret_cast<int*>(P.partial + ((int64_t)s * P.n_q_heads + h0) * P.n_splits * (HD + 2) + 2);
+    __syncthreads();  // this split's partials (and split 0's resets) before its flag
+    if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" :: "l"(flag0 + split * (HD + 2)), "r"((int32_t)epoch) : "memory");
+    if (warp == 0) {  // one warp waits for every split's epoch (lane = split), with back-off: 144 CTAs
+                      // x 18 flags of acquire-polling otherwise crowd the flags' L2 lines
+        for (int r0 = 0; r0 < P.n_splits; r0 += 32) {
+            const int r = r0 + lane;
+            int v = (int32_t)epoch;
+            if (r < P.n_splits)
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag0 + r * (HD + 2)) : "memory");
+                    if (v == (int32_t)epoch) break;
+                    __nanosleep(64);
+                }
+        }
+    }
+    __syncthreads();
+    if (warp < NH) {  // warp h: lanes over the splits
+        const int h = warp;
+        const float* part = P.partial + ((int64_t)s * P.n_q_heads + h0 + h) * P.n_splits * (HD + 2);
+        float M = -INFINITY, L = 0.f;
+        if (P.n_splits <= 32) {  // lane = split (the fixed order of the previous last-split combine)
+            float ms = -INFINITY, ls = 0.f;
+            if (lane < P.n_splits) {
+                ms = __ldcg(part + lane * (HD + 2));
+                ls = __ldcg(part + lane * (HD + 2) + 1);
+            }
+            M = ms;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+            L = (ms == -INFINITY) ? 0.f : ls * exp2f(ms - M);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+        } else {
+            for (int r0 = 0; r0 < P.n_splits; r0 += 32) {
+                const int r = r0 + lane;
+                if (r < P.n_splits) {
+                    const float ms = __ldcg(part + r * (HD + 2)), ls = __ldcg(part + r * (HD + 2) + 1);
+                    if (ms != -INFINITY) {
+                        const float mn = fmaxf(M, ms);
+                        L = L * exp2f(M - mn) + ls * exp2f(ms - mn);
+                        M = mn;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {  // (m, l) over the lanes
+                const float Mo = __shfl_xor_sync(0xffffffffu, M, o), Lo = __shfl_xor_sync(0xffffffffu, L, o);
+                const float mn = fmaxf(M, Mo);
+                L = (M == -INFINITY ? 0.f : L * exp2f(M - mn)) + (Mo == -INFINITY ? 0.f : Lo * exp2f(Mo - mn));
+                M = mn;
+            }
+        }
+        if (lane == 0) {
+            const float lse = M + log2f(L);
+            s_lse[h] = lse;
+            if (split == 0 && P.lse) P.lse[(int64_t)s * P.n_q_heads + h0 + h] = lse;
         }
     }
     __syncthreads();
     ATT_TRACE(4);
-    if (threadIdx.x < NH)
-        s_lse[threadIdx.x] = __ldcg(P.partial + ((int64_t)s * P.n_q_heads + h0 + threadIdx.x) * P.n_splits * (HD + 2) + 2);
-    __syncthreads();
     for (int g0 = 0; g0 < NH; g0 += P.group) {
         const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;
         const int slot = (int)((epoch - 1) % Hh);
@@ -1552,7 +1579,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1) calib_tc_kernel(const __grid_c
     // ---- map state: the last CTA to finish emitting advances it (everyone has read the old one)
     __syncthreads();
     if (last_split(P.counters + (int64_t)s * P.n_q_heads + h0, P.n_splits)) {
-        if (threadIdx.x == 0) *ready = 0;  // every split is past its wait: no stale epoch can match later
+        // every split is past its wait: clear the published epochs (the next layer's pass of this step
+        // has the same epoch)
+        for (int r = threadIdx.x; r < P.n_splits; r += ATT_THREADS) flag0[r * (HD + 2)] = 0;
         if (threadIdx.x == 0)
             for (int g0 = 0; g0 < NH; g0 += P.group) {
                 const int map = s * P.maps_per_seq + P.map_base + (h0 + g0) / P.group;

@@ -22,6 +22,6 @@ L.ap_attn_debug_trace(0, buf)
 full = np.array(buf, dtype=np.int64).reshape(16, 16)
 a = full[:, :10]
 t0 = a[a > 0].min()
-print("cta   entry   setup  tiles_done  emit_start  lse_seen  emitted  end  pre_last  is_last  published")
+print("cta   entry   setup  tiles_issued  epi_done  lse_seen  emitted  end  published  -  -")
 for r in range(16):
     if a[r, 0]: print(r, " ".join(f"{(x - a[r, 0]) if x else -1:9d}" for x in a[r]))

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-V=paper_2502_04077_b200/lib/variants
-for v in "paper_2502_04077_b200/lib/libattnpred.so" $V/s1000.so $V/s8000.so; do echo "lib=$v"; ATTNPRED_LIB=$v ATTNPRED_FUSED_SELECT=1 timeout 300 python scripts/dbg/forecast_knobs.py; ATTNPRED_LIB=$v ATTNPRED_FUSED_SELECT=1 HEADS=8 timeout 300 python scripts/wsm_cta.py 2>&1 | grep "prod_last\|exit \|roles\|group0"; done
+timeout 900 python -m pytest tests/test_gpu_attention.py tests/test_gpu_decode.py tests/test_gpu_head_split.py tests/test_gpu_prefetch.py -x -q 2>&1 | tail -3
+timeout 600 python bench.py > gpurun_out/bench_calib2.json 2> gpurun_out/bench_calib2.err; tail -c 200 gpurun_out/bench_calib2.json
