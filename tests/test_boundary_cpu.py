@@ -36,14 +36,18 @@ def test_library_loads_and_exports_every_declared_symbol():
 def test_struct_layouts_match_header(tmp_path):
     from paper_2502_04077_b200 import _lib
     src = tmp_path / "sz.c"
+    sel_fields = ("ring", "status", "tie_ws", "k_map", "fused_done")
+    st_fields = ("n_pushed", "width", "r_wgen", "tie_n", "prev_kth")
+    offs = "".join(f', offsetof(ap_selector, {f})' for f in sel_fields)
+    offs += "".join(f', offsetof(ap_map_state, {f})' for f in st_fields)
+    fmt = " ".join(["%zu"] * (2 + len(sel_fields) + len(st_fields)))
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "attnpred.h"\n'
-                   'int main(){printf("%zu %zu %zu %zu\\n", sizeof(ap_map_state), sizeof(ap_selector),'
-                   ' offsetof(ap_selector, ring), offsetof(ap_selector, status));}\n')
+                   f'int main(){{printf("{fmt}\\n", sizeof(ap_map_state), sizeof(ap_selector){offs});}}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
-    assert got == [ctypes.sizeof(_lib.MapState), ctypes.sizeof(_lib.Selector),
-                   _lib.Selector.ring.offset, _lib.Selector.status.offset]
+    assert got == [ctypes.sizeof(_lib.MapState), ctypes.sizeof(_lib.Selector)] + \
+        [getattr(_lib.Selector, f).offset for f in sel_fields] + [getattr(_lib.MapState, f).offset for f in st_fields]
 
 
 def test_status_codes_map_to_reference_exceptions():
