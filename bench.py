@@ -536,7 +536,7 @@ def roofline_for(eng, args, us, W, key):
             "traffic_source": "ncu dram__bytes_read+write of the forecaster launch, profiles/roofline_traffic.json "
                               "(not measured in this run)" if traffic is not None else None,
             "peak_kind": peak_kind,
-            "kernel": "ap_sel_step (conv_forecast_wsm_kernel + sel_topk_reg_kernel + tie refine_kernel)",
+            "kernel": "ap_sel_step (conv_forecast_wsm_kernel + sel_topk_band_kernel + tie refine_kernel)",
             "maps": n_maps,
             "us_per_launch": round(us, 2), "us_per_layer": round(us / eng.shape.n_layers, 3),
             "algorithmic_bytes_per_launch": b_alg,
