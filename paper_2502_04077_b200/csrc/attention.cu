@@ -36,10 +36,18 @@ constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ long long g_att_trace[16 * 16];  // debug: clock64 per phase, CTAs (split, 0, 0)
 __device__ int g_att_trace_on;
+// Phase traces are compiled in only with -DAP_ATT_TRACE (scripts/attn_trace.py, calib_trace.py build a
+// variant library): the on/off flag is a global load, and on thread 0 of the traced CTAs it sat on the
+// critical path of every launch (ncu: 11% of the sparse kernel's stall samples at the first trace point).
+#ifdef AP_ATT_TRACE
 #define ATT_TRACE2(e) \
     if (lane == 0 && blockIdx.y == 0 && blockIdx.z == 0 && g_att_trace_on && blockIdx.x < 16) g_att_trace[blockIdx.x * 16 + (e)] = clock64();
 #define ATT_TRACE(e) \
     if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && g_att_trace_on) g_att_trace[blockIdx.x * 16 + (e)] = clock64();
+#else
+#define ATT_TRACE2(e) do { } while (0)
+#define ATT_TRACE(e) do { } while (0)
+#endif
 
 struct AttnParams {
     int32_t n_seq, n_q_heads, n_kv_heads, t_max, n_splits, block;
@@ -896,8 +904,10 @@ __global__ void __launch_bounds__(ATT_THREADS) sparse_cluster_kernel(const __gri
     const int n_units = (int)sb + n_local + ms.n_mid;
     const int per = (n_units + CL - 1) / CL;
     const int u0 = split * per, u1 = min(n_units, u0 + per);
+#ifdef AP_ATT_TRACE
     if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && g_att_trace_on)
         g_att_trace[blockIdx.x * 16 + 12] = clock64() + (u1 & 0);  // after the state load is consumed
+#endif
     const int h0 = g * NH;
     const int kvh = h0 / (P.n_q_heads / P.n_kv_heads);
     const __nv_bfloat16* kh = P.k + ((int64_t)s * P.n_kv_heads + kvh) * P.t_max * HD;

@@ -1,4 +1,10 @@
 """Per-phase clock64 trace of the calibration (K-only dense) kernel, CTAs of KV head 0."""
+import os
+# the phase traces are compiled in only with -DAP_ATT_TRACE:
+#   SRC=attention scripts/build_wsm_variants.sh att_trace:AP_ATT_TRACE=1
+os.environ.setdefault("ATTNPRED_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                   "paper_2502_04077_b200", "lib", "variants", "att_trace.so"))
+
 import ctypes, sys, os
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
