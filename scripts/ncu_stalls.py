@@ -36,7 +36,7 @@ def main():
         st = {k[6:]: int(v) for k, v in rec.items() if k.startswith("stall_") and "Not Issued" not in k and v.isdigit() and int(v) > 0}
         lines.append((tot, f"{path}:{ln}", r[1].strip()[:60], st))
     total = sum(l[0] for l in lines) or 1
-    for tot, loc, src, st in sorted(lines, reverse=True)[:n]:
+    for tot, loc, src, st in sorted(lines, key=lambda x: (x[0], x[1]), reverse=True)[:n]:
         top = sorted(st.items(), key=lambda kv: -kv[1])[:4]
         print(f"{tot / total:6.1%} {loc:22s} {src:60s} " + " ".join(f"{k}={v}" for k, v in top))
 
