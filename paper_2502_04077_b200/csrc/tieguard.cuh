@@ -325,11 +325,12 @@ template <int = 0>
 __global__ void __launch_bounds__(NT) refine_kernel(ap_selector s, Params tp) {
     __shared__ RefineSmem sm;
     int* ws = s.tie_ws;
-    for (;;) {
-        if (threadIdx.x == 0) sm.unit = atomicAdd(&ws[H_NEXT], 1);
-        __syncthreads();
-        const int u = sm.unit;
-        if (u >= __ldcg(&ws[H_UNITS])) break;
+    // units are dealt statically (unit u on CTA u % gridDim.x: the list is complete when this launch
+    // starts), so CTAs without a unit — all of them on most steps — leave after one read, with no
+    // contended atomics
+    const int n_units = __ldcg(&ws[H_UNITS]);
+    if ((int)blockIdx.x >= n_units) return;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         if (threadIdx.x == 0) {
             sm.val = __ldcg(&ws[HDR + u]) - 1;
             ws[HDR + u] = 0;  // cleared for the next step
@@ -339,9 +340,9 @@ __global__ void __launch_bounds__(NT) refine_kernel(ap_selector s, Params tp) {
     }
     if (threadIdx.x == 0) {  // the last CTA out resets the work list for the next step
         __threadfence();
-        if (atomicAdd(&ws[H_DONE], 1) == (int)gridDim.x - 1) {
+        const int active = n_units < (int)gridDim.x ? n_units : (int)gridDim.x;
+        if (atomicAdd(&ws[H_DONE], 1) == active - 1) {
             ws[H_UNITS] = 0;
-            ws[H_NEXT] = 0;
             ws[H_DONE] = 0;
             __threadfence();
         }
