@@ -7,6 +7,22 @@
 
 namespace ap {
 
+// Nested search bands around the previous k-th score tau: half-widths 2^-2, 2^-4, 2^-6, 2^-8 of |tau|
+// (how far the boundary moves between two updates depends on the rows: on the decode engine's maps
+// the 2^-2 band holds the new boundary 99.9% of the time with ~34 keys, on tightly clustered synthetic
+// scores the 2^-8 band does with ~20; scripts/dbg/topk_stats.py)
+constexpr int TK_NB = 4;
+__device__ __forceinline__ float tk_band(int i) { return i == 0 ? 0.25f : i == 1 ? 0.0625f : i == 2 ? 0.015625f : 0.00390625f; }
+#ifdef AP_TOPK_STATS  // profiling only: [maps, boundary inside the band, fast path taken, sum of band sizes]
+__device__ int g_topk_stats[4];
+extern "C" int ap_debug_topk_stats(int* host_out) {
+    const cudaError_t e = cudaMemcpyFromSymbol(host_out, g_topk_stats, 4 * sizeof(int));
+    int z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_topk_stats, z, sizeof(z));
+    return e == cudaSuccess ? 0 : 5;
+}
+#endif
+
 // Band variant (the default for rows of <= NT * IPT blocks).  Scores move little between two updates
 // of a map (an incremental forecast changes five of H history rows), so the boundary is first looked
 // for in a narrow band around the previous update's k-th score (ap_map_state.prev_kth): one counting
@@ -25,7 +41,8 @@ struct SelSmem {  // shared memory of one map's selection by an NT-thread group
     uint32_t c_key[TK_CAND];
     int c_id[TK_CAND];
     uint32_t mask[NT * IPT / 32 + 1];
-    int nan, amax, nmask, above, band, cnt, bcast;
+    int nan, amax, nmask, cnt, bcast;
+    int above[TK_NB], band[TK_NB];  // per search band: keys above it, keys in it
     unsigned kmn, kmx, tmin;
 };
 
@@ -38,8 +55,9 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
     uint32_t* c_key = sh.c_key;
     int* c_id = sh.c_id;
     uint32_t* s_mask = sh.mask;
-    int &s_nan = sh.nan, &s_amax = sh.amax, &s_nmask = sh.nmask, &s_above = sh.above, &s_band = sh.band,
-        &s_cnt = sh.cnt, &s_bcast = sh.bcast;
+    int &s_nan = sh.nan, &s_amax = sh.amax, &s_nmask = sh.nmask, &s_cnt = sh.cnt, &s_bcast = sh.bcast;
+    int* s_above = sh.above;
+    int* s_band = sh.band;
     unsigned &s_kmn = sh.kmn, &s_kmx = sh.kmx, &s_tmin = sh.tmin;
     const int tid = grp.tid(), lane = tid & 31;
     // the row's scores are requested before the map state they depend on arrives (one round trip, not two)
@@ -67,7 +85,8 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
     if (update && s.k_mid > 0 && st.width > 0) {
         for (int w = tid; w < words; w += NT) s_mask[w] = 0u;
         if (tid == 0) {
-            s_nan = 0; s_amax = 0; s_nmask = 0; s_above = 0; s_band = 0; s_cnt = 0;
+            s_nan = 0; s_amax = 0; s_nmask = 0; s_cnt = 0;
+            for (int i = 0; i < TK_NB; ++i) s_above[i] = s_band[i] = 0;
             s_kmn = 0xffffffffu; s_kmx = 0u; s_tmin = 0xffffffffu;
         }
         const int W = st.width;
@@ -102,32 +121,43 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
                 kmx = max(kmx, key[q]);
             }
         }
-        // band around the previous k-th score: +-2^-8 |tau|
-        uint32_t blo = 1u, bhi = 0u;  // empty band: no previous boundary
-        if (kth) {
-            const float tau = tie::key_value(kth), d = fmaxf(0.00390625f * fabsf(tau), 1e-30f);
-            blo = order_key(tau - d);
-            bhi = order_key(tau + d);
-        }
-        int na = 0, nb = 0;
+        uint32_t lo_b[TK_NB], hi_b[TK_NB];  // search bands (empty without a previous boundary)
+        const float tau = tie::key_value(kth);
 #pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-            na += key[q] > bhi;
-            nb += key[q] >= blo && key[q] <= bhi;
+        for (int i = 0; i < TK_NB; ++i) {
+            const float d = fmaxf(tk_band(i) * fabsf(tau), 1e-30f);
+            lo_b[i] = kth ? order_key(tau - d) : 1u;
+            hi_b[i] = kth ? order_key(tau + d) : 0u;
         }
+        int na[TK_NB], nb[TK_NB];
+#pragma unroll
+        for (int i = 0; i < TK_NB; ++i) na[i] = nb[i] = 0;
+#pragma unroll
+        for (int q = 0; q < IPT; ++q)
+#pragma unroll
+            for (int i = 0; i < TK_NB; ++i) {
+                na[i] += key[q] > hi_b[i];
+                nb[i] += key[q] >= lo_b[i] && key[q] <= hi_b[i];
+            }
         grp.sync();  // shared state initialised
         // CTA reductions: one shared atomic per warp
         nm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nm);
-        na = (int)__reduce_add_sync(0xffffffffu, (unsigned)na);
-        nb = (int)__reduce_add_sync(0xffffffffu, (unsigned)nb);
+#pragma unroll
+        for (int i = 0; i < TK_NB; ++i) {
+            na[i] = (int)__reduce_add_sync(0xffffffffu, (unsigned)na[i]);
+            nb[i] = (int)__reduce_add_sync(0xffffffffu, (unsigned)nb[i]);
+        }
         kmn = __reduce_min_sync(0xffffffffu, kmn);
         kmx = __reduce_max_sync(0xffffffffu, kmx);
         const unsigned am = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));  // non-negative floats
         if (__any_sync(0xffffffffu, nan) && lane == 0) s_nan = 1;
         if (lane == 0) {
             atomicAdd(&s_nmask, nm);
-            if (na) atomicAdd(&s_above, na);
-            if (nb) atomicAdd(&s_band, nb);
+#pragma unroll
+            for (int i = 0; i < TK_NB; ++i) {
+                if (na[i]) atomicAdd(&s_above[i], na[i]);
+                if (nb[i]) atomicAdd(&s_band[i], nb[i]);
+            }
             atomicMin(&s_kmn, kmn);
             atomicMax(&s_kmx, kmx);
             atomicMax(&s_amax, (int)am);
@@ -139,8 +169,28 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
         const int k = kcap < available ? kcap : available;
         uint32_t take = 0u;  // bit q: block i0 + q is selected
         if (k > 0) {
-            const int above = s_above, band = s_band;
-            if (above < k && above + band >= k && band <= TK_CAND) {
+            // the narrowest band that brackets the k-th key and is small enough to rank directly
+            int sel_b = -1;
+#pragma unroll
+            for (int i = 0; i < TK_NB; ++i)
+                if (s_above[i] < k && s_above[i] + s_band[i] >= k && s_band[i] <= TK_CAND) sel_b = i;
+            const int above = sel_b >= 0 ? s_above[sel_b] : 0, band = sel_b >= 0 ? s_band[sel_b] : 0;
+            uint32_t blo = 1u, bhi = 0u;
+#pragma unroll
+            for (int i = 0; i < TK_NB; ++i)
+                if (i == sel_b) {
+                    blo = lo_b[i];
+                    bhi = hi_b[i];
+                }
+#ifdef AP_TOPK_STATS
+            if (tid == 0) {
+                atomicAdd(&g_topk_stats[0], 1);
+                if (sel_b >= 0) atomicAdd(&g_topk_stats[1], 1);
+                if (sel_b >= 0) atomicAdd(&g_topk_stats[2], 1);
+                atomicAdd(&g_topk_stats[3], band);
+            }
+#endif
+            if (sel_b >= 0) {
                 // fast path: the k-th key is in the band; rank the band's keys among themselves
                 const int need = k - above;
                 uint32_t inband = 0u;
