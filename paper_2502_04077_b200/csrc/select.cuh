@@ -309,14 +309,9 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
         grp.sync();
         for (int w = tid; w < words; w += NT) mask[w] = s_mask[w];
         kth = k > 0 ? s_tmin : 0u;
-        if (k > 0 && tp.enabled && s.tie_ws) {
-            auto kf = [&](int i) -> uint32_t {
-                const bool masked = (i < sink_hi) || (i >= local_lo && i < local_hi);
-                return masked ? 0u : order_key(sc[i]);
-            };
-            tie_n = tie::detect<NT>(s, tp, m, kf, W, k, kth, __int_as_float(s_amax), sink_hi, local_lo, local_hi,
-                                    scan_tmp, &s_bcast, grp);
-        }
+        if (k > 0 && tp.enabled && s.tie_ws)  // (the keys are still in registers: no second read of the row)
+            tie_n = tie::detect_regs<NT, IPT>(s, tp, m, key, i0, W, k, kth, __int_as_float(s_amax), sink_hi, local_lo,
+                                              local_hi, scan_tmp, hist, &s_bcast, grp);
         if (tid == 0) {
             st.n_mid = count;
             st.mid_clip = t;

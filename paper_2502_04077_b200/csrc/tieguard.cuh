@@ -100,6 +100,72 @@ __device__ int detect(const ap_selector& s, const Params& tp, int m, KeyFn keyfn
     return NB;
 }
 
+// The same for a thread group holding the map's keys in registers (thread t: blocks [i0, i0 + IPT),
+// i0 = t * IPT; key 0 = masked): the common unambiguous case costs one barrier and no global loads.
+// red: >= 2 * NTH / 32 ints of scratch shared memory.
+template <int NTH, int IPT, class G>
+__device__ int detect_regs(const ap_selector& s, const Params& tp, int m, const uint32_t (&key)[IPT], int i0, int W,
+                           int k, uint32_t T, float amax, int sink_hi, int local_lo, int local_hi, int* scan_tmp,
+                           int* red, int* s_bcast, const G& grp) {
+    const float tau = key_value(T);
+    const float band = tp.rel * fmaxf(fabsf(tau), tp.floor * amax);
+    const uint32_t khi = order_key(tau + band), klo = order_key(tau - band);
+    const int tid = grp.tid(), lane = tid & 31, warp = tid >> 5;
+    int na = 0, nb = 0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+        na += key[q] > khi;
+        nb += key[q] >= klo && key[q] <= khi;
+    }
+    const int wa = (int)__reduce_add_sync(0xffffffffu, (unsigned)na), wb = (int)__reduce_add_sync(0xffffffffu, (unsigned)nb);
+    if (lane == 0) {
+        red[warp] = wa;
+        red[NTH / 32 + warp] = wb;
+    }
+    grp.sync();
+    int NA = 0, NB = 0;
+#pragma unroll
+    for (int w = 0; w < NTH / 32; ++w) {
+        NA += red[w];
+        NB += red[NTH / 32 + w];
+    }
+    grp.sync();  // (red is reused by the caller)
+    const int need = k - NA;
+    if (NB <= need) return 0;
+    int* ws = s.tie_ws;
+    if (NB > CAP || s.history > NG * MAX_RG) {
+        if (tid == 0) atomicAdd(&ws[H_OVERFLOW], 1);
+        return -NB;
+    }
+    int tot = 0;
+    int pos = group_excl_scan<NTH>(nb, scan_tmp, tot, grp);
+    int* rec = ws + rec_off(s.n_maps) + (int64_t)m * REC;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+        if (key[q] >= klo && key[q] <= khi) rec[OFF_IDS + pos++] = i0 + q;  // ascending block ids
+    for (int j = tid; j < NB; j += NTH) rec[OFF_CPEND + j] = NG;
+    if (tid == 0) {
+        rec[R_NA] = NA;
+        rec[R_NEED] = need;
+        rec[R_NB] = NB;
+        rec[R_KLO] = (int)klo;
+        rec[R_KHI] = (int)khi;
+        rec[R_PENDING] = NB;
+        rec[R_W] = W;
+        rec[R_SINK_HI] = sink_hi;
+        rec[R_LOCAL_LO] = local_lo;
+        rec[R_LOCAL_HI] = local_hi;
+        *s_bcast = atomicAdd(&ws[H_UNITS], NB * NG);
+        atomicAdd(&ws[H_MAPS], 1);
+        atomicAdd(&ws[H_CANDS], NB);
+    }
+    __threadfence();  // the record before its units: a fused consumer may take a unit as soon as it is listed
+    grp.sync();
+    const int ub = *s_bcast;
+    for (int u = tid; u < NB * NG; u += NTH) st_volatile(ws + HDR + ub + u, (m * CAP + u / NG) * NG + u % NG + 1);
+    return NB;
+}
+
 // The same for one warp holding a map's keys in registers (sel_topk_warp_kernel: block q * 32 + lane in
 // key[q]).  All lanes of the warp.
 template <int IPT>
