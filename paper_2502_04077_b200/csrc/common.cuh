@@ -211,6 +211,29 @@ __device__ __forceinline__ int group_excl_scan(int v, int* smem_warp /*[NT/32+1]
     g.sync();
     return base + x - v;
 }
+// One-barrier form: every thread sums the warp totals before it.  smem_warp must not be rewritten until
+// the group has passed another barrier.
+template <int NT, class G>
+__device__ __forceinline__ int group_excl_scan1(int v, int* smem_warp /*[NT/32]*/, int& total, const G& g) {
+    const int lane = g.tid() & 31, warp = g.tid() >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem_warp[warp] = x;
+    g.sync();
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) {
+        const int t = smem_warp[w];
+        base += w < warp ? t : 0;
+        tot += t;
+    }
+    total = tot;
+    return base + x - v;
+}
 template <int NT>
 __device__ __forceinline__ int block_excl_scan(int v, int* smem_warp /*[NT/32+1]*/, int& total) {
     return group_excl_scan<NT>(v, smem_warp, total, CtaGroup{});

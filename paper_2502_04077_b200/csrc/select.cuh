@@ -212,16 +212,14 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
                         const uint32_t kj = c_key[j];
                         rank += kj > kq || (kj == kq && c_id[j] < iq);
                     }
-                    if (rank < need) atomicOr(&s_mask[iq >> 5], 1u << (iq & 31));  // (s_mask: scratch here)
+                    if (rank < need) atomicOr(&s_mask[iq >> 5], 1u << (iq & 31));
                 }
                 grp.sync();
+                // (the band's chosen ids are already in the mask image; `take` adds the keys above the band)
 #pragma unroll
                 for (int q = 0; q < IPT; ++q)
                     if (key[q] > bhi || ((inband >> q) & 1u && (s_mask[(i0 + q) >> 5] >> ((i0 + q) & 31)) & 1u))
                         take |= 1u << q;
-                grp.sync();  // every band decision read: s_mask is rebuilt from `take` below
-                for (int w = tid; w < words; w += NT) s_mask[w] = 0u;
-                grp.sync();
             } else {
                 // radix select of the k-th largest key, 8 bits per pass, skipping the bytes every unmasked
                 // key shares (they all lie in [kmn, kmx])
@@ -277,7 +275,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
             }
             // ordered emission (ascending ids) and the bitmask image in shared memory
             int total = 0;
-            int pos = group_excl_scan<NT>(__popc(take), scan_tmp, total, grp);
+            int pos = group_excl_scan1<NT>(__popc(take), scan_tmp, total, grp);
             unsigned tmin = 0xffffffffu;
 #pragma unroll
             for (int q = 0; q < IPT; ++q)
