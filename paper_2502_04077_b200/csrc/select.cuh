@@ -7,6 +7,16 @@
 
 namespace ap {
 
+#ifdef AP_SEL_TRACE  // profiling only: clock64 phase stamps of map 0's selection (the last launch)
+__device__ long long g_sel_trace[16];
+extern "C" int ap_debug_sel_trace(long long* host_out) {
+    return cudaMemcpyFromSymbol(host_out, g_sel_trace, 16 * sizeof(long long)) == cudaSuccess ? 0 : 5;
+}
+#define SEL_TRACE(e) if (m == 0 && tid == 0) g_sel_trace[e] = clock64();
+#else
+#define SEL_TRACE(e)
+#endif
+
 // Nested search bands around the previous k-th score tau: half-widths 2^-2, 2^-4, 2^-6, 2^-8 of |tau|
 // (how far the boundary moves between two updates depends on the rows: on the decode engine's maps
 // the 2^-2 band holds the new boundary 99.9% of the time with ~34 keys, on tightly clustered synthetic
@@ -38,8 +48,7 @@ template <int NT, int IPT>
 struct SelSmem {  // shared memory of one map's selection by an NT-thread group
     int hist[256];
     int scan_tmp[NT / 32 + 2];
-    uint32_t c_key[TK_CAND];
-    int c_id[TK_CAND];
+    __align__(16) unsigned long long c_pk[TK_CAND + 2];  // band keys packed (key << 32 | ~id): one compare orders them
     uint32_t mask[NT * IPT / 32 + 1];
     int nan, amax, nmask, cnt, bcast;
     int above[TK_NB], band[TK_NB];  // per search band: keys above it, keys in it
@@ -52,8 +61,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
     static_assert(IPT <= 32 && IPT % 4 == 0, "one take bit per key, 16-byte loads");
     int* hist = sh.hist;
     int* scan_tmp = sh.scan_tmp;
-    uint32_t* c_key = sh.c_key;
-    int* c_id = sh.c_id;
+    unsigned long long* c_pk = sh.c_pk;
     uint32_t* s_mask = sh.mask;
     int &s_nan = sh.nan, &s_amax = sh.amax, &s_nmask = sh.nmask, &s_cnt = sh.cnt, &s_bcast = sh.bcast;
     int* s_above = sh.above;
@@ -74,6 +82,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
 #pragma unroll
         for (int q = 0; q < IPT; ++q) vals[q] = i0 + q < s.w_max ? __ldcg(sc + i0 + q) : -INFINITY;
     }
+    SEL_TRACE(0);
     ap_map_state st = s.state[m];
     const bool update = (st.counter % s.update_interval) == 0;
     const int words = (s.w_max + 31) / 32;
@@ -140,6 +149,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
                 nb[i] += key[q] >= lo_b[i] && key[q] <= hi_b[i];
             }
         grp.sync();  // shared state initialised
+        SEL_TRACE(1);
         // CTA reductions: one shared atomic per warp
         nm = (int)__reduce_add_sync(0xffffffffu, (unsigned)nm);
 #pragma unroll
@@ -163,6 +173,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
             atomicMax(&s_amax, (int)am);
         }
         grp.sync();
+        SEL_TRACE(2);
         if (s_nan) raise_status(s.status, AP_ENUMERIC);
         const int available = W - s_nmask;
         const int kcap = s.k_map ? min(max(s.k_map[m], 0), s.k_mid) : s.k_mid;
@@ -182,6 +193,16 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
                     blo = lo_b[i];
                     bhi = hi_b[i];
                 }
+#ifdef AP_SEL_TRACE
+            if (m == 0 && tid == 0) {
+                g_sel_trace[8] = sel_b;
+                g_sel_trace[9] = band;
+                g_sel_trace[10] = s_band[0];
+                g_sel_trace[11] = s_above[0];
+                g_sel_trace[12] = k;
+                g_sel_trace[13] = s_band[3];
+            }
+#endif
 #ifdef AP_TOPK_STATS
             if (tid == 0) {
                 atomicAdd(&g_topk_stats[0], 1);
@@ -193,25 +214,29 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
             if (sel_b >= 0) {
                 // fast path: the k-th key is in the band; rank the band's keys among themselves
                 const int need = k - above;
+                // gather the band's keys by a scan of the per-thread counts (same-address shared atomics
+                // serialise), packed as key << 32 | ~id so that "ahead in (key desc, index asc)" is one compare
                 uint32_t inband = 0u;
 #pragma unroll
                 for (int q = 0; q < IPT; ++q)
-                    if (key[q] >= blo && key[q] <= bhi) {
-                        const int slot = atomicAdd(&s_cnt, 1);
-                        c_key[slot] = key[q];
-                        c_id[slot] = i0 + q;
-                        inband |= 1u << q;
-                    }
+                    if (key[q] >= blo && key[q] <= bhi) inband |= 1u << q;
+                int tot_b = 0;
+                int slot = group_excl_scan1<NT>(__popc(inband), scan_tmp, tot_b, grp);
+#pragma unroll
+                for (int q = 0; q < IPT; ++q)
+                    if ((inband >> q) & 1u) c_pk[slot++] = (unsigned long long)key[q] << 32 | (uint32_t)~(uint32_t)(i0 + q);
+                if (tid == 0) c_pk[band] = 0ull;  // pad to a pair (0 is behind every real entry)
                 grp.sync();
-                    if (tid < band) {  // one thread per band key: its rank among the band (key desc, index asc)
-                    const uint32_t kq = c_key[tid];
-                    const int iq = c_id[tid];
+                if (tid < band) {  // one thread per band key: how many band keys are ahead of it
+                    const unsigned long long mine = c_pk[tid];
+                    const ulonglong2* pk = reinterpret_cast<const ulonglong2*>(c_pk);
                     int rank = 0;
 #pragma unroll 4
-                    for (int j = 0; j < band; ++j) {
-                        const uint32_t kj = c_key[j];
-                        rank += kj > kq || (kj == kq && c_id[j] < iq);
+                    for (int j = 0; j < (band + 1) / 2; ++j) {
+                        const ulonglong2 v = pk[j];
+                        rank += (v.x > mine) + (v.y > mine);
                     }
+                    const int iq = (int)~(uint32_t)mine;
                     if (rank < need) atomicOr(&s_mask[iq >> 5], 1u << (iq & 31));
                 }
                 grp.sync();
@@ -275,6 +300,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
             }
             // ordered emission (ascending ids) and the bitmask image in shared memory
             int total = 0;
+            SEL_TRACE(3);
             int pos = group_excl_scan1<NT>(__popc(take), scan_tmp, total, grp);
             unsigned tmin = 0xffffffffu;
 #pragma unroll
@@ -306,6 +332,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
         }
         grp.sync();
         for (int w = tid; w < words; w += NT) mask[w] = s_mask[w];
+        SEL_TRACE(4);
         kth = k > 0 ? s_tmin : 0u;
         if (k > 0 && tp.enabled && s.tie_ws)  // (the keys are still in registers: no second read of the row)
             tie_n = tie::detect_regs<NT, IPT>(s, tp, m, key, i0, W, k, kth, __int_as_float(s_amax), sink_hi, local_lo,
@@ -317,6 +344,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
             st.r_width = st.width;
             st.r_wgen = tp.wgen ? *tp.wgen : 0;
             st.tie_n = tie_n;
+            SEL_TRACE(5);
             st.prev_kth = kth;
         }
     } else if (update && s.k_mid <= 0) {
