@@ -85,6 +85,7 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
     SEL_TRACE(0);
     ap_map_state st = s.state[m];
     const bool update = (st.counter % s.update_interval) == 0;
+    SEL_TRACE(6);
     const int words = (s.w_max + 31) / 32;
     uint32_t* mask = s.mid_mask + (int64_t)m * words;
     int32_t* mid = s.mid_blocks + (int64_t)m * (s.k_mid > 0 ? s.k_mid : 1);
@@ -111,25 +112,29 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
         int local_hi = ls < nl ? (int)((nl + b - 1) / b) : 0;
         sink_hi = sink_hi > W ? W : sink_hi;
         local_hi = local_hi > W ? W : local_hi;
+        // this thread's blocks [i0, i0 + IPT) as bit masks: inside the row, and selectable (not sink / local)
+        auto span = [&](int lo, int hi) -> uint32_t {  // bits q with lo <= i0 + q < hi
+            const int a = max(lo - i0, 0), z = min(hi - i0, IPT);
+            if (a >= z) return 0u;
+            const uint32_t upto = z >= 32 ? 0xffffffffu : (1u << z) - 1u;
+            return upto & ~((1u << a) - 1u);
+        };
+        const uint32_t in_row = span(0, W);
+        const uint32_t live = in_row & ~(span(0, sink_hi) | span(local_lo, local_hi));
         uint32_t key[IPT];
         int nm = 0;
         bool nan = false;
         float amax = 0.f;
-        unsigned kmn = 0xffffffffu, kmx = 0u;
 #pragma unroll
         for (int q = 0; q < IPT; ++q) {
-            const int i = i0 + q;
-            const float v = i < W ? vals[q] : -INFINITY;
-            nan |= v != v;
-            const bool masked = i >= W || (i < sink_hi) || (i >= local_lo && i < local_hi);
-            key[q] = masked ? 0u : order_key(v);  // 0 sorts below every real key (and is never taken)
-            nm += i < W && (masked || v == -INFINITY);
-            if (!masked && fabsf(v) <= 3.402823466e38f) amax = fmaxf(amax, fabsf(v));
-            if (key[q]) {
-                kmn = min(kmn, key[q]);
-                kmx = max(kmx, key[q]);
-            }
+            const float v = vals[q];
+            const bool r = (in_row >> q) & 1u, l = (live >> q) & 1u;
+            nan |= r && v != v;
+            key[q] = l ? order_key(v) : 0u;  // 0 sorts below every real key (and is never taken)
+            nm += r && (!l || v == -INFINITY);
+            if (l && fabsf(v) <= 3.402823466e38f) amax = fmaxf(amax, fabsf(v));
         }
+        SEL_TRACE(7);
         uint32_t lo_b[TK_NB], hi_b[TK_NB];  // search bands (empty without a previous boundary)
         const float tau = tie::key_value(kth);
 #pragma unroll
@@ -157,8 +162,6 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
             na[i] = (int)__reduce_add_sync(0xffffffffu, (unsigned)na[i]);
             nb[i] = (int)__reduce_add_sync(0xffffffffu, (unsigned)nb[i]);
         }
-        kmn = __reduce_min_sync(0xffffffffu, kmn);
-        kmx = __reduce_max_sync(0xffffffffu, kmx);
         const unsigned am = __reduce_max_sync(0xffffffffu, __float_as_uint(amax));  // non-negative floats
         if (__any_sync(0xffffffffu, nan) && lane == 0) s_nan = 1;
         if (lane == 0) {
@@ -168,8 +171,6 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
                 if (na[i]) atomicAdd(&s_above[i], na[i]);
                 if (nb[i]) atomicAdd(&s_band[i], nb[i]);
             }
-            atomicMin(&s_kmn, kmn);
-            atomicMax(&s_kmx, kmx);
             atomicMax(&s_amax, (int)am);
         }
         grp.sync();
@@ -247,7 +248,21 @@ __device__ void select_map(const ap_selector& s, const tie::Params& tp, int m, c
                         take |= 1u << q;
             } else {
                 // radix select of the k-th largest key, 8 bits per pass, skipping the bytes every unmasked
-                // key shares (they all lie in [kmn, kmx])
+                // key shares (they all lie in [kmn, kmx], taken here: this path is rare)
+                unsigned kmn = 0xffffffffu, kmx = 0u;
+#pragma unroll
+                for (int q = 0; q < IPT; ++q)
+                    if (key[q]) {
+                        kmn = min(kmn, key[q]);
+                        kmx = max(kmx, key[q]);
+                    }
+                kmn = __reduce_min_sync(0xffffffffu, kmn);
+                kmx = __reduce_max_sync(0xffffffffu, kmx);
+                if (lane == 0) {
+                    atomicMin(&s_kmn, kmn);
+                    atomicMax(&s_kmx, kmx);
+                }
+                grp.sync();
                 kmn = s_kmn;
                 kmx = s_kmx;
                 const int top = (kmn ^ kmx) ? 31 - __clz(kmn ^ kmx) : -1;

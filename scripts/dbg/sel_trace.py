@@ -15,5 +15,5 @@ names = ["entry", "state+init", "keys+reductions", "search", "emit+mask", "detec
 for _ in range(6):
     eng.step(); torch.cuda.synchronize(); L.ap_debug_sel_trace(buf)
     t = list(buf)
-    print("  ".join(f"{names[i]} {t[i] - t[0]}" for i in range(1, 6)),
+    print(f"state {t[6] - t[0]} keys {t[7] - t[0]} ", "  ".join(f"{names[i]} {t[i] - t[0]}" for i in range(1, 6)),
           f"| band idx {t[8]} size {t[9]} (widest {t[10]}, above it {t[11]}, narrowest {t[13]}) k {t[12]}")
