@@ -371,6 +371,10 @@ int ap_argmax_rows(const void* logits, int32_t rows, int64_t n, void* workspace,
                    int64_t* tokens, void* stream);
 /* seq_len[i] += by */
 int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream);
+/* The start of a decode step in one launch: seq_len[i] += by for i < n, and out[s][:] = embed[tokens[s]][:]
+ * (bf16 rows of `hidden` elements, s < n) — ap_advance plus the embedding lookup. */
+int ap_advance_embed(int32_t* seq_len, int32_t n, int32_t by, const void* embed, const int64_t* tokens, void* out,
+                     int32_t hidden, void* stream);
 
 /* Batch-1..4 bf16 GEMV y[s] = W x[s] (W [N][K] row-major, K % 8 == 0, fp32 accumulate), HBM-streaming.
  * rows_per_warp: ignored (ABI slot of an earlier kernel).  flags: bit 0 = RMSNORM prologue (h = x [+ residual], written to residual_out

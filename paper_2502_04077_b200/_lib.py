@@ -135,6 +135,7 @@ SIGNATURES = {
     "ap_rope_append": (ctypes.c_int, [_P, _I32, _I32, _I32, _P, _P, _P, _P, _I32, ctypes.c_float, _P]),
     "ap_silu_mul": (ctypes.c_int, [_P, _P, _I32, _I32, _P]),
     "ap_advance": (ctypes.c_int, [_P, _I32, _I32, _P]),
+    "ap_advance_embed": (ctypes.c_int, [_P, _I32, _I32, _P, _P, _P, _I32, _P]),
     "ap_gemv": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, ctypes.c_float, _P, _P, _P]),
     "ap_gemm_tc_workspace_bytes": (ctypes.c_int64, [_I32, _I32, _I32]),
     "ap_gemm_tc": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, ctypes.c_int64, _P]),

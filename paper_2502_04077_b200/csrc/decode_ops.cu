@@ -160,6 +160,20 @@ __global__ void advance_kernel(int32_t* seq_len, int n, int by) {
     if (i < n) seq_len[i] += by;
 }
 
+// grid (chunks, n): sequence s copies embedding row tokens[s] in 16-byte pieces; CTA (0, s) also advances
+// seq_len[s].  Launched with programmatic dependent launch: the next step's first projection may start
+// streaming its weights while this runs.
+__global__ void advance_embed_kernel(int32_t* seq_len, int by, const uint4* __restrict__ embed,
+                                     const int64_t* __restrict__ tokens, uint4* __restrict__ out, int hidden16) {
+    pdl_trigger();
+    pdl_wait();  // the token comes from the previous step's argmax
+    const int s = blockIdx.y;
+    if (blockIdx.x == 0 && threadIdx.x == 0) seq_len[s] += by;
+    const int64_t tok = tokens[s];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < hidden16; i += gridDim.x * blockDim.x)
+        out[(int64_t)s * hidden16 + i] = embed[tok * hidden16 + i];
+}
+
 }  // namespace ap
 
 using namespace ap;
@@ -216,6 +230,17 @@ int ap_argmax_rows(const void* logits, int32_t rows, int64_t n, void* workspace,
 int ap_advance(int32_t* seq_len, int32_t n, int32_t by, void* stream) {
     advance_kernel<<<(n + 127) / 128, 128, 0, as_stream(stream)>>>(seq_len, n, by);
     return launch_status("ap_advance");
+}
+
+int ap_advance_embed(int32_t* seq_len, int32_t n, int32_t by, const void* embed, const int64_t* tokens, void* out,
+                     int32_t hidden, void* stream) {
+    AP_REQUIRE(seq_len && embed && tokens && out && n >= 1 && n <= 65535, AP_EPARAM, "bad advance_embed operands");
+    AP_REQUIRE(hidden > 0 && hidden % 8 == 0, AP_EPARAM, "hidden must be a multiple of 8 (16-byte rows)");
+    const int hidden16 = hidden / 8;
+    const int chunks = (hidden16 + 127) / 128 < 8 ? (hidden16 + 127) / 128 : 8;
+    launch_ex(advance_embed_kernel, dim3(chunks, n), dim3(128), 0, as_stream(stream), 1, seq_len, by,
+              (const uint4*)embed, tokens, (uint4*)out, hidden16);
+    return launch_status("ap_advance_embed");
 }
 
 }  // extern "C"

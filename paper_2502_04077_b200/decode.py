@@ -393,7 +393,9 @@ class DecodeEngine:
         self._overlap_now = bool(self.overlap) and selector and variant in ("plain", "calib")
         # GEMV / calibration grids leave the reserved SMs to the side-stream selector (captured with the graph)
         _lib.check(_lib.fn("ap_set_sm_reserve")(self.overlap if self._overlap_now else 0), "ap_set_sm_reserve")
-        _lib.check(_lib.fn("ap_advance")(_lib.ptr(self.seq_len), S, 1, s))
+        # seq_len += 1 and the embedding lookup of the previous step's token, one launch
+        _lib.check(_lib.fn("ap_advance_embed")(_lib.ptr(self.seq_len), S, 1, _lib.ptr(self.embed), _lib.ptr(self.tok),
+                                               _lib.ptr(self.r), sh.hidden, s), "ap_advance_embed")
         main = torch.cuda.current_stream()
         if self.voff is not None and variant in ("plain", "calib"):
             # cross-token prefetch: the blocks predicted at the end of the previous token stream in on a
@@ -403,7 +405,6 @@ class DecodeEngine:
                 for l in range(sh.n_layers):
                     self.voff.prefetch(self.sel, l, self.sel_layers * self.maps_per_layer, stream=self.pf_stream)
                     self.pf_events[l].record(self.pf_stream)
-        torch.index_select(self.embed, 0, self.tok, out=self.r)
         for l in range(sh.n_layers):
             self._layer(l, variant)
         if self.voff is not None and variant in ("plain", "calib"):
