@@ -90,3 +90,22 @@ def test_overlapped_selector_equals_end_of_token_step():
         assert torch.equal(eng.sel.mid_blocks, ref.sel.mid_blocks)
         assert torch.equal(eng.logits, ref.logits)
     assert eng.sel.n_maps == TINY.n_layers * 2
+
+
+@pytest.mark.gpu
+def test_advance_embed_equals_advance_and_index_select():
+    """ap_advance_embed (the first launch of a step) == seq_len += by, then embed[tokens] rows."""
+    import torch
+    from paper_2502_04077_b200 import _lib
+    _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    V, Hd, S = 1000, 4096, 3
+    embed = torch.randn(V, Hd, device="cuda", generator=g).to(torch.bfloat16)
+    tok = torch.tensor([7, 999, 0], dtype=torch.int64, device="cuda")
+    seq = torch.tensor([10, 20, 30], dtype=torch.int32, device="cuda")
+    out = torch.zeros(S, Hd, dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.fn("ap_advance_embed")(_lib.ptr(seq), S, 2, _lib.ptr(embed), _lib.ptr(tok), _lib.ptr(out), Hd,
+                                           _lib.stream_handle()), "ap_advance_embed")
+    torch.cuda.synchronize()
+    assert seq.tolist() == [12, 22, 32]
+    assert torch.equal(out, torch.index_select(embed, 0, tok))
